@@ -1,0 +1,741 @@
+// fm_abi.cu — plan construction, launch dispatch and the extern "C" ABI
+// declared in include/fftmorph_b200.h.
+//
+// Host-side bookkeeping restates the reference's plan/range logic:
+//   required_lr            umbra.py:172-174   (here with both data minima removed)
+//   make_plan / ranges     fft_conv.py:80-91, tensor.py:76-101
+//   reflect / negate       morphology.py:147-163 (erosion duality, l' = max f)
+//   crop / _paste          morphology.py:51-62,131-140
+// Kernels: fm_tile.cuh (encode + spatial FFT conv), fm_tonal.cuh (inverse
+// tonal FFT + threshold + degree), fm_naive.cuh (exact direct oracle).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fftmorph_b200.h"
+#include "fm_naive.cuh"
+#include "fm_tile.cuh"
+#include "fm_tonal.cuh"
+
+using namespace fm;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+std::mutex g_tw_mu;
+unsigned long long g_tw_init_mask = 0;  // devices whose c_tw is initialised
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define FM_CUDA(call)                                                               \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(FM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+constexpr double kPi = 3.14159265358979323846;
+
+int ensure_twiddles(int device) {
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  if (device < 64 && (g_tw_init_mask >> device) & 1ull) return FM_OK;
+  std::vector<float2> tw(kTwTotal);
+  const int sizes[5] = {16, 32, 64, 128, 256};
+  const int offs[5] = {0, 16, 48, 112, 240};
+  for (int s = 0; s < 5; ++s)
+    for (int j = 0; j < sizes[s]; ++j) {
+      const double ang = -2.0 * kPi * j / sizes[s];
+      tw[offs[s] + j] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+    }
+  FM_CUDA(cudaMemcpyToSymbol(c_tw, tw.data(), sizeof(float2) * kTwTotal));
+  if (device < 64) g_tw_init_mask |= (1ull << device);
+  return FM_OK;
+}
+
+bool smooth235(int n) {
+  if (n < 1) return false;
+  for (int p : {2, 3, 5})
+    while (n % p == 0) n /= p;
+  return n == 1;
+}
+
+std::vector<int> radix_plan(int n) {
+  std::vector<int> r;
+  while (n % 8 == 0) { r.push_back(8); n /= 8; }
+  while (n % 4 == 0) { r.push_back(4); n /= 4; }
+  while (n % 2 == 0) { r.push_back(2); n /= 2; }
+  while (n % 3 == 0) { r.push_back(3); n /= 3; }
+  while (n % 5 == 0) { r.push_back(5); n /= 5; }
+  return r;
+}
+
+// ---- kernel variants ------------------------------------------------------
+typedef void (*tile_launch_fn)(dim3, size_t, cudaStream_t, const TileArgs&);
+
+template <int PY, int PX, int NT, bool TWO_D, bool SPEC>
+void launch_tile(dim3 grid, size_t smem, cudaStream_t s, const TileArgs& a) {
+  tile_conv_kernel<PY, PX, NT, TWO_D, SPEC><<<grid, NT, smem, s>>>(a);
+}
+
+template <int PY, int PX, int NT, bool TWO_D, bool SPEC>
+cudaError_t set_smem_attr(size_t smem) {
+  return cudaFuncSetAttribute(tile_conv_kernel<PY, PX, NT, TWO_D, SPEC>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+struct Variant {
+  int two_d, py, px, nt;
+  int smem_fixed;
+  tile_launch_fn conv, spec;
+  cudaError_t (*attr_conv)(size_t);
+  cudaError_t (*attr_spec)(size_t);
+};
+
+#define FM_VARIANT(TD, PY, PX, NT)                                                        \
+  Variant {                                                                               \
+    TD, PY, PX, NT, TileCfg<PY, PX, NT, TD>::kSmemFixed, &launch_tile<PY, PX, NT, TD, false>, \
+        &launch_tile<PY, PX, NT, TD, true>, &set_smem_attr<PY, PX, NT, TD, false>,          \
+        &set_smem_attr<PY, PX, NT, TD, true>                                                \
+  }
+
+const Variant kVariants[] = {
+    FM_VARIANT(true, 16, 16, 64),   FM_VARIANT(true, 32, 32, 128), FM_VARIANT(true, 64, 64, 256),
+    FM_VARIANT(true, 128, 128, 512), FM_VARIANT(false, 32, 16, 64),  FM_VARIANT(false, 32, 32, 128),
+    FM_VARIANT(false, 32, 64, 128),  FM_VARIANT(false, 32, 128, 256), FM_VARIANT(false, 32, 256, 256),
+};
+
+int dtype_size(int dt) { return dt == FM_U8 ? 1 : dt == FM_U16 ? 2 : 4; }
+
+constexpr int kSmemLimit = 227 * 1024;
+constexpr int kTabBudget = 48 * 1024;
+
+}  // namespace
+
+struct fm_plan {
+  fm_plan_desc d{};
+  int device = 0;
+  bool two_d = true;
+  int64_t H = 1, W = 1, batch = 1;
+  int my = 1, mx = 1;
+  int64_t lo_y = 0, lo_x = 0;  // lo of the SE actually convolved (reflected for erosion)
+  int se_min = 0, se_max = 0, se_count = 0;
+  int lr = 0, T = 0, N = 0, K = 0;
+  std::vector<int> radix;
+  const Variant* var = nullptr;
+  int PY = 1, PX = 16, QY = 1, QX = 1, tiles_y = 1, tiles_x = 1, tiles_total = 1, tile_ctas = 1;
+  int DY = 0, DX = 0;
+  int64_t OH = 1, OW = 1, off_y = 0, off_x = 0;
+  int k_chunk = 1, kchunks = 1;
+  int64_t ipc = 1;  // images per launch
+  int copies = 16;
+  size_t conv_smem = 0, tonal_smem = 0;
+  int tonal_threads = 128, tonal_stride = 1;
+  int enc_sign = 1, enc_bias = 0, vmax = 0;
+  int out_sign = 1, out_bias = 0;
+  // device buffers
+  float2* spec = nullptr;
+  float2* tabT = nullptr;
+  float2* twN = nullptr;
+  float2* wT = nullptr;
+  float2* chat = nullptr;
+  int* stats = nullptr;  // [0] = deviation bits, [1] = value error
+  int32_t* se_vals_d = nullptr;
+  uint8_t* se_def_d = nullptr;
+  // host-buffer path staging
+  void* h_img = nullptr;
+  uint8_t* h_def = nullptr;
+  int32_t* h_out = nullptr;
+  uint8_t* h_valid = nullptr;
+  cudaStream_t last_stream = nullptr;
+  // event timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;                  // reusable events
+  std::vector<std::pair<int, int>> pending_conv, pending_tonal;  // (start, stop) indices into ev_pool
+  size_t ev_next = 0;
+  fm_timing acc{};
+  double conv_bytes_per_img = 0, tonal_bytes_per_img = 0, conv_flops_per_img = 0;
+};
+
+namespace {
+
+void free_plan(fm_plan* p) {
+  if (!p) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  cudaFree(p->spec);
+  cudaFree(p->tabT);
+  cudaFree(p->twN);
+  cudaFree(p->wT);
+  cudaFree(p->chat);
+  cudaFree(p->stats);
+  cudaFree(p->se_vals_d);
+  cudaFree(p->se_def_d);
+  cudaFree(p->h_img);
+  cudaFree(p->h_def);
+  cudaFree(p->h_out);
+  cudaFree(p->h_valid);
+  for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+  cudaSetDevice(prev);
+  delete p;
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+cudaEvent_t next_event(fm_plan* p) {
+  if (p->ev_next == p->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    p->ev_pool.push_back(e);
+  }
+  return p->ev_pool[p->ev_next++];
+}
+
+int validate_common(const fm_plan_desc* d) {
+  if (!d) return fail(FM_EINVAL, "null descriptor");
+  if (d->ndim != 1 && d->ndim != 2) return fail(FM_EUNSUPPORTED, "only 1-D signals and 2-D images are supported");
+  if (d->mode != FM_DILATE && d->mode != FM_ERODE) return fail(FM_EINVAL, "mode must be FM_DILATE or FM_ERODE");
+  if (d->img_dtype < FM_U8 || d->img_dtype > FM_I32) return fail(FM_EINVAL, "bad image dtype");
+  if (d->batch < 1) return fail(FM_EINVAL, "batch must be >= 1");
+  for (int i = 0; i < d->ndim; ++i) {
+    if (d->shape[i] < 1) return fail(FM_EINVAL, "empty grid");
+    if (d->se_shape[i] < 1) return fail(FM_EINVAL, "empty structuring element");
+    if (d->shape[i] > (1 << 30) || d->se_shape[i] > (1 << 30)) return fail(FM_EUNSUPPORTED, "extent too large");
+  }
+  return FM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fm_abi_version(void) { return FM_ABI_VERSION; }
+const char* fm_last_error(void) { return g_err.c_str(); }
+int64_t fm_kernel_launches(void) { return (int64_t)g_launches.load(); }
+
+int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* se_values,
+                   const uint8_t* se_defined) {
+  if (!out_plan) return fail(FM_EINVAL, "null plan pointer");
+  *out_plan = nullptr;
+  int rc = validate_common(desc);
+  if (rc) return rc;
+  if (!se_values) return fail(FM_EINVAL, "null SE values");
+  const fm_plan_desc& d = *desc;
+  if (d.img_min > d.img_max) return fail(FM_EINVAL, "img_min > img_max");
+
+  fm_plan* p = new fm_plan();
+  p->d = d;
+  p->device = d.device;
+  p->two_d = d.ndim == 2;
+  p->batch = d.batch;
+  if (p->two_d) {
+    p->H = d.shape[0];
+    p->W = d.shape[1];
+    p->my = (int)d.se_shape[0];
+    p->mx = (int)d.se_shape[1];
+  } else {
+    p->H = 1;
+    p->W = d.shape[0];
+    p->my = 1;
+    p->mx = (int)d.se_shape[0];
+  }
+  const int64_t se_n = (int64_t)p->my * p->mx;
+  // SE as convolved: reflected for erosion (reflect(b), morphology.py:147-152)
+  std::vector<int32_t> sv(se_n);
+  std::vector<uint8_t> sd(se_n);
+  for (int64_t i = 0; i < se_n; ++i) {
+    const int64_t src = (d.mode == FM_ERODE) ? (se_n - 1 - i) : i;
+    sv[i] = se_values[src];
+    sd[i] = se_defined ? (se_defined[src] ? 1 : 0) : 1;
+  }
+  int64_t lo_y = p->two_d ? d.se_lo[0] : 0, lo_x = p->two_d ? d.se_lo[1] : d.se_lo[0];
+  if (d.mode == FM_ERODE) {
+    lo_y = -(lo_y + p->my - 1);
+    lo_x = -(lo_x + p->mx - 1);
+  }
+  p->lo_y = lo_y;
+  p->lo_x = lo_x;
+  int smin = INT32_MAX, smax = INT32_MIN, cnt = 0;
+  for (int64_t i = 0; i < se_n; ++i)
+    if (sd[i]) {
+      smin = std::min(smin, sv[i]);
+      smax = std::max(smax, sv[i]);
+      ++cnt;
+    }
+  if (cnt == 0) { free_plan(p); return fail(FM_EINVAL, "grid needs at least one defined pixel"); }
+  if (smin < 0) { free_plan(p); return fail(FM_EINVAL, "tonal lift needs non-negative values"); }
+  p->se_min = smin;
+  p->se_max = smax;
+  p->se_count = cnt;
+
+  // tonal extent: only the spread of values matters (dilation commutes with
+  // constant shifts of f and b); l_R of the reference is max f + max b.
+  const int64_t lr64 = (int64_t)(d.img_max - d.img_min) + (smax - smin);
+  if (lr64 > 100000) { free_plan(p); return fail(FM_EUNSUPPORTED, "tonal range too large for the FFT path"); }
+  p->lr = (int)lr64;
+  // encode / decode
+  if (d.mode == FM_DILATE) {
+    p->enc_sign = 1;
+    p->enc_bias = -d.img_min;
+    p->out_sign = 1;
+    p->out_bias = d.img_min + smin;
+  } else {
+    p->enc_sign = -1;
+    p->enc_bias = d.img_max;
+    p->out_sign = -1;
+    p->out_bias = d.img_max - smin;
+  }
+  p->vmax = d.img_max - d.img_min;
+
+  // tonal length: even, > l_R, with T/2 5-smooth
+  int T = d.tonal_len;
+  if (T > 0) {
+    if (T % 2 || T < p->lr + 1 || !smooth235(T / 2)) {
+      free_plan(p);
+      return fail(FM_EINVAL, "forced tonal_len must be even, > l_R and have a 2-3-5-smooth half");
+    }
+  } else {
+    T = std::max(2, p->lr + 1);
+    if (T % 2) ++T;
+    while (!smooth235(T / 2)) T += 2;
+  }
+  p->T = T;
+  p->N = T / 2;
+  p->K = p->N + 1;
+  p->radix = radix_plan(p->N);
+  if (p->radix.size() > 12) { free_plan(p); return fail(FM_EUNSUPPORTED, "tonal radix plan too deep"); }
+
+  // output region and overlap-save offsets (tensor.py:76-101, morphology.py:131-140)
+  const int64_t hi_y = lo_y + p->my - 1, hi_x = lo_x + p->mx - 1;
+  if (d.crop) {
+    p->off_y = 0;
+    p->off_x = 0;
+    p->OH = p->H;
+    p->OW = p->W;
+  } else {
+    p->off_y = p->two_d ? lo_y : 0;
+    p->off_x = lo_x;
+    p->OH = p->two_d ? p->H + p->my - 1 : 1;
+    p->OW = p->W + p->mx - 1;
+  }
+  const int64_t DY = p->off_y - hi_y, DX = p->off_x - hi_x;
+  if (DY < -(1 << 30) || DY > (1 << 30) || DX < -(1 << 30) || DX > (1 << 30)) {
+    free_plan(p);
+    return fail(FM_EUNSUPPORTED, "SE offset too large");
+  }
+  p->DY = p->two_d ? (int)DY : 0;
+  p->DX = (int)DX;
+
+  // tile choice: minimise tiles * P^2 * (log2 P^2 + 2) over the built variants
+  double best = 1e300;
+  const Variant* bv = nullptr;
+  for (const Variant& v : kVariants) {
+    if ((bool)v.two_d != p->two_d) continue;
+    const int P = v.px;
+    if (d.tile > 0 && d.tile != P) continue;
+    if (P < p->mx || (p->two_d && P < p->my)) continue;
+    const int qx = P - p->mx + 1, qy = p->two_d ? P - p->my + 1 : 1;
+    const double tx = std::ceil((double)p->OW / qx), ty = p->two_d ? std::ceil((double)p->OH / qy) : 1.0;
+    const double pts = p->two_d ? (double)P * P : (double)P;
+    const double cost = tx * ty * pts * (std::log2(pts) + 2.0) + tx * ty * 2048.0;
+    if (cost < best) {
+      best = cost;
+      bv = &v;
+    }
+  }
+  if (!bv) {
+    free_plan(p);
+    return fail(FM_EUNSUPPORTED, "structuring element larger than the largest FFT tile (" +
+                                     std::string(p->two_d ? "128x128" : "256") + ")");
+  }
+  p->var = bv;
+  p->PY = bv->py;
+  p->PX = bv->px;
+  p->QX = p->PX - p->mx + 1;
+  p->QY = p->two_d ? p->PY - p->my + 1 : 1;
+  p->tiles_x = (int)((p->OW + p->QX - 1) / p->QX);
+  p->tiles_y = p->two_d ? (int)((p->OH + p->QY - 1) / p->QY) : 1;
+  p->tiles_total = p->tiles_x * p->tiles_y;
+  p->tile_ctas = p->two_d ? p->tiles_total : (p->tiles_total + p->PY - 1) / p->PY;
+
+  // tonal-table replication and shared memory
+  int copies = 16;
+  while (copies > 1 && (size_t)T * copies * 8 > kTabBudget) copies >>= 1;
+  while (copies > 1 && bv->smem_fixed + (size_t)T * copies * 8 > kSmemLimit) copies >>= 1;
+  p->copies = copies;
+  p->conv_smem = bv->smem_fixed + (size_t)T * copies * 8;
+  if (p->conv_smem > kSmemLimit) { free_plan(p); return fail(FM_EUNSUPPORTED, "tonal length too large for shared memory"); }
+
+  // tonal kernel geometry
+  p->tonal_stride = (p->N + 1) | 1;
+  int nt = 128;
+  while (nt > 32 && (size_t)(2 * p->N + 2 * (size_t)nt * p->tonal_stride) * 8 > 200 * 1024) nt -= 32;
+  p->tonal_threads = nt;
+  p->tonal_smem = (size_t)(2 * p->N + 2 * (size_t)nt * p->tonal_stride) * 8;
+  if (p->tonal_smem > kSmemLimit) { free_plan(p); return fail(FM_EUNSUPPORTED, "tonal length too large for the tonal kernel"); }
+
+  // spectral scratch and launch chunking
+  const int64_t per_img = (int64_t)p->K * p->OH * p->OW * 8;
+  const int64_t budget = d.scratch_bytes > 0 ? d.scratch_bytes : (int64_t)4 << 30;
+  p->ipc = std::max<int64_t>(1, std::min<int64_t>(p->batch, budget / std::max<int64_t>(per_img, 1)));
+  const int occ = p->two_d ? std::max(1, (kSmemLimit) / (int)(p->conv_smem + 1024)) : 2;
+  const int64_t target = 148LL * 2 * occ;
+  const int64_t base = (int64_t)p->tile_ctas * p->ipc;
+  int kch = (int)std::min<int64_t>(p->K, std::max<int64_t>(1, (target + base - 1) / base));
+  p->k_chunk = (p->K + kch - 1) / kch;
+  p->kchunks = (p->K + p->k_chunk - 1) / p->k_chunk;
+
+  {
+    const double npx = (double)p->OH * p->OW;
+    const double in_b = (double)p->H * p->W * dtype_size(d.img_dtype);
+    p->conv_bytes_per_img = in_b + (double)p->K * npx * 8.0;
+    p->tonal_bytes_per_img = (double)p->K * npx * 8.0 + npx * 4.0;
+    const double pts = p->two_d ? (double)p->PY * p->PX : (double)p->PX;
+    p->conv_flops_per_img = (double)p->tiles_total * p->K * (2.0 * 5.0 * pts * std::log2(pts) + 6.0 * pts);
+  }
+  DeviceGuard dg(p->device);
+  rc = ensure_twiddles(p->device);
+  if (rc) { free_plan(p); return rc; }
+  auto cfail = [&](cudaError_t e, const char* what) {
+    free_plan(p);
+    return fail(FM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  cudaError_t e;
+  if ((e = bv->attr_conv(p->conv_smem)) != cudaSuccess) return cfail(e, "conv smem attribute");
+  if ((e = bv->attr_spec(p->conv_smem)) != cudaSuccess) return cfail(e, "spec smem attribute");
+  if ((e = cudaFuncSetAttribute(tonal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tonal_smem)) != cudaSuccess)
+    return cfail(e, "tonal smem attribute");
+
+  const size_t npts = (size_t)p->PY * p->PX;
+  if ((e = cudaMalloc(&p->spec, sizeof(float2) * npts * p->K)) != cudaSuccess) return cfail(e, "spec alloc");
+  if ((e = cudaMalloc(&p->tabT, sizeof(float2) * T)) != cudaSuccess) return cfail(e, "table alloc");
+  if ((e = cudaMalloc(&p->twN, sizeof(float2) * std::max(1, p->N))) != cudaSuccess) return cfail(e, "table alloc");
+  if ((e = cudaMalloc(&p->wT, sizeof(float2) * std::max(1, p->N))) != cudaSuccess) return cfail(e, "table alloc");
+  if ((e = cudaMalloc(&p->stats, sizeof(int) * 4)) != cudaSuccess) return cfail(e, "stats alloc");
+  if ((e = cudaMalloc(&p->se_vals_d, sizeof(int32_t) * se_n)) != cudaSuccess) return cfail(e, "se alloc");
+  if ((e = cudaMalloc(&p->se_def_d, se_n)) != cudaSuccess) return cfail(e, "se alloc");
+  if ((e = cudaMalloc(&p->chat, (size_t)per_img * p->ipc)) != cudaSuccess) {
+    free_plan(p);
+    return fail(FM_ENOMEM, std::string("spectral scratch alloc: ") + cudaGetErrorString(e));
+  }
+  std::vector<float2> h(T);
+  for (int r = 0; r < T; ++r) {
+    const double ang = -2.0 * kPi * r / T;
+    h[r] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+  cudaMemcpy(p->tabT, h.data(), sizeof(float2) * T, cudaMemcpyHostToDevice);
+  std::vector<float2> tn(std::max(1, p->N)), wt(std::max(1, p->N));
+  for (int j = 0; j < p->N; ++j) {
+    const double a1 = 2.0 * kPi * j / p->N, a2 = 2.0 * kPi * j / T;
+    tn[j] = make_float2((float)std::cos(a1), (float)std::sin(a1));
+    wt[j] = make_float2((float)std::cos(a2), (float)std::sin(a2));
+  }
+  cudaMemcpy(p->twN, tn.data(), sizeof(float2) * tn.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->wT, wt.data(), sizeof(float2) * wt.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(p->se_vals_d, sv.data(), sizeof(int32_t) * se_n, cudaMemcpyHostToDevice);
+  cudaMemcpy(p->se_def_d, sd.data(), se_n, cudaMemcpyHostToDevice);
+  cudaMemset(p->stats, 0, sizeof(int) * 4);
+
+  // SE spectrum: same encode + forward passes as the image tiles, scaled by
+  // 1/(PY_eff * PX * T) so the inverse transforms need no normalisation.
+  TileArgs a{};
+  a.se_vals = p->se_vals_d;
+  a.se_def = p->se_def_d;
+  a.H = 1;
+  a.W = 1;
+  a.my = p->my;
+  a.mx = p->mx;
+  a.T = T;
+  a.K = p->K;
+  a.magicT = (uint32_t)((1ull << 32) / (uint64_t)T);
+  a.k_chunk = 1;
+  a.enc_sign = 1;
+  a.enc_bias = -smin;
+  a.vmax = 1 << 30;
+  a.copies = copies;
+  a.tabT = p->tabT;
+  a.spec = p->spec;
+  a.spec_out = p->spec;
+  a.spec_scale = (float)(1.0 / ((double)(p->two_d ? p->PY : 1) * p->PX * T));
+  a.tiles_x = 1;
+  a.tiles_total = 1;
+  a.err = p->stats + 1;
+  bv->spec(dim3(1, p->K, 1), p->conv_smem, 0, a);
+  g_launches++;
+  if ((e = cudaGetLastError()) != cudaSuccess) return cfail(e, "SE spectrum launch");
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cfail(e, "SE spectrum");
+  *out_plan = p;
+  return FM_OK;
+}
+
+int fm_plan_query(const fm_plan* p, fm_plan_info* info) {
+  if (!p || !info) return fail(FM_EINVAL, "null argument");
+  std::memset(info, 0, sizeof(*info));
+  info->tonal_len = p->T;
+  info->planes = p->K;
+  info->l_r = p->lr;
+  info->tile_y = p->two_d ? p->PY : 1;
+  info->tile_x = p->PX;
+  info->valid_y = p->QY;
+  info->valid_x = p->QX;
+  info->tiles_y = p->tiles_y;
+  info->tiles_x = p->tiles_x;
+  info->k_chunk = p->k_chunk;
+  info->out_shape[0] = p->two_d ? p->OH : p->OW;
+  info->out_shape[1] = p->two_d ? p->OW : 0;
+  info->out_lo_offset[0] = p->two_d ? p->off_y : p->off_x;
+  info->out_lo_offset[1] = p->two_d ? p->off_x : 0;
+  info->images_per_launch = p->ipc;
+  info->scratch_bytes = (int64_t)p->K * p->OH * p->OW * 8 * p->ipc;
+  info->se_min = p->se_min;
+  info->se_max = p->se_max;
+  info->se_count = p->se_count;
+  return FM_OK;
+}
+
+int fm_reset_stats(fm_plan* p, void* stream) {
+  if (!p) return fail(FM_EINVAL, "null plan");
+  DeviceGuard dg(p->device);
+  FM_CUDA(cudaMemsetAsync(p->stats, 0, sizeof(int) * 4, (cudaStream_t)stream));
+  return FM_OK;
+}
+
+int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t* out, uint8_t* valid,
+               void* stream) {
+  if (!p || !img || !out) return fail(FM_EINVAL, "null argument");
+  DeviceGuard dg(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  p->last_stream = s;
+  const int64_t npix = p->OH * p->OW;
+  const int64_t img_elems = p->H * p->W;
+  const int dsz = dtype_size(p->d.img_dtype);
+  for (int64_t c0 = 0; c0 < p->batch; c0 += p->ipc) {
+    const int n = (int)std::min<int64_t>(p->ipc, p->batch - c0);
+    TileArgs a{};
+    a.img = reinterpret_cast<const char*>(img) + (size_t)c0 * img_elems * dsz;
+    a.img_def = img_defined ? img_defined + (size_t)c0 * img_elems : nullptr;
+    a.img_dtype = p->d.img_dtype;
+    a.H = (int)p->H;
+    a.W = (int)p->W;
+    a.OH = (int)p->OH;
+    a.OW = (int)p->OW;
+    a.DY = p->DY;
+    a.DX = p->DX;
+    a.QY = p->QY;
+    a.QX = p->QX;
+    a.my = p->my;
+    a.mx = p->mx;
+    a.tiles_x = p->tiles_x;
+    a.tiles_total = p->tiles_total;
+    a.T = p->T;
+    a.K = p->K;
+    a.magicT = (uint32_t)((1ull << 32) / (uint64_t)p->T);
+    a.k_chunk = p->k_chunk;
+    a.enc_sign = p->enc_sign;
+    a.enc_bias = p->enc_bias;
+    a.vmax = p->vmax;
+    a.copies = p->copies;
+    a.tabT = p->tabT;
+    a.spec = p->spec;
+    a.chat = p->chat;
+    a.err = p->stats + 1;
+    int e0 = -1;
+    if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
+    p->var->conv(dim3(p->tile_ctas, p->kchunks, n), p->conv_smem, s, a);
+    g_launches++;
+    FM_CUDA(cudaGetLastError());
+    if (p->timing) {
+      FM_CUDA(cudaEventRecord(next_event(p), s));
+      p->pending_conv.push_back({e0, e0 + 1});
+      p->acc.conv_bytes += p->conv_bytes_per_img * n;
+      p->acc.conv_flops += p->conv_flops_per_img * n;
+    }
+
+    TonalArgs t{};
+    t.chat = p->chat;
+    t.npix = npix;
+    t.K = p->K;
+    t.N = p->N;
+    t.T = p->T;
+    t.nstages = (int)p->radix.size();
+    for (size_t i = 0; i < p->radix.size(); ++i) t.radix[i] = p->radix[i];
+    t.twN = p->twN;
+    t.wT = p->wT;
+    t.out = out + (size_t)c0 * npix;
+    t.valid = valid ? valid + (size_t)c0 * npix : nullptr;
+    t.out_sign = p->out_sign;
+    t.out_bias = p->out_bias;
+    t.fill = p->d.fill;
+    t.stride = p->tonal_stride;
+    t.dev_max = reinterpret_cast<float*>(p->stats);
+    const int nt = p->tonal_threads;
+    int e1 = -1;
+    if (p->timing) { e1 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
+    tonal_kernel<<<dim3((unsigned)((npix + nt - 1) / nt), n), nt, p->tonal_smem, s>>>(t);
+    g_launches++;
+    FM_CUDA(cudaGetLastError());
+    if (p->timing) {
+      FM_CUDA(cudaEventRecord(next_event(p), s));
+      p->pending_tonal.push_back({e1, e1 + 1});
+      p->acc.tonal_bytes += (p->tonal_bytes_per_img + (valid ? (double)npix : 0.0)) * n;
+    }
+  }
+  return FM_OK;
+}
+
+int fm_set_timing(fm_plan* p, int enable) {
+  if (!p) return fail(FM_EINVAL, "null plan");
+  p->timing = enable != 0;
+  return FM_OK;
+}
+
+int fm_get_timing(fm_plan* p, fm_timing* out, int reset) {
+  if (!p) return fail(FM_EINVAL, "null plan");
+  DeviceGuard dg(p->device);
+  FM_CUDA(cudaStreamSynchronize(p->last_stream));
+  FM_CUDA(cudaDeviceSynchronize());
+  for (auto& pr : p->pending_conv) {
+    float ms = 0.f;
+    FM_CUDA(cudaEventElapsedTime(&ms, p->ev_pool[pr.first], p->ev_pool[pr.second]));
+    p->acc.conv_ms += ms;
+    p->acc.conv_launches++;
+  }
+  for (auto& pr : p->pending_tonal) {
+    float ms = 0.f;
+    FM_CUDA(cudaEventElapsedTime(&ms, p->ev_pool[pr.first], p->ev_pool[pr.second]));
+    p->acc.tonal_ms += ms;
+    p->acc.tonal_launches++;
+  }
+  p->pending_conv.clear();
+  p->pending_tonal.clear();
+  p->ev_next = 0;
+  if (out) *out = p->acc;
+  if (reset) p->acc = fm_timing{};
+  return FM_OK;
+}
+
+int fm_read_stats(fm_plan* p, fm_stats* st) {
+  if (!p) return fail(FM_EINVAL, "null plan");
+  DeviceGuard dg(p->device);
+  FM_CUDA(cudaStreamSynchronize(p->last_stream));
+  int h[2] = {0, 0};
+  FM_CUDA(cudaMemcpy(h, p->stats, sizeof(int) * 2, cudaMemcpyDeviceToHost));
+  float dev;
+  std::memcpy(&dev, &h[0], sizeof(float));
+  if (st) {
+    st->max_abs_deviation = dev;
+    st->value_error = h[1];
+  }
+  if (h[1]) return fail(FM_EINVAL, "image value outside the plan's [img_min, img_max] range");
+  if (dev >= 0.25f) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "pre-rounding deviation %.3g >= 0.25; precision budget logic is broken", dev);
+    return fail(FM_EDEVIATION, buf);
+  }
+  return FM_OK;
+}
+
+int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, int32_t* out_host,
+                    uint8_t* valid_host, void* stream) {
+  if (!p || !img_host || !out_host) return fail(FM_EINVAL, "null argument");
+  DeviceGuard dg(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t in_n = (size_t)p->batch * p->H * p->W;
+  const size_t out_n = (size_t)p->batch * p->OH * p->OW;
+  const size_t dsz = dtype_size(p->d.img_dtype);
+  if (!p->h_img) {
+    FM_CUDA(cudaMalloc(&p->h_img, in_n * dsz));
+    FM_CUDA(cudaMalloc(&p->h_def, in_n));
+    FM_CUDA(cudaMalloc(&p->h_out, out_n * sizeof(int32_t)));
+    FM_CUDA(cudaMalloc(&p->h_valid, out_n));
+  }
+  FM_CUDA(cudaMemcpyAsync(p->h_img, img_host, in_n * dsz, cudaMemcpyHostToDevice, s));
+  if (def_host) FM_CUDA(cudaMemcpyAsync(p->h_def, def_host, in_n, cudaMemcpyHostToDevice, s));
+  int rc = fm_execute(p, p->h_img, def_host ? p->h_def : nullptr, p->h_out, valid_host ? p->h_valid : nullptr, stream);
+  if (rc) return rc;
+  FM_CUDA(cudaMemcpyAsync(out_host, p->h_out, out_n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (valid_host) FM_CUDA(cudaMemcpyAsync(valid_host, p->h_valid, out_n, cudaMemcpyDeviceToHost, s));
+  FM_CUDA(cudaStreamSynchronize(s));
+  return FM_OK;
+}
+
+void fm_plan_destroy(fm_plan* p) { free_plan(p); }
+
+int fm_naive(const fm_plan_desc* desc, const int32_t* se_values, const uint8_t* se_defined, const void* img,
+             const uint8_t* img_defined, int32_t* out, uint8_t* valid, void* stream) {
+  int rc = validate_common(desc);
+  if (rc) return rc;
+  if (!se_values || !img || !out) return fail(FM_EINVAL, "null argument");
+  const fm_plan_desc& d = *desc;
+  const bool two_d = d.ndim == 2;
+  const int64_t H = two_d ? d.shape[0] : 1, W = two_d ? d.shape[1] : d.shape[0];
+  const int64_t my = two_d ? d.se_shape[0] : 1, mx = two_d ? d.se_shape[1] : d.se_shape[0];
+  const int64_t lo_y = two_d ? d.se_lo[0] : 0, lo_x = two_d ? d.se_lo[1] : d.se_lo[0];
+  std::vector<int4> ent;
+  for (int64_t jy = 0; jy < my; ++jy)
+    for (int64_t jx = 0; jx < mx; ++jx) {
+      const int64_t i = jy * mx + jx;
+      if (se_defined && !se_defined[i]) continue;
+      ent.push_back(make_int4((int)jy, (int)jx, se_values[i], 0));
+    }
+  if (ent.empty()) return fail(FM_EINVAL, "grid needs at least one defined pixel");
+  const bool erode = d.mode == FM_ERODE;
+  // output ranges: dilate_naive (tensor.py:76-89) / erode_naive (morphology.py:92-93)
+  int64_t off_y = 0, off_x = 0, OH = H, OW = W;
+  if (!d.crop) {
+    off_y = two_d ? (erode ? -(lo_y + my - 1) : lo_y) : 0;
+    off_x = erode ? -(lo_x + mx - 1) : lo_x;
+    OH = two_d ? H + my - 1 : 1;
+    OW = W + mx - 1;
+  }
+  NaiveArgs a{};
+  a.img = img;
+  a.img_def = img_defined;
+  a.img_dtype = d.img_dtype;
+  a.H = (int)H;
+  a.W = (int)W;
+  a.OH = (int)OH;
+  a.OW = (int)OW;
+  // dilation: i = a + (off - lo) - j ; erosion: i = a + (off + lo) + j
+  a.CY = (int)(erode ? off_y + lo_y : off_y - lo_y);
+  a.CX = (int)(erode ? off_x + lo_x : off_x - lo_x);
+  if (!two_d) a.CY = 0;
+  a.erode = erode ? 1 : 0;
+  a.nent = (int)ent.size();
+  a.fill = d.fill;
+  a.out = out;
+  a.valid = valid;
+  DeviceGuard dg(d.device);
+  int4* dent = nullptr;
+  FM_CUDA(cudaMalloc(&dent, sizeof(int4) * ent.size()));
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(dent, ent.data(), sizeof(int4) * ent.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    a.ent = dent;
+    naive_kernel<<<dim3((unsigned)((OW + 31) / 32), (unsigned)((OH + 7) / 8), (unsigned)d.batch), 256, 0, s>>>(a);
+    g_launches++;
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  }
+  cudaFree(dent);
+  if (e != cudaSuccess) return fail(FM_ECUDA, std::string("naive kernel: ") + cudaGetErrorString(e));
+  return FM_OK;
+}
+
+}  // extern "C"

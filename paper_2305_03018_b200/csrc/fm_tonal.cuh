@@ -1,0 +1,119 @@
+// fm_tonal.cuh — per-pixel inverse tonal transform fused with the threshold
+// and the highest-nonzero-degree reduction (Step 3 of the paper).
+//
+// Replaces irfftn's tonal axis + slice + rint + deviation check
+// (fft_conv.py:139-149) and project_with_validity (umbra.py:189-205) + the
+// erosion duality store (morphology.py:175-180): for every output pixel the
+// K = T/2+1 complex spectral values Chat[k] (already scaled by 1/T) are turned
+// into the T real counts c(t) with a half-length complex inverse FFT
+// (c2r packing), then
+//     value = max{ t : c(t) > 0.5 }   (np.rint(c) >= 1, umbra.py:198)
+//     valid = any t with c(t) > 0.5   (has_any, umbra.py:199)
+// and out = valid ? out_sign*value + out_bias : fill.  max|c - rint(c)| is
+// reduced block-wide and atomically into the plan's deviation slot.
+#pragma once
+#include "fm_dft.cuh"
+
+namespace fm {
+
+struct TonalArgs {
+  const float2* chat;  // [imgs][K][npix]
+  int64_t npix;        // OH*OW
+  int K, N, T;         // N = T/2
+  int nstages;
+  int radix[12];
+  const float2* twN;   // [N] exp(+2 pi i j / N)
+  const float2* wT;    // [N] exp(+2 pi i k / T)
+  int32_t* out;        // [imgs][npix]
+  uint8_t* valid;      // nullable
+  int out_sign, out_bias, fill;
+  int stride;          // per-pixel smem stride (float2), odd
+  float* dev_max;      // max |c - rint c| (float bits, atomicMax as int)
+};
+
+template <int R>
+__device__ __forceinline__ void stockham_stage(const float2* in, float2* out, int N, int Ns,
+                                               const float2* twN) {
+  const int M = N / R;
+  const int tstep = N / (Ns * R);
+  for (int j = 0; j < M; ++j) {
+    float2 v[R];
+    const int jm = j % Ns;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = in[j + r * M];
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], twN[(jm * r * tstep) % N]);
+    }
+    dft<R, true>(v);
+    const int idxD = (j / Ns) * Ns * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[idxD + r * Ns] = v[r];
+  }
+}
+
+__global__ void __launch_bounds__(128) tonal_kernel(const TonalArgs a) {
+  extern __shared__ __align__(16) float2 tsm[];
+  const int N = a.N;
+  float2* twN = tsm;
+  float2* wT = tsm + N;
+  float2* bufA = tsm + 2 * N;
+  float2* bufB = bufA + (size_t)blockDim.x * a.stride;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    twN[i] = a.twN[i];
+    wT[i] = a.wT[i];
+  }
+  __syncthreads();
+
+  const int img = blockIdx.y;
+  const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float dev = 0.f;
+  if (pix < a.npix) {
+    const float2* src = a.chat + (size_t)img * a.K * a.npix + pix;
+    float2* A = bufA + (size_t)threadIdx.x * a.stride;
+    float2* B = bufB + (size_t)threadIdx.x * a.stride;
+    for (int k = 0; k <= N; ++k) A[k] = __ldcs(src + (size_t)k * a.npix);
+    // c2r packing: Z[k] = (X[k] + X[N-k]^*) + i w_T^{-k}... so that the
+    // unnormalised length-N inverse DFT of Z gives z[n] = c(2n) + i c(2n+1).
+    for (int k = 0; k < N; ++k) {
+      const float2 xk = A[k];
+      const float2 xc = conjf2(A[N - k]);
+      const float2 s = cadd(xk, xc);
+      const float2 d = csub(xk, xc);
+      B[k] = cadd(s, mul_pi(cmul(wT[k], d)));
+    }
+    float2* in = B;
+    float2* outb = A;
+    int Ns = 1;
+    for (int st = 0; st < a.nstages; ++st) {
+      const int R = a.radix[st];
+      switch (R) {
+        case 2: stockham_stage<2>(in, outb, N, Ns, twN); break;
+        case 3: stockham_stage<3>(in, outb, N, Ns, twN); break;
+        case 4: stockham_stage<4>(in, outb, N, Ns, twN); break;
+        case 5: stockham_stage<5>(in, outb, N, Ns, twN); break;
+        default: stockham_stage<8>(in, outb, N, Ns, twN); break;
+      }
+      Ns *= R;
+      float2* t = in;
+      in = outb;
+      outb = t;
+    }
+    int top = -1;
+    for (int n = 0; n < N; ++n) {
+      const float2 z = in[n];
+      dev = fmaxf(dev, fabsf(z.x - rintf(z.x)));
+      dev = fmaxf(dev, fabsf(z.y - rintf(z.y)));
+      if (z.x > 0.5f) top = 2 * n;
+      if (z.y > 0.5f) top = 2 * n + 1;
+    }
+    const size_t o = (size_t)img * a.npix + pix;
+    a.out[o] = top >= 0 ? a.out_sign * top + a.out_bias : a.fill;
+    if (a.valid) a.valid[o] = top >= 0 ? 1 : 0;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, off));
+  if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+}
+
+}  // namespace fm

@@ -1,0 +1,283 @@
+"""Drop-in operators: the reference's dilation / erosion entry points on B200.
+
+Same names, signatures, argument meaning, return types and error behaviour as
+``fftmorph.morphology`` (reference morphology.py:30-239).  The value
+computation of every FFT operator runs in the sm_100a library through
+:class:`~paper_2305_03018_b200.engine.MorphPlan`; this module does only the
+host bookkeeping the reference does in Python (validation, ``lo`` / range
+arithmetic, ``tonal_max``, ``stats``).  The ``naive`` method runs the GPU
+direct kernel (same semantics as dilate_naive / erode_naive); nothing here
+computes image values on the CPU.
+"""
+
+from __future__ import annotations
+
+import enum
+
+import numpy as np
+import torch
+
+from . import engine
+from .grid import GridFunction, full_output_range, intersect_ranges
+
+
+class MorphMethod(enum.Enum):
+    """morphology.py:30-41."""
+    NAIVE = "naive"
+    FFT_UMBRA = "fft"
+
+    @classmethod
+    def parse(cls, name) -> "MorphMethod":
+        if isinstance(name, cls):
+            return name
+        for m in cls:
+            if name in (m.value, m.name, m.name.lower()):
+                return m
+        raise ValueError(f"unknown method {name!r}")
+
+
+# --------------------------------------------------------------------------- helpers
+
+def _device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2305_03018_b200 needs a CUDA device (B200); there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _upload(g: GridFunction, dev):
+    """Device copy of a grid's values in the narrowest supported dtype, plus its mask."""
+    vals = g.values
+    dv = vals[g.defined]
+    lo_v, hi_v = int(dv.min()), int(dv.max())
+    if lo_v >= 0 and hi_v <= 255:
+        dt, npdt = torch.uint8, np.uint8
+    elif lo_v >= 0 and hi_v <= 65535:
+        dt, npdt = torch.uint16, np.uint16
+    elif lo_v >= -(2**31) and hi_v < 2**31:
+        dt, npdt = torch.int32, np.int32
+    else:
+        raise NotImplementedError("image values beyond int32")
+    host = np.where(g.defined, vals, 0).astype(npdt)
+    t = torch.from_numpy(host).to(dev, non_blocking=False)
+    mask = None if g.gap_free else torch.from_numpy(g.defined.astype(np.uint8)).to(dev)
+    return t, mask, dt, lo_v, hi_v
+
+
+def _run_fft(f: GridFunction, b: GridFunction, *, mode: str, crop: bool, fill: int,
+             stats: dict | None):
+    dev = _device()
+    img, mask, dt, vmin, vmax = _upload(f, dev)
+    plan = engine.plan_cache.get(
+        shape=f.shape, se_values=b.values, se_defined=None if b.gap_free else b.defined,
+        se_lo=b.lo, mode=mode, crop=crop, img_dtype=dt, img_min=vmin, img_max=vmax,
+        fill=fill, batch=1, device=dev)
+    plan.reset_stats()
+    out, valid = plan.execute(img.unsqueeze(0), None if mask is None else mask.unsqueeze(0))
+    dev_max = plan.read_stats()          # raises ArithmeticError at >= 0.25 (fft_conv.py:145-148)
+    if stats is not None:
+        # morphology.py:125-128; padded_shape reports the B200 FFT extents: tile + tonal length
+        stats["max_abs_deviation"] = max(stats.get("max_abs_deviation", 0.0), dev_max)
+        info = plan.info
+        tile = (info["tile_x"],) if f.ndim == 1 else (info["tile_y"], info["tile_x"])
+        stats["padded_shape"] = tuple(tile) + (info["tonal_len"],)
+    values = out[0].cpu().numpy().astype(np.int64)
+    vmask = valid[0].cpu().numpy().astype(bool)
+    return values, vmask, plan
+
+
+def _empty_crop_quirk(f_ranges, conv_ranges):
+    # Reference quirk: with crop=True and F ∩ (F⊕B) empty,
+    # intersect_ranges returns None and project_with_validity raises TypeError
+    # (morphology.py:132-133 -> umbra.py:193 -> tensor.py:96).  Mirrored for drop-in parity.
+    if intersect_ranges(f_ranges, conv_ranges) is None:
+        raise TypeError("'NoneType' object is not iterable (image domain and dilation range "
+                        "do not intersect; reference dilate_fft raises here)")
+
+
+# --------------------------------------------------------------------------- FFT path
+
+def dilate_fft(f, b, *, crop: bool = True, return_validity: bool = False,
+               stats: dict | None = None):
+    """Exact dilation via the tonal lift (morphology.py:116-144), on the GPU."""
+    f = GridFunction.coerce(f)
+    b = GridFunction.coerce(b)
+    if f.ndim != b.ndim:
+        raise ValueError("rank mismatch")
+    if f.min_defined() < 0 or b.min_defined() < 0:
+        raise ValueError("tonal lift needs non-negative values")
+    conv = full_output_range(f.ranges, b.ranges)
+    if crop:
+        _empty_crop_quirk(f.ranges, conv)
+    values, valid, _ = _run_fft(f, b, mode="dilate", crop=crop, fill=0, stats=stats)
+    out_ranges = f.ranges if crop else conv
+    tonal_max = max(f.tonal_max + b.max_defined(), 1)
+    g = GridFunction(values, lo=tuple(lo for lo, _ in out_ranges), tonal_max=tonal_max)
+    return (g, valid) if return_validity else g
+
+
+def reflect(b) -> GridFunction:
+    """Index negation about the origin; values and gaps carried along (morphology.py:147-152)."""
+    b = GridFunction.coerce(b)
+    rev = (slice(None, None, -1),) * b.ndim
+    lo = tuple(-hi for hi in b.hi)
+    return GridFunction(b.values[rev], b.defined[rev], lo=lo,
+                        tonal_max=b.tonal_max, signed=b.signed)
+
+
+def negate(f, l: int) -> GridFunction:
+    """Pointwise l - f(x); gaps preserved (morphology.py:155-163)."""
+    f = GridFunction.coerce(f)
+    l = int(l)
+    if f.min_defined() < 0:
+        raise ValueError("cannot negate a grid with negative values")
+    if l < f.max_defined():
+        raise ValueError(f"l={l} below max value {f.max_defined()}")
+    values = np.where(f.defined, l - f.values, np.int64(0))
+    return GridFunction(values, f.defined.copy(), lo=f.lo, tonal_max=max(l, 1))
+
+
+def erode_fft(f, b, l: int | None = None, *, return_validity: bool = False,
+              stats: dict | None = None):
+    """Erosion by duality, l - dilate_fft(negate(f, l), reflect(b)) (morphology.py:166-180).
+
+    Computed in one GPU pass with l' = max f in place of l (bit-identical at
+    valid pixels, shorter tonal axis); pixels with no pair get l."""
+    f = GridFunction.coerce(f)
+    b = GridFunction.coerce(b)
+    if l is None:
+        l = f.tonal_max
+    l = int(l)
+    # negate(f, l) checks (morphology.py:158-161)
+    if f.min_defined() < 0:
+        raise ValueError("cannot negate a grid with negative values")
+    if l < f.max_defined():
+        raise ValueError(f"l={l} below max value {f.max_defined()}")
+    if f.ndim != b.ndim:
+        raise ValueError("rank mismatch")
+    # dilate_fft(negate(f), reflect(b)) checks (morphology.py:119-120)
+    if b.min_defined() < 0:
+        raise ValueError("tonal lift needs non-negative values")
+    rb_ranges = tuple((-hi, -lo) for lo, hi in b.ranges)
+    _empty_crop_quirk(f.ranges, full_output_range(f.ranges, rb_ranges))
+    values, valid, _ = _run_fft(f, b, mode="erode", crop=True, fill=l, stats=stats)
+    g = GridFunction(values, lo=f.lo, tonal_max=max(f.tonal_max, l), signed=True)
+    return (g, valid) if return_validity else g
+
+
+def _dilate_fft_signed(f, b, **kw):
+    """dilate_fft extended to signed inputs by a value shift (morphology.py:198-216).
+
+    The shift is applied inside the encode (v = f - min f) and undone in the
+    degree store, so no shifted copy of the image is built."""
+    f = GridFunction.coerce(f)
+    b = GridFunction.coerce(b)
+    m = f.min_defined()
+    if m >= 0:
+        return dilate_fft(f, b, **kw)
+    crop = kw.get("crop", True)
+    want_validity = kw.get("return_validity", False)
+    stats = kw.get("stats")
+    unknown = set(kw) - {"crop", "return_validity", "stats"}
+    if unknown:
+        raise TypeError(f"unexpected keyword argument {sorted(unknown)[0]!r}")
+    if f.ndim != b.ndim:
+        raise ValueError("rank mismatch")
+    if b.min_defined() < 0:
+        raise ValueError("tonal lift needs non-negative values")
+    conv = full_output_range(f.ranges, b.ranges)
+    if crop:
+        _empty_crop_quirk(f.ranges, conv)
+    values, valid, _ = _run_fft(f, b, mode="dilate", crop=crop, fill=0, stats=stats)
+    out_ranges = f.ranges if crop else conv
+    shift = -m
+    tonal_max = max(f.tonal_max + shift + b.max_defined(), 1)
+    g = GridFunction(values, lo=tuple(lo for lo, _ in out_ranges), tonal_max=tonal_max, signed=True)
+    return (g, valid) if want_validity else g
+
+
+# --------------------------------------------------------------------------- direct path
+
+def _naive(f: GridFunction, b: GridFunction, *, mode: str, crop: bool, fill: int):
+    dev = _device()
+    if f.ndim != b.ndim:
+        raise ValueError("rank mismatch")
+    if f.ndim not in (1, 2):
+        raise NotImplementedError("only 1-D signals and 2-D images are supported")
+    bound = max(abs(f.max_defined()), abs(f.min_defined())) + max(abs(b.max_defined()), abs(b.min_defined()))
+    if bound >= 2**31:
+        raise NotImplementedError("values beyond int32")
+    img, mask, _, _, _ = _upload(f, dev)
+    out, valid = engine.naive(img=img.unsqueeze(0), defined=None if mask is None else mask.unsqueeze(0),
+                              shape=f.shape, se_values=b.values,
+                              se_defined=None if b.gap_free else b.defined, se_lo=b.lo,
+                              mode=mode, crop=crop, fill=fill)
+    return out[0].cpu().numpy().astype(np.int64), valid[0].cpu().numpy().astype(bool)
+
+
+def dilate_naive(f, b, *, crop: bool = True, return_validity: bool = False):
+    """Sliding max of f(x-y)+b(y) over all defined pairs (morphology.py:65-85), GPU direct kernel."""
+    f = GridFunction.coerce(f)
+    b = GridFunction.coerce(b)
+    out_ranges = full_output_range(f.ranges, b.ranges)
+    values, valid = _naive(f, b, mode="dilate", crop=crop, fill=0)
+    if crop:
+        out_ranges = f.ranges
+    tonal_max = max(f.tonal_max + b.max_defined(), 1)
+    g = GridFunction(values, lo=tuple(lo for lo, _ in out_ranges), tonal_max=tonal_max, signed=f.signed)
+    return (g, valid) if return_validity else g
+
+
+def erode_naive(f, b, *, crop: bool = True, return_validity: bool = False):
+    """Sliding min of f(x+y)-b(y); neutral f.tonal_max where no pair exists (morphology.py:88-113)."""
+    f = GridFunction.coerce(f)
+    b = GridFunction.coerce(b)
+    out_ranges = tuple((flo - bhi, fhi - blo) for (flo, fhi), (blo, bhi) in zip(f.ranges, b.ranges))
+    values, valid = _naive(f, b, mode="erode", crop=crop, fill=f.tonal_max)
+    if crop:
+        out_ranges = f.ranges
+    g = GridFunction(values, lo=tuple(lo for lo, _ in out_ranges), tonal_max=f.tonal_max, signed=True)
+    return (g, valid) if return_validity else g
+
+
+# --------------------------------------------------------------------------- dispatch + compound
+
+def dilate(f, b, method=MorphMethod.NAIVE, **kw):
+    """morphology.py:183-187."""
+    method = MorphMethod.parse(method)
+    if method is MorphMethod.NAIVE:
+        return dilate_naive(f, b, **kw)
+    return _dilate_fft_signed(f, b, **kw)
+
+
+def erode(f, b, method=MorphMethod.NAIVE, l: int | None = None, **kw):
+    """morphology.py:190-195."""
+    method = MorphMethod.parse(method)
+    if method is MorphMethod.NAIVE:
+        return erode_naive(f, b, **kw)
+    return erode_fft(f, b, l=l, **kw)
+
+
+def opening(f, b, method=MorphMethod.NAIVE, l: int | None = None,
+            stats: dict | None = None) -> GridFunction:
+    """morphology.py:219-222."""
+    kw = {} if MorphMethod.parse(method) is MorphMethod.NAIVE else {"stats": stats}
+    return dilate(erode(f, b, method, l=l, **kw), b, method, **kw)
+
+
+def closing(f, b, method=MorphMethod.NAIVE, l: int | None = None,
+            stats: dict | None = None) -> GridFunction:
+    """morphology.py:225-229."""
+    kw = {} if MorphMethod.parse(method) is MorphMethod.NAIVE else {"stats": stats}
+    d = dilate(f, b, method, **kw)
+    return erode(d, b, method, l=d.tonal_max if l is None else l, **kw)
+
+
+def beucher_gradient(f, b, method=MorphMethod.NAIVE, l: int | None = None,
+                     stats: dict | None = None) -> GridFunction:
+    """morphology.py:232-239."""
+    kw = {} if MorphMethod.parse(method) is MorphMethod.NAIVE else {"stats": stats}
+    d = dilate(f, b, method, **kw)
+    e = erode(f, b, method, l=l, **kw)
+    values = np.maximum(d.values - e.values, np.int64(0))
+    return GridFunction(values, lo=GridFunction.coerce(f).lo,
+                        tonal_max=max(int(values.max()), 1))

@@ -1,0 +1,84 @@
+"""CPU: the C-ABI library builds, loads and exports every symbol of
+include/fftmorph_b200.h; the ctypes structs match the C layout.  No compute
+calls (no GPU here)."""
+
+import ctypes
+import re
+import subprocess
+import textwrap
+
+import pytest
+
+from conftest import ROOT
+from paper_2305_03018_b200 import _lib
+from paper_2305_03018_b200 import build as B
+
+HEADER = ROOT / "include" / "fftmorph_b200.h"
+
+
+def _declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fm_[a-z_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return _lib.load()
+
+
+def test_header_and_binding_agree():
+    assert sorted(_lib.EXPORTED) == _declared_functions()
+
+
+def test_library_exports_every_symbol(lib):
+    for name in _declared_functions():
+        assert hasattr(lib, name), name
+    assert lib.fm_abi_version() == 1
+
+
+def test_dynamic_symbol_table():
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("nm unavailable")
+    syms = set(re.findall(r"\bT (fm_\w+)", out.stdout))
+    assert set(_declared_functions()) <= syms
+
+
+def test_sm100a_code_in_library():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_struct_layouts_match_header(tmp_path):
+    src = tmp_path / "sz.c"
+    src.write_text(textwrap.dedent("""
+        #include <stdio.h>
+        #include <stddef.h>
+        #include "fftmorph_b200.h"
+        int main(void) {
+          printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(fm_plan_desc), sizeof(fm_plan_info), sizeof(fm_stats),
+                 offsetof(fm_plan_desc, img_min), offsetof(fm_plan_desc, scratch_bytes),
+                 offsetof(fm_plan_info, se_count));
+          return 0;
+        }
+    """))
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    want = [ctypes.sizeof(_lib.PlanDesc), ctypes.sizeof(_lib.PlanInfo), ctypes.sizeof(_lib.Stats),
+            _lib.PlanDesc.img_min.offset, _lib.PlanDesc.scratch_bytes.offset, _lib.PlanInfo.se_count.offset]
+    assert got == want
+
+
+def test_error_string_without_gpu(lib):
+    # validation happens before any CUDA call: a null descriptor is FM_EINVAL
+    h = ctypes.c_void_p()
+    rc = lib.fm_plan_create(ctypes.byref(h), None, None, None)
+    assert rc == _lib.FM_EINVAL
+    assert b"null" in lib.fm_last_error()
+    with pytest.raises(ValueError):
+        _lib.check(rc)

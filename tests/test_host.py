@@ -1,0 +1,126 @@
+"""CPU: host-side logic of the drop-in boundary (no kernel calls).
+
+GridFunction semantics (umbra.py:23-133), range helpers (tensor.py:76-101),
+MorphMethod parsing, reflect / negate (morphology.py:147-163), validation
+errors raised before any device work, and the sharding geometry.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import flat_se
+from paper_2305_03018_b200 import (GridFunction, MorphMethod, dilate_fft, erode_fft,
+                                   full_output_range, intersect_ranges, negate, reflect)
+from paper_2305_03018_b200 import sharding
+
+
+class TestGrid:
+    def test_validation(self):
+        with pytest.raises(ValueError):
+            GridFunction(np.zeros(0))
+        with pytest.raises(ValueError):
+            GridFunction(np.array([1, 2]), defined=np.array([False, False]))
+        with pytest.raises(ValueError):
+            GridFunction(np.array([1, 300]))
+        with pytest.raises(ValueError):
+            GridFunction(np.array([-1, 2]))
+        with pytest.raises(ValueError):
+            GridFunction(np.array([1, 2]), lo=(0, 0))
+        with pytest.raises(ValueError):
+            GridFunction(np.array([1, 2]), tonal_max=0)
+        g = GridFunction(np.array([-1, 2]), signed=True)
+        assert g.min_defined() == -1
+
+    def test_properties_and_tokens(self):
+        g = GridFunction.from_tokens([1, 2, None, 0], lo=(-1,), tonal_max=2)
+        assert g.ranges == ((-1, 2),) and g.hi == (2,)
+        assert g.to_list() == [1, 2, None, 0]
+        assert g.at(0) == 2 and g.at(1) is None
+        assert not g.gap_free and g.max_defined() == 2
+        with pytest.raises(IndexError):
+            g.at(3)
+        assert not g.values.flags.writeable
+
+    def test_equality_rule(self):
+        a = GridFunction(np.array([1, 5]), defined=np.array([True, False]), tonal_max=9)
+        b = GridFunction(np.array([1, 7]), defined=np.array([True, False]), tonal_max=3, signed=True)
+        assert a == b                      # gap values, tonal_max and signed are ignored
+        c = GridFunction(np.array([1, 7]), defined=np.array([True, False]), lo=(1,), tonal_max=7)
+        assert a != c
+
+    def test_duck_typed_foreign_grid(self):
+        class Foreign:
+            values = np.array([3, 4])
+            defined = np.array([True, True])
+            lo = (0,)
+            tonal_max = 4
+            signed = False
+        g = GridFunction.coerce(Foreign())
+        assert g == Foreign() and Foreign() == g or g == Foreign()
+
+
+def test_ranges():
+    assert full_output_range(((-1, 7),), ((-3, 5),)) == ((-4, 12),)
+    assert intersect_ranges(((0, 5),), ((6, 9),)) is None
+    assert intersect_ranges(((0, 5), (1, 2)), ((3, 9), (0, 9))) == ((3, 5), (1, 2))
+
+
+def test_method_parse():
+    assert MorphMethod.parse("fft") is MorphMethod.FFT_UMBRA
+    assert MorphMethod.parse("NAIVE") is MorphMethod.NAIVE
+    with pytest.raises(ValueError):
+        MorphMethod.parse("quick")
+
+
+def test_reflect_negate(example_image, example_se):
+    r = reflect(example_se)
+    assert r.lo == (-2,) and r.to_list() == [0, None, 2, 1]
+    assert reflect(reflect(example_se)) == example_se
+    assert reflect(flat_se(5)) == flat_se(5)
+    assert negate(example_image, 7).to_list() == [4, 7, 0, 1, 5, 0]
+    assert negate(negate(example_image, 7), 7) == example_image
+    with pytest.raises(ValueError):
+        negate(example_image, 5)
+
+
+def test_validation_errors_before_device(example_image):
+    neg = GridFunction(np.array([-1, 2]), tonal_max=3, signed=True)
+    with pytest.raises(ValueError):
+        dilate_fft(neg, flat_se(3))
+    with pytest.raises(ValueError):
+        erode_fft(example_image, flat_se(3), l=5)
+    bneg = GridFunction(np.array([-1, 0]), tonal_max=1, signed=True)
+    with pytest.raises(ValueError):
+        dilate_fft(example_image, bneg)
+    with pytest.raises(ValueError):
+        dilate_fft(example_image, flat_se(3, ndim=2))
+
+
+def test_shard_range_partition():
+    for n in (0, 1, 7, 64, 65):
+        for w in (1, 2, 3, 8):
+            parts = [sharding.shard_range(n, r, w) for r in range(w)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+            sizes = [e - s for s, e in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("mode", ["dilate", "erode"])
+def test_strip_windows_cover_dependency_cone(mode):
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        H = int(rng.integers(1, 60))
+        w = int(rng.integers(1, 6))
+        my = int(rng.integers(1, 12))
+        lo = int(rng.integers(-14, 4))
+        plan = sharding.strips(H, w, lo, my, mode)
+        for s in plan:
+            for y in range(s.out0, s.out1):
+                for j in range(my):
+                    yy = y - (lo + j) if mode == "dilate" else y + (lo + j)
+                    if 0 <= yy < H:
+                        assert s.in0 <= yy < s.in1
+            assert s.in0 <= s.out0 and s.out1 <= s.in1
+        for src, dst, r0, r1 in sharding.halo_transfers(plan):
+            assert plan[src].out0 <= r0 < r1 <= plan[src].out1
