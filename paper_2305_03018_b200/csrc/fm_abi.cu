@@ -45,6 +45,8 @@ int fail(int code, const std::string& msg) {
 
 constexpr double kPi = 3.14159265358979323846;
 
+int set_all_smem_attrs();
+
 int ensure_twiddles(int device) {
   std::lock_guard<std::mutex> lk(g_tw_mu);
   if (device < 64 && (g_tw_init_mask >> device) & 1ull) return FM_OK;
@@ -57,6 +59,17 @@ int ensure_twiddles(int device) {
       tw[offs[s] + j] = make_float2((float)std::cos(ang), (float)std::sin(ang));
     }
   FM_CUDA(cudaMemcpyToSymbol(c_tw, tw.data(), sizeof(float2) * kTwTotal));
+  std::vector<float2> tt(kTonalTabTotal);
+  for (int i = 0; i < kTonalCount; ++i) {
+    const int n = kTonalNs[i], off = tonal_off(n);
+    for (int j = 0; j < 2 * n; ++j) {
+      const double ang = 2.0 * kPi * j / (2.0 * n);
+      tt[off + j] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+    }
+  }
+  FM_CUDA(cudaMemcpyToSymbol(c_ttw, tt.data(), sizeof(float2) * kTonalTabTotal));
+  int rc = set_all_smem_attrs();
+  if (rc) return rc;
   if (device < 64) g_tw_init_mask |= (1ull << device);
   return FM_OK;
 }
@@ -113,10 +126,56 @@ const Variant kVariants[] = {
     FM_VARIANT(false, 32, 64, 128),  FM_VARIANT(false, 32, 128, 256), FM_VARIANT(false, 32, 256, 256),
 };
 
+typedef void (*tonal_launch_fn)(dim3, int, size_t, cudaStream_t, const TonalArgs&);
+template <int N, bool SM, int NT>
+void launch_tonal(dim3 grid, int nt, size_t smem, cudaStream_t s, const TonalArgs& a) {
+  tonal_kernel_t<N, SM, NT><<<grid, NT, smem, s>>>(a);
+}
+template <int N>
+constexpr bool tonal_sm() { return N > kTonalRegMax; }
+template <int N>
+constexpr int tonal_nt() { return N > kTonalRegMax ? 64 : 128; }
+
+struct TonalVariant {
+  int n, nt, smem;
+  tonal_launch_fn fn;
+  cudaError_t (*attr)();
+};
+template <int N>
+cudaError_t tonal_attr() {
+  return cudaFuncSetAttribute(tonal_kernel_t<N, tonal_sm<N>(), tonal_nt<N>()>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+#define FM_TV(N) \
+  TonalVariant { N, tonal_nt<N>(), tonal_sm<N>() ? 2 * N * tonal_nt<N>() * 8 : 0, &launch_tonal<N, tonal_sm<N>(), tonal_nt<N>()>, &tonal_attr<N> }
+const TonalVariant kTonal[] = {
+    FM_TV(1),  FM_TV(2),  FM_TV(3),  FM_TV(4),  FM_TV(5),   FM_TV(6),   FM_TV(8),   FM_TV(9),   FM_TV(10),
+    FM_TV(12), FM_TV(15), FM_TV(16), FM_TV(18), FM_TV(20),  FM_TV(24),  FM_TV(25),  FM_TV(27),  FM_TV(30),
+    FM_TV(32), FM_TV(36), FM_TV(40), FM_TV(45), FM_TV(48),  FM_TV(50),  FM_TV(54),  FM_TV(60),  FM_TV(64),
+    FM_TV(72), FM_TV(75), FM_TV(80), FM_TV(81), FM_TV(90),  FM_TV(96),  FM_TV(100), FM_TV(108), FM_TV(120),
+    FM_TV(125), FM_TV(128), FM_TV(135), FM_TV(144), FM_TV(150), FM_TV(160)};
+static_assert(sizeof(kTonal) / sizeof(TonalVariant) == kTonalCount, "tonal variant table");
+
+const TonalVariant* find_tonal(int n) {
+  for (const TonalVariant& v : kTonal)
+    if (v.n == n) return &v;
+  return nullptr;
+}
+
 int dtype_size(int dt) { return dt == FM_U8 ? 1 : dt == FM_U16 ? 2 : 4; }
 
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kTabBudget = 48 * 1024;
+
+int set_all_smem_attrs() {
+  for (const Variant& v : kVariants) {
+    FM_CUDA(v.attr_conv(kSmemLimit));
+    FM_CUDA(v.attr_spec(kSmemLimit));
+  }
+  for (const TonalVariant& v : kTonal) FM_CUDA(v.attr());
+  FM_CUDA(cudaFuncSetAttribute(tonal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+  return FM_OK;
+}
 
 }  // namespace
 
@@ -139,6 +198,7 @@ struct fm_plan {
   int copies = 16;
   size_t conv_smem = 0, tonal_smem = 0;
   int tonal_threads = 128, tonal_stride = 1;
+  const TonalVariant* tonal_var = nullptr;
   int enc_sign = 1, enc_bias = 0, vmax = 0;
   int out_sign = 1, out_bias = 0;
   // device buffers
@@ -383,6 +443,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   if (p->conv_smem > kSmemLimit) { free_plan(p); return fail(FM_EUNSUPPORTED, "tonal length too large for shared memory"); }
 
   // tonal kernel geometry
+  p->tonal_var = find_tonal(p->N);
   p->tonal_stride = (p->N + 1) | 1;
   int nt = 128;
   while (nt > 32 && (size_t)(2 * p->N + 2 * (size_t)nt * p->tonal_stride) * 8 > 200 * 1024) nt -= 32;
@@ -417,10 +478,6 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     return fail(FM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
   };
   cudaError_t e;
-  if ((e = bv->attr_conv(p->conv_smem)) != cudaSuccess) return cfail(e, "conv smem attribute");
-  if ((e = bv->attr_spec(p->conv_smem)) != cudaSuccess) return cfail(e, "spec smem attribute");
-  if ((e = cudaFuncSetAttribute(tonal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->tonal_smem)) != cudaSuccess)
-    return cfail(e, "tonal smem attribute");
 
   const size_t npts = (size_t)p->PY * p->PX;
   if ((e = cudaMalloc(&p->spec, sizeof(float2) * npts * p->K)) != cudaSuccess) return cfail(e, "spec alloc");
@@ -584,10 +641,15 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
     t.fill = p->d.fill;
     t.stride = p->tonal_stride;
     t.dev_max = reinterpret_cast<float*>(p->stats);
-    const int nt = p->tonal_threads;
     int e1 = -1;
     if (p->timing) { e1 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
-    tonal_kernel<<<dim3((unsigned)((npix + nt - 1) / nt), n), nt, p->tonal_smem, s>>>(t);
+    if (p->tonal_var) {
+      const int nt = p->tonal_var->nt;
+      p->tonal_var->fn(dim3((unsigned)((npix + nt - 1) / nt), n), nt, p->tonal_var->smem, s, t);
+    } else {
+      const int nt = p->tonal_threads;
+      tonal_kernel<<<dim3((unsigned)((npix + nt - 1) / nt), n), nt, p->tonal_smem, s>>>(t);
+    }
     g_launches++;
     FM_CUDA(cudaGetLastError());
     if (p->timing) {

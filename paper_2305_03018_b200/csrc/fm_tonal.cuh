@@ -52,6 +52,163 @@ __device__ __forceinline__ void stockham_stage(const float2* in, float2* out, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// Compile-time tonal FFTs.  For every 5-smooth N <= 160 the inverse length-N
+// FFT is a fully unrolled Stockham recursion (radices 8,4,2,3,5) whose
+// twiddles are compile-time offsets into one __constant__ table (constant-bank
+// operands, no index arithmetic).  N <= 80: the pixel's spectrum lives in
+// registers; 80 < N <= 160: in a thread-interleaved shared-memory array.
+#define FM_TONAL_NS                                                                                         \
+  1, 2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16, 18, 20, 24, 25, 27, 30, 32, 36, 40, 45, 48, 50, 54, 60, 64, 72, 75, 80, \
+      81, 90, 96, 100, 108, 120, 125, 128, 135, 144, 150, 160
+constexpr int kTonalNs[] = {FM_TONAL_NS};
+constexpr int kTonalCount = sizeof(kTonalNs) / sizeof(int);
+constexpr int kTonalRegMax = 80;
+
+__host__ __device__ constexpr int tonal_off(int n) {
+  constexpr int ns[] = {FM_TONAL_NS};
+  int off = 0;
+  for (int i = 0; i < (int)(sizeof(ns) / sizeof(int)); ++i) {
+    if (ns[i] == n) return off;
+    off += 2 * ns[i];
+  }
+  return -1;
+}
+__host__ __device__ constexpr int tonal_tab_total() {
+  constexpr int ns[] = {FM_TONAL_NS};
+  int off = 0;
+  for (int i = 0; i < (int)(sizeof(ns) / sizeof(int)); ++i) off += 2 * ns[i];
+  return off;
+}
+constexpr int kTonalTabTotal = tonal_tab_total();
+
+// W_{2N}^j = exp(+2 pi i j / (2N)), j < 2N, for each supported N (inverse sign).
+__constant__ float2 c_ttw[kTonalTabTotal];
+
+__host__ __device__ constexpr int radix_at(int n, int i) {
+  const int ps[5] = {8, 4, 2, 3, 5};
+  int idx = 0;
+  for (int q = 0; q < 5; ++q)
+    while (n % ps[q] == 0) {
+      if (idx == i) return ps[q];
+      n /= ps[q];
+      ++idx;
+    }
+  return 0;
+}
+__host__ __device__ constexpr int num_radices(int n) {
+  int c = 0;
+  while (radix_at(n, c) != 0) ++c;
+  return c;
+}
+
+template <int NT>
+struct SmemArr {
+  float2* p;
+  __device__ __forceinline__ float2& operator[](int i) const { return p[i * NT]; }
+};
+
+template <class A> struct IsSmemArr { static constexpr bool value = false; };
+template <int NT> struct IsSmemArr<SmemArr<NT>> { static constexpr bool value = true; };
+
+template <int N, int R, int Ns, class A, class B>
+__device__ __forceinline__ void stock_stage(A& in, B& out) {
+  constexpr int M = N / R;
+  constexpr int tstep = N / (Ns * R);
+  constexpr int off = tonal_off(N);
+  // register arrays need full unrolling (compile-time indices); shared-memory
+  // arrays are walked with a rolled loop to keep register pressure bounded
+  constexpr int U = IsSmemArr<A>::value ? 1 : M;
+#pragma unroll U
+  for (int j = 0; j < M; ++j) {
+    float2 v[R];
+    const int jm = j % Ns;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = in[j + r * M];
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], c_ttw[off + 2 * ((jm * r * tstep) % N)]);
+    }
+    dft<R, true>(v);
+    const int idxD = (j / Ns) * Ns * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[idxD + r * Ns] = v[r];
+  }
+}
+
+template <int N, int I, int Ns, class A>
+__device__ __forceinline__ void stock_run(A& a, A& b) {
+  constexpr int R = radix_at(N, I);
+  if constexpr (R != 0) {
+    stock_stage<N, R, Ns>(a, b);
+    stock_run<N, I + 1, Ns * R>(b, a);
+  }
+}
+
+template <int N, class A>
+__device__ __forceinline__ int tonal_threshold(const A& res, float& dev) {
+  int top = -1;
+  constexpr int U = IsSmemArr<A>::value ? 4 : N;
+#pragma unroll U
+  for (int n = 0; n < N; ++n) {
+    const float2 z = res[n];
+    dev = fmaxf(dev, fabsf(z.x - rintf(z.x)));
+    dev = fmaxf(dev, fabsf(z.y - rintf(z.y)));
+    top = z.x > 0.5f ? 2 * n : top;
+    top = z.y > 0.5f ? 2 * n + 1 : top;
+  }
+  return top;
+}
+
+template <int N, bool SM, int NT>
+__global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
+  constexpr int off = tonal_off(N);
+  const int img = blockIdx.y;
+  const int64_t pix = (int64_t)blockIdx.x * NT + threadIdx.x;
+  float dev = 0.f;
+  if (pix < a.npix) {
+    const float2* src = a.chat + (size_t)img * a.K * a.npix + pix;
+    int top;
+    if constexpr (!SM) {
+      float2 X[N + 1];
+#pragma unroll
+      for (int k = 0; k <= N; ++k) X[k] = __ldcs(src + (size_t)k * a.npix);
+      float2 A[N], B[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const float2 xk = X[k], xc = conjf2(X[N - k]);
+        A[k] = cadd(cadd(xk, xc), mul_pi(cmul(c_ttw[off + k], csub(xk, xc))));
+      }
+      stock_run<N, 0, 1>(A, B);
+      if constexpr (num_radices(N) % 2 == 0) top = tonal_threshold<N>(A, dev);
+      else top = tonal_threshold<N>(B, dev);
+    } else {
+      extern __shared__ __align__(16) float2 tsm_t[];
+      SmemArr<NT> A{tsm_t + threadIdx.x}, B{tsm_t + (size_t)N * NT + threadIdx.x};
+      // X[0..N-1] -> B, X[N] stays in a register
+#pragma unroll 8
+      for (int k = 0; k < N; ++k) B[k] = __ldcs(src + (size_t)k * a.npix);
+      const float2 xN = __ldcs(src + (size_t)N * a.npix);
+#pragma unroll 4
+      for (int k = 0; k < N; ++k) {
+        const float2 xk = B[k];
+        const float2 xc = conjf2(k == 0 ? xN : B[N - k]);
+        A[k] = cadd(cadd(xk, xc), mul_pi(cmul(c_ttw[off + k], csub(xk, xc))));
+      }
+      stock_run<N, 0, 1>(A, B);
+      if constexpr (num_radices(N) % 2 == 0) top = tonal_threshold<N>(A, dev);
+      else top = tonal_threshold<N>(B, dev);
+    }
+    const size_t o = (size_t)img * a.npix + pix;
+    a.out[o] = top >= 0 ? a.out_sign * top + a.out_bias : a.fill;
+    if (a.valid) a.valid[o] = top >= 0 ? 1 : 0;
+  }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
+  if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+}
+
+// generic runtime-N fallback (N > 160)
 __global__ void __launch_bounds__(128) tonal_kernel(const TonalArgs a) {
   extern __shared__ __align__(16) float2 tsm[];
   const int N = a.N;

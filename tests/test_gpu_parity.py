@@ -300,7 +300,7 @@ def test_tile_and_tonal_length_invariance():
         v, valid, dev, plan = _plan_run(w, "dilate", tile=tile)
         assert plan.info["tile_x"] == tile
         assert np.array_equal(v[0], ref) and np.array_equal(valid[0].astype(bool), refv), tile
-    for T in (36, 40, 64, 80):
+    for T in (36, 40, 64, 80, 162, 270, 400):   # register, shared-memory and generic tonal kernels
         v, valid, dev, plan = _plan_run(w, "dilate", tonal_len=T)
         assert plan.info["tonal_len"] == T
         assert np.array_equal(v[0], ref), T
