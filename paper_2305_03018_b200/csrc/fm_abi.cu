@@ -121,9 +121,9 @@ struct Variant {
   }
 
 const Variant kVariants[] = {
-    FM_VARIANT(true, 16, 16, 64),   FM_VARIANT(true, 32, 32, 128), FM_VARIANT(true, 64, 64, 256),
-    FM_VARIANT(true, 128, 128, 512), FM_VARIANT(false, 32, 16, 64),  FM_VARIANT(false, 32, 32, 128),
-    FM_VARIANT(false, 32, 64, 128),  FM_VARIANT(false, 32, 128, 256), FM_VARIANT(false, 32, 256, 256),
+    FM_VARIANT(true, 16, 16, 32),   FM_VARIANT(true, 32, 32, 64),   FM_VARIANT(true, 64, 64, 256),
+    FM_VARIANT(true, 128, 128, 512), FM_VARIANT(false, 32, 16, 64),  FM_VARIANT(false, 32, 32, 64),
+    FM_VARIANT(false, 32, 64, 128),  FM_VARIANT(false, 32, 128, 128), FM_VARIANT(false, 32, 256, 256),
 };
 
 typedef void (*tonal_launch_fn)(dim3, int, size_t, cudaStream_t, const TonalArgs&);
@@ -165,7 +165,6 @@ const TonalVariant* find_tonal(int n) {
 int dtype_size(int dt) { return dt == FM_U8 ? 1 : dt == FM_U16 ? 2 : 4; }
 
 constexpr int kSmemLimit = 227 * 1024;
-constexpr int kTabBudget = 48 * 1024;
 
 int set_all_smem_attrs() {
   for (const Variant& v : kVariants) {
@@ -195,15 +194,13 @@ struct fm_plan {
   int64_t OH = 1, OW = 1, off_y = 0, off_x = 0;
   int k_chunk = 1, kchunks = 1;
   int64_t ipc = 1;  // images per launch
-  int copies = 16;
   size_t conv_smem = 0, tonal_smem = 0;
   int tonal_threads = 128, tonal_stride = 1;
   const TonalVariant* tonal_var = nullptr;
   int enc_sign = 1, enc_bias = 0, vmax = 0;
   int out_sign = 1, out_bias = 0;
   // device buffers
-  float2* spec = nullptr;
-  float2* tabT = nullptr;
+  float4* spec = nullptr;
   float2* twN = nullptr;
   float2* wT = nullptr;
   float2* chat = nullptr;
@@ -233,7 +230,6 @@ void free_plan(fm_plan* p) {
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
   cudaFree(p->spec);
-  cudaFree(p->tabT);
   cudaFree(p->twN);
   cudaFree(p->wT);
   cudaFree(p->chat);
@@ -434,13 +430,9 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   p->tiles_total = p->tiles_x * p->tiles_y;
   p->tile_ctas = p->two_d ? p->tiles_total : (p->tiles_total + p->PY - 1) / p->PY;
 
-  // tonal-table replication and shared memory
-  int copies = 16;
-  while (copies > 1 && (size_t)T * copies * 8 > kTabBudget) copies >>= 1;
-  while (copies > 1 && bv->smem_fixed + (size_t)T * copies * 8 > kSmemLimit) copies >>= 1;
-  p->copies = copies;
-  p->conv_smem = bv->smem_fixed + (size_t)T * copies * 8;
-  if (p->conv_smem > kSmemLimit) { free_plan(p); return fail(FM_EUNSUPPORTED, "tonal length too large for shared memory"); }
+  // shared memory (tile buffer + spectrum staging + tonal indices)
+  p->conv_smem = bv->smem_fixed;
+  if (p->conv_smem > kSmemLimit) { free_plan(p); return fail(FM_EUNSUPPORTED, "tile too large for shared memory"); }
 
   // tonal kernel geometry
   p->tonal_var = find_tonal(p->N);
@@ -481,7 +473,6 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
 
   const size_t npts = (size_t)p->PY * p->PX;
   if ((e = cudaMalloc(&p->spec, sizeof(float2) * npts * p->K)) != cudaSuccess) return cfail(e, "spec alloc");
-  if ((e = cudaMalloc(&p->tabT, sizeof(float2) * T)) != cudaSuccess) return cfail(e, "table alloc");
   if ((e = cudaMalloc(&p->twN, sizeof(float2) * std::max(1, p->N))) != cudaSuccess) return cfail(e, "table alloc");
   if ((e = cudaMalloc(&p->wT, sizeof(float2) * std::max(1, p->N))) != cudaSuccess) return cfail(e, "table alloc");
   if ((e = cudaMalloc(&p->stats, sizeof(int) * 4)) != cudaSuccess) return cfail(e, "stats alloc");
@@ -491,12 +482,6 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     free_plan(p);
     return fail(FM_ENOMEM, std::string("spectral scratch alloc: ") + cudaGetErrorString(e));
   }
-  std::vector<float2> h(T);
-  for (int r = 0; r < T; ++r) {
-    const double ang = -2.0 * kPi * r / T;
-    h[r] = make_float2((float)std::cos(ang), (float)std::sin(ang));
-  }
-  cudaMemcpy(p->tabT, h.data(), sizeof(float2) * T, cudaMemcpyHostToDevice);
   std::vector<float2> tn(std::max(1, p->N)), wt(std::max(1, p->N));
   for (int j = 0; j < p->N; ++j) {
     const double a1 = 2.0 * kPi * j / p->N, a2 = 2.0 * kPi * j / T;
@@ -525,8 +510,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   a.enc_sign = 1;
   a.enc_bias = -smin;
   a.vmax = 1 << 30;
-  a.copies = copies;
-  a.tabT = p->tabT;
+  a.two_pi_over_T = (float)(2.0 * kPi / T);
   a.spec = p->spec;
   a.spec_out = p->spec;
   a.spec_scale = (float)(1.0 / ((double)(p->two_d ? p->PY : 1) * p->PX * T));
@@ -607,8 +591,7 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
     a.enc_sign = p->enc_sign;
     a.enc_bias = p->enc_bias;
     a.vmax = p->vmax;
-    a.copies = p->copies;
-    a.tabT = p->tabT;
+    a.two_pi_over_T = (float)(2.0 * kPi / p->T);
     a.spec = p->spec;
     a.chat = p->chat;
     a.err = p->stats + 1;

@@ -8,7 +8,7 @@
 //       never exists;
 //   (b) runs the forward 2-D FFT (y axis, then x axis; radix-R1 x radix-R2
 //       four-step per axis, butterflies in registers, exchanges through a
-//       swizzled shared-memory tile);
+//       padded shared-memory tile);
 //   (c) multiplies by the cached SE spectrum for k (fa *= fb, fft_conv.py:137),
 //       fused into the last forward pass;
 //   (d) runs the inverse FFT (x axis, then y axis) and writes only the
@@ -16,6 +16,20 @@
 //       Chat[img][k][out_y][out_x] (complex64) for the tonal kernel.
 // With SPEC=true the same code computes the SE spectrum (rfftn(b),
 // fft_conv.py:135-136) once per plan and stores it in thread-register order.
+//
+// Data movement:
+//  * every thread works on PAIRS of horizontally adjacent tile points, so each
+//    shared-memory access is one 128-bit LDS/STS; rows are padded to PX+2
+//    complex values (16-byte aligned; 8 consecutive rows at one x hit 8
+//    distinct 16-byte bank groups, so row passes whose lanes run down the rows
+//    are conflict-free; column passes read contiguous row segments); all
+//    per-element offsets are compile-time immediates;
+//  * the tonal DFT twiddle of the encode is one MUFU sincos on an exactly
+//    reduced integer angle (no table, no shared memory);
+//  * the SE spectrum for plane k (L2-resident, read by every tile) is streamed
+//    into shared memory with per-thread cp.async (LDGSTS) in thread order, two
+//    chunks ahead, so its L2 latency overlaps the FFT passes instead of
+//    stalling the spectral product.
 #pragma once
 #include "fm_dft.cuh"
 
@@ -31,7 +45,6 @@ template <> struct Split<128> { static constexpr int R1 = 16, R2 = 8; };
 template <> struct Split<256> { static constexpr int R1 = 16, R2 = 16; };
 
 // Twiddle tables W_P^j = exp(-2 pi i j / P) for P = 16..256, concatenated.
-// Offsets: 16 -> 0, 32 -> 16, 64 -> 48, 128 -> 112, 256 -> 240 (496 entries).
 template <int P> struct TwOff;
 template <> struct TwOff<16> { static constexpr int v = 0; };
 template <> struct TwOff<32> { static constexpr int v = 16; };
@@ -58,10 +71,9 @@ struct TileArgs {
   int k_chunk;
   int enc_sign, enc_bias;     // v = enc_sign * f + enc_bias (CONV) / v = b - se_min (SPEC)
   int vmax;                   // largest legal v
-  int copies;                 // tonal-table replication (power of 2, <= 16)
-  const float2* tabT;         // [T] exp(-2 pi i r / T)
-  const float2* spec;         // [K][thread order] SE spectrum (CONV reads, SPEC writes)
-  float2* spec_out;           // SPEC
+  float two_pi_over_T;        // 2 pi / T
+  const float4* spec;         // [K][thread order] SE spectrum, pairs (CONV reads)
+  float4* spec_out;           // SPEC writes
   float spec_scale;           // SPEC: 1 / (PY_eff * PX * T)
   float2* chat;               // CONV: [imgs][K][OH*OW]
   int* err;                   // value-range error flag
@@ -74,25 +86,27 @@ struct TileCfg {
   static constexpr int R1x = Split<PX>::R1, R2x = Split<PX>::R2;
   static constexpr int R1y = TWO_D ? Split<PY>::R1 : 1;
   static constexpr int R2y = TWO_D ? Split<PY>::R2 : 1;
+  static constexpr int RS = PX + 2;              // padded row stride (complex values)
   static constexpr int NPTS = PY * PX;
-  static constexpr int E = NPTS / NT;
-  static constexpr int G_yA = TWO_D ? PX * R2y / NT : 0;
-  static constexpr int G_yB = TWO_D ? PX * R1y / NT : 0;
-  static constexpr int G_xA = PY * R2x / NT;
-  static constexpr int G_xB = PY * R1x / NT;
-  static constexpr int SWZ = 15;
-  static_assert(NPTS % NT == 0, "tile points must divide among threads");
-  static_assert(G_xA * R1x == E && G_xB * R2x == E, "x-axis item split");
-  static_assert(!TWO_D || (G_yA * R1y == E && G_yB * R2y == E), "y-axis item split");
+  static constexpr int XP = PX / 2;              // column pairs
+  static constexpr int G_yA = TWO_D ? XP * R2y / NT : 0;   // items (xp, n2): R1y pairs each
+  static constexpr int G_yB = TWO_D ? XP * R1y / NT : 0;   // items (xp, k1): R2y pairs each
+  static constexpr int G_xA = PY * (R2x / 2) / NT;         // items (y, n2 pair): 2 x R1x values
+  static constexpr int G_xB = PY * R1x / NT;               // items (y, k1): R2x values
+  static_assert(!TWO_D || (G_yA >= 1 && G_yA * NT == XP * R2y && G_yB >= 1 && G_yB * NT == XP * R1y),
+                "y-axis item split");
+  static_assert(G_xA >= 1 && G_xA * NT == PY * (R2x / 2) && G_xB >= 1 && G_xB * NT == PY * R1x,
+                "x-axis item split");
   static_assert(PX >= 16, "min tile edge 16");
-  // shared memory bytes excluding the tonal table
-  static constexpr int kSmemFixed = NPTS * 8 + ((NPTS * 2 + 15) / 16) * 16;
+  static constexpr int kBufBytes = PY * RS * 8;
+  static constexpr int kSpecPairs = NPTS / 2;           // float4 per tonal plane
+  static constexpr int SQ = R2x / 2;                    // float4 per x-pass-B item
+  static constexpr int kChunkF4 = SQ * NT;              // float4 per spectrum chunk (one item per thread)
+  static constexpr int NBUF = G_xB >= 2 ? 2 : 1;
+  static constexpr int kSpecBytes = NBUF * kChunkF4 * 16;
+  static constexpr int kTvBytes = ((NPTS * 2 + 15) / 16) * 16;
+  static constexpr int kSmemFixed = kBufBytes + kSpecBytes + kTvBytes;
 };
-
-// swizzled position of tile element (y, x): XOR the low 4 bits of x with y
-// so that 16 consecutive rows at one x hit 16 distinct 8-byte bank pairs.
-template <int PX>
-__device__ __forceinline__ int sidx(int y, int x) { return y * PX + (x ^ (y & 15)); }
 
 __device__ __forceinline__ int load_img(const void* img, int dtype, int64_t i) {
   if (dtype == 0) return (int)__ldg(reinterpret_cast<const uint8_t*>(img) + i);
@@ -100,243 +114,341 @@ __device__ __forceinline__ int load_img(const void* img, int dtype, int64_t i) {
   return __ldg(reinterpret_cast<const int32_t*>(img) + i);
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+// 16-byte global -> shared async copy (LDGSTS), L2-only caching
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 template <int PY, int PX, int NT, bool TWO_D, bool SPEC>
 __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   using C = TileCfg<PY, PX, NT, TWO_D>;
+  constexpr int RS = C::RS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* buf = reinterpret_cast<float2*>(smem_raw);
-  uint16_t* tv = reinterpret_cast<uint16_t*>(smem_raw + C::NPTS * 8);
-  float2* tab = reinterpret_cast<float2*>(smem_raw + C::kSmemFixed);
+  float4* sbuf = reinterpret_cast<float4*>(smem_raw + C::kBufBytes);
+  uint16_t* tv = reinterpret_cast<uint16_t*>(smem_raw + C::kBufBytes + C::kSpecBytes);
+  const uint32_t* tv32 = reinterpret_cast<const uint32_t*>(tv);
+
+  auto ld2 = [&](int y, int x) -> float4 { return *reinterpret_cast<const float4*>(buf + y * RS + x); };
+  auto st2 = [&](int y, int x, float2 p, float2 q) {
+    *reinterpret_cast<float4*>(buf + y * RS + x) = make_float4(p.x, p.y, q.x, q.y);
+  };
 
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
   const int img = SPEC ? 0 : blockIdx.z;
   const int T = a.T;
-  const int copies = a.copies;
-  const int cmask = copies - 1;
-
-  // ---- tonal twiddle table, replicated `copies` times for conflict-free lookups
-  for (int i = tid; i < T * copies; i += NT) tab[i] = a.tabT[i / copies];
 
   // ---- stage the tile's tonal indices v(x) (kSent = no entry)
-  int ty = 0, tx = 0;
-  if (TWO_D) {
-    ty = blockIdx.x / a.tiles_x;
-    tx = blockIdx.x - ty * a.tiles_x;
-  }
-  int bad = 0;
-  for (int p = tid; p < C::NPTS; p += NT) {
-    const int py = p / PX, px = p - (p / PX) * PX;
-    uint16_t t = kSent;
-    if (SPEC) {
-      const int sy = TWO_D ? py : 0;
-      if (sy < a.my && px < a.mx) {
-        const int si = sy * a.mx + px;
-        if (a.se_def == nullptr || a.se_def[si]) t = (uint16_t)(a.se_vals[si] + a.enc_bias);
-      }
-    } else {
-      int iy, ix;
-      bool rowok;
-      if (TWO_D) {
-        iy = ty * a.QY + a.DY + py;
-        ix = tx * a.QX + a.DX + px;
-        rowok = true;
+  {
+    int ty = 0, tx = 0;
+    if (TWO_D && !SPEC) {
+      ty = blockIdx.x / a.tiles_x;
+      tx = blockIdx.x - ty * a.tiles_x;
+    }
+    int bad = 0;
+    for (int p = tid; p < C::NPTS; p += NT) {
+      const int py = p / PX, px = p - (p / PX) * PX;
+      uint16_t t = kSent;
+      if (SPEC) {
+        const int sy = TWO_D ? py : 0;
+        if (sy < a.my && px < a.mx) {
+          const int si = sy * a.mx + px;
+          if (a.se_def == nullptr || a.se_def[si]) t = (uint16_t)(a.se_vals[si] + a.enc_bias);
+        }
       } else {
-        const int tile = blockIdx.x * PY + py;
-        iy = 0;
-        ix = tile * a.QX + a.DX + px;
-        rowok = tile < a.tiles_total;
-      }
-      if (rowok && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
-        const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
-        if (a.img_def == nullptr || a.img_def[gi]) {
-          const int v = a.enc_sign * load_img(a.img, a.img_dtype, gi) + a.enc_bias;
-          if (v < 0 || v > a.vmax) bad = 1;
-          else t = (uint16_t)v;
+        int iy, ix;
+        bool rowok;
+        if (TWO_D) {
+          iy = ty * a.QY + a.DY + py;
+          ix = tx * a.QX + a.DX + px;
+          rowok = true;
+        } else {
+          const int tile = blockIdx.x * PY + py;
+          iy = 0;
+          ix = tile * a.QX + a.DX + px;
+          rowok = tile < a.tiles_total;
+        }
+        if (rowok && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
+          const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
+          if (a.img_def == nullptr || a.img_def[gi]) {
+            const int v = a.enc_sign * load_img(a.img, a.img_dtype, gi) + a.enc_bias;
+            if (v < 0 || v > a.vmax) bad = 1;
+            else t = (uint16_t)v;
+          }
         }
       }
+      tv[p] = t;
     }
-    tv[p] = t;
+    if (!SPEC && bad) atomicOr(a.err, 1);
   }
-  if (!SPEC && bad) atomicOr(a.err, 1);
   __syncthreads();
-
+  const int ty = (TWO_D && !SPEC) ? blockIdx.x / a.tiles_x : 0;
+  const int tx = (TWO_D && !SPEC) ? blockIdx.x - ty * a.tiles_x : 0;
   const int k_begin = blockIdx.y * a.k_chunk;
   const int k_end = min(a.K, k_begin + a.k_chunk);
 
+  // per-thread spectrum chunk copy: item g of plane k -> buffer g % NBUF (own slots only)
+  auto spec_fetch = [&](int k, int g) {
+    const float4* src = a.spec + (size_t)k * C::kSpecPairs + (size_t)g * C::kChunkF4 + tid;
+    float4* dst = sbuf + (g % C::NBUF) * C::kChunkF4 + tid;
+#pragma unroll
+    for (int q = 0; q < C::SQ; ++q) cp_async16(dst + q * NT, src + q * NT);
+    cp_async_commit();
+  };
+
   for (int k = k_begin; k < k_end; ++k) {
-    // encode helper: w_T^{k v} from the replicated table
+    if constexpr (!SPEC) {
+#pragma unroll
+      for (int g = 0; g < C::NBUF; ++g) spec_fetch(k, g);
+    }
+    // encode helper: w_T^{k v} = exp(-2 pi i ((k v) mod T) / T).  The index is
+    // reduced exactly in integers to r' in [-T/2, T/2], so the MUFU sin/cos
+    // argument stays in [-pi, pi] (abs. error < 4e-7, far inside the 0.5 budget).
+    // Branch-free: the sentinel's (meaningless) angle is computed and then masked.
     auto enc = [&](uint32_t t) -> float2 {
-      if (t == kSent) return make_float2(0.f, 0.f);
       const uint32_t n = (uint32_t)k * t;
       uint32_t r = n - __umulhi(n, a.magicT) * (uint32_t)T;
-      if (r >= (uint32_t)T) r -= (uint32_t)T;
-      return tab[r * copies + (lane & cmask)];
+      r = (r >= (uint32_t)T) ? r - (uint32_t)T : r;
+      const int rr = (2 * r > (uint32_t)T) ? (int)r - T : (int)r;
+      float sn, cs;
+      __sincosf((float)rr * a.two_pi_over_T, &sn, &cs);
+      const bool live = t != kSent;
+      return make_float2(live ? cs : 0.f, live ? -sn : 0.f);
     };
 
     if constexpr (TWO_D) {
-      // ---------------- forward y, pass A (with encode)
+      // ---------------- forward y, pass A (with encode): item (xp, n2)
 #pragma unroll
       for (int g = 0; g < C::G_yA; ++g) {
         const int i = tid + NT * g;
-        const int x = i % PX, n2 = i / PX;
-        float2 w[C::R1y];
+        const int xp = i % C::XP, n2 = i / C::XP;
+        float2 wa[C::R1y], wb[C::R1y];
 #pragma unroll
-        for (int n1 = 0; n1 < C::R1y; ++n1) w[n1] = enc(tv[(n2 + C::R2y * n1) * PX + x]);
-        dft<C::R1y, false>(w);
+        for (int n1 = 0; n1 < C::R1y; ++n1) {
+          const uint32_t tt = tv32[((n2 + C::R2y * n1) * PX) / 2 + xp];
+          wa[n1] = enc(tt & 0xFFFFu);
+          wb[n1] = enc(tt >> 16);
+        }
+        dft<C::R1y, false>(wa);
+        dft<C::R1y, false>(wb);
 #pragma unroll
         for (int k1 = 0; k1 < C::R1y; ++k1) {
-          const float2 z = (k1 == 0) ? w[k1] : cmul(w[k1], c_tw[TwOff<PY>::v + n2 * k1]);
-          buf[sidx<PX>(n2 + C::R2y * k1, x)] = z;
+          float2 za = wa[k1], zb = wb[k1];
+          if (k1 != 0) {
+            const float2 w = c_tw[TwOff<PY>::v + n2 * k1];
+            za = cmul(za, w);
+            zb = cmul(zb, w);
+          }
+          st2(n2 + C::R2y * k1, 2 * xp, za, zb);
         }
       }
       __syncthreads();
-      // ---------------- forward y, pass B
+      // ---------------- forward y, pass B: item (xp, k1)
 #pragma unroll
       for (int g = 0; g < C::G_yB; ++g) {
         const int i = tid + NT * g;
-        const int x = i % PX, k1 = i / PX;
-        float2 w[C::R2y];
+        const int xp = i % C::XP, k1 = i / C::XP;
+        float2 wa[C::R2y], wb[C::R2y];
 #pragma unroll
-        for (int n2 = 0; n2 < C::R2y; ++n2) w[n2] = buf[sidx<PX>(n2 + C::R2y * k1, x)];
-        dft<C::R2y, false>(w);
-#pragma unroll
-        for (int k2 = 0; k2 < C::R2y; ++k2) buf[sidx<PX>(k2 + C::R2y * k1, x)] = w[k2];
-      }
-      __syncthreads();
-      // ---------------- forward x, pass A
-#pragma unroll
-      for (int g = 0; g < C::G_xA; ++g) {
-        const int i = tid + NT * g;
-        const int y = i % PY, n2 = i / PY;
-        float2 w[C::R1x];
-#pragma unroll
-        for (int n1 = 0; n1 < C::R1x; ++n1) w[n1] = buf[sidx<PX>(y, n2 + C::R2x * n1)];
-        dft<C::R1x, false>(w);
-#pragma unroll
-        for (int k1 = 0; k1 < C::R1x; ++k1) {
-          const float2 z = (k1 == 0) ? w[k1] : cmul(w[k1], c_tw[TwOff<PX>::v + n2 * k1]);
-          buf[sidx<PX>(y, n2 + C::R2x * k1)] = z;
+        for (int n2 = 0; n2 < C::R2y; ++n2) {
+          const float4 p = ld2(n2 + C::R2y * k1, 2 * xp);
+          wa[n2] = make_float2(p.x, p.y);
+          wb[n2] = make_float2(p.z, p.w);
         }
-      }
-      __syncthreads();
-    } else {
-      // ---------------- 1-D: forward x, pass A with encode (row y = independent tile)
+        dft<C::R2y, false>(wa);
+        dft<C::R2y, false>(wb);
 #pragma unroll
-      for (int g = 0; g < C::G_xA; ++g) {
-        const int i = tid + NT * g;
-        const int y = i % PY, n2 = i / PY;
-        float2 w[C::R1x];
-#pragma unroll
-        for (int n1 = 0; n1 < C::R1x; ++n1) w[n1] = enc(tv[y * PX + n2 + C::R2x * n1]);
-        dft<C::R1x, false>(w);
-#pragma unroll
-        for (int k1 = 0; k1 < C::R1x; ++k1) {
-          const float2 z = (k1 == 0) ? w[k1] : cmul(w[k1], c_tw[TwOff<PX>::v + n2 * k1]);
-          buf[sidx<PX>(y, n2 + C::R2x * k1)] = z;
-        }
+        for (int k2 = 0; k2 < C::R2y; ++k2) st2(k2 + C::R2y * k1, 2 * xp, wa[k2], wb[k2]);
       }
       __syncthreads();
     }
 
-    // ---------------- forward x, pass B (+ spectral product + inverse x pass B)
+    // ---------------- forward x, pass A: item (y, n2 pair); 1-D: with encode
+#pragma unroll
+    for (int g = 0; g < C::G_xA; ++g) {
+      const int i = tid + NT * g;
+      const int y = i % PY, n2 = 2 * (i / PY);
+      float2 wa[C::R1x], wb[C::R1x];
+#pragma unroll
+      for (int n1 = 0; n1 < C::R1x; ++n1) {
+        if constexpr (TWO_D) {
+          const float4 p = ld2(y, n2 + C::R2x * n1);
+          wa[n1] = make_float2(p.x, p.y);
+          wb[n1] = make_float2(p.z, p.w);
+        } else {
+          const uint32_t tt = tv32[(y * PX + n2 + C::R2x * n1) / 2];
+          wa[n1] = enc(tt & 0xFFFFu);
+          wb[n1] = enc(tt >> 16);
+        }
+      }
+      dft<C::R1x, false>(wa);
+      dft<C::R1x, false>(wb);
+#pragma unroll
+      for (int k1 = 0; k1 < C::R1x; ++k1) {
+        float2 za = wa[k1], zb = wb[k1];
+        if (k1 != 0) {
+          za = cmul(za, c_tw[TwOff<PX>::v + n2 * k1]);
+          zb = cmul(zb, c_tw[TwOff<PX>::v + (n2 + 1) * k1]);
+        }
+        st2(y, n2 + C::R2x * k1, za, zb);
+      }
+    }
+    __syncthreads();
+
+    // ---------------- forward x, pass B (+ spectral product + inverse x pass B): item (y, k1)
     {
-      const float2* sk = a.spec + (size_t)k * C::NPTS;
-      float2* so = SPEC ? a.spec_out + (size_t)k * C::NPTS : nullptr;
+      float4* so = SPEC ? a.spec_out + (size_t)k * C::kSpecPairs : nullptr;
 #pragma unroll
       for (int g = 0; g < C::G_xB; ++g) {
         const int i = tid + NT * g;
         const int y = i % PY, k1 = i / PY;
         float2 w[C::R2x];
 #pragma unroll
-        for (int n2 = 0; n2 < C::R2x; ++n2) w[n2] = buf[sidx<PX>(y, n2 + C::R2x * k1)];
+        for (int q = 0; q < C::SQ; ++q) {
+          const float4 p = ld2(y, 2 * q + C::R2x * k1);
+          w[2 * q] = make_float2(p.x, p.y);
+          w[2 * q + 1] = make_float2(p.z, p.w);
+        }
         dft<C::R2x, false>(w);
         if constexpr (SPEC) {
+          const float s = a.spec_scale;
 #pragma unroll
-          for (int e = 0; e < C::R2x; ++e) so[(g * C::R2x + e) * NT + tid] = cscale(w[e], a.spec_scale);
+          for (int q = 0; q < C::SQ; ++q)
+            so[(g * C::SQ + q) * NT + tid] =
+                make_float4(w[2 * q].x * s, w[2 * q].y * s, w[2 * q + 1].x * s, w[2 * q + 1].y * s);
         } else {
+          // chunk g landed? (the newest NBUF-1 groups may still be in flight)
+          if (g + C::NBUF <= C::G_xB) cp_async_wait<C::NBUF - 1>();
+          else cp_async_wait<0>();
+          const float4* sp = sbuf + (g % C::NBUF) * C::kChunkF4 + tid;
+          float4 s4[C::SQ];
 #pragma unroll
-          for (int e = 0; e < C::R2x; ++e) w[e] = cmul(w[e], __ldg(sk + (g * C::R2x + e) * NT + tid));
+          for (int q = 0; q < C::SQ; ++q) s4[q] = sp[q * NT];
+#pragma unroll
+          for (int q = 0; q < C::SQ; ++q) {
+            w[2 * q] = cmul(w[2 * q], make_float2(s4[q].x, s4[q].y));
+            w[2 * q + 1] = cmul(w[2 * q + 1], make_float2(s4[q].z, s4[q].w));
+          }
+          // refill this thread's own slots (their values are consumed above)
+          if (g + C::NBUF < C::G_xB) spec_fetch(k, g + C::NBUF);
           dft<C::R2x, true>(w);
 #pragma unroll
-          for (int n2 = 0; n2 < C::R2x; ++n2) buf[sidx<PX>(y, n2 + C::R2x * k1)] = w[n2];
+          for (int q = 0; q < C::SQ; ++q) st2(y, 2 * q + C::R2x * k1, w[2 * q], w[2 * q + 1]);
         }
       }
     }
-    if constexpr (SPEC) {
-      __syncthreads();
-      continue;
-    } else {
-      __syncthreads();
-      // ---------------- inverse x, pass A
+    __syncthreads();
+    if constexpr (SPEC) continue;
+
+    // ---------------- inverse x, pass A: item (y, n2 pair); 1-D: output store
 #pragma unroll
-      for (int g = 0; g < C::G_xA; ++g) {
-        const int i = tid + NT * g;
-        const int y = i % PY, n2 = i / PY;
-        float2 w[C::R1x];
+    for (int g = 0; g < C::G_xA; ++g) {
+      const int i = tid + NT * g;
+      const int y = i % PY, n2 = 2 * (i / PY);
+      float2 wa[C::R1x], wb[C::R1x];
 #pragma unroll
-        for (int k1 = 0; k1 < C::R1x; ++k1) {
-          const float2 z = buf[sidx<PX>(y, n2 + C::R2x * k1)];
-          w[k1] = (k1 == 0) ? z : cmulc(z, c_tw[TwOff<PX>::v + n2 * k1]);
-        }
-        dft<C::R1x, true>(w);
-        if constexpr (TWO_D) {
-#pragma unroll
-          for (int n1 = 0; n1 < C::R1x; ++n1) buf[sidx<PX>(y, n2 + C::R2x * n1)] = w[n1];
-        } else {
-          // 1-D output: row y is tile (blockIdx.x*PY + y); positions x >= mx-1 are valid
-          const int tile = blockIdx.x * PY + y;
-          if (tile < a.tiles_total) {
-            float2* dst = a.chat + ((size_t)img * a.K + k) * (size_t)a.OW;
-#pragma unroll
-            for (int n1 = 0; n1 < C::R1x; ++n1) {
-              const int x = n2 + C::R2x * n1;
-              const int ox = tile * a.QX + x - (a.mx - 1);
-              if (x >= a.mx - 1 && ox < a.OW) dst[ox] = w[n1];
-            }
-          }
+      for (int k1 = 0; k1 < C::R1x; ++k1) {
+        const float4 p = ld2(y, n2 + C::R2x * k1);
+        wa[k1] = make_float2(p.x, p.y);
+        wb[k1] = make_float2(p.z, p.w);
+        if (k1 != 0) {
+          wa[k1] = cmulc(wa[k1], c_tw[TwOff<PX>::v + n2 * k1]);
+          wb[k1] = cmulc(wb[k1], c_tw[TwOff<PX>::v + (n2 + 1) * k1]);
         }
       }
-      __syncthreads();
+      dft<C::R1x, true>(wa);
+      dft<C::R1x, true>(wb);
       if constexpr (TWO_D) {
-        // ---------------- inverse y, pass B
 #pragma unroll
-        for (int g = 0; g < C::G_yB; ++g) {
-          const int i = tid + NT * g;
-          const int x = i % PX, k1 = i / PX;
-          float2 w[C::R2y];
+        for (int n1 = 0; n1 < C::R1x; ++n1) st2(y, n2 + C::R2x * n1, wa[n1], wb[n1]);
+      } else {
+        // 1-D output: row y is tile (blockIdx.x*PY + y); positions x >= mx-1 are valid
+        const int tile = blockIdx.x * PY + y;
+        if (tile < a.tiles_total) {
+          float2* dst = a.chat + ((size_t)img * a.K + k) * (size_t)a.OW;
 #pragma unroll
-          for (int k2 = 0; k2 < C::R2y; ++k2) w[k2] = buf[sidx<PX>(k2 + C::R2y * k1, x)];
-          dft<C::R2y, true>(w);
-#pragma unroll
-          for (int n2 = 0; n2 < C::R2y; ++n2) buf[sidx<PX>(n2 + C::R2y * k1, x)] = w[n2];
-        }
-        __syncthreads();
-        // ---------------- inverse y, pass A + store of the valid window
-        float2* dst = a.chat + ((size_t)img * a.K + k) * (size_t)a.OH * a.OW;
-#pragma unroll
-        for (int g = 0; g < C::G_yA; ++g) {
-          const int i = tid + NT * g;
-          const int x = i % PX, n2 = i / PX;
-          float2 w[C::R1y];
-#pragma unroll
-          for (int k1 = 0; k1 < C::R1y; ++k1) {
-            const float2 z = buf[sidx<PX>(n2 + C::R2y * k1, x)];
-            w[k1] = (k1 == 0) ? z : cmulc(z, c_tw[TwOff<PY>::v + n2 * k1]);
+          for (int n1 = 0; n1 < C::R1x; ++n1) {
+            const int x = n2 + C::R2x * n1;
+            const int ox = tile * a.QX + x - (a.mx - 1);
+            if (x >= a.mx - 1 && ox < a.OW) dst[ox] = wa[n1];
+            if (x + 1 >= a.mx - 1 && ox + 1 < a.OW) dst[ox + 1] = wb[n1];
           }
-          dft<C::R1y, true>(w);
-          const int ox = tx * a.QX + x - (a.mx - 1);
-          if (x >= a.mx - 1 && ox < a.OW) {
+        }
+      }
+    }
+    __syncthreads();
+    if constexpr (TWO_D) {
+      // column pairs entirely left of the valid window are not needed any more
+      const int xp_min = (a.mx - 1) / 2;
+      // ---------------- inverse y, pass B: item (xp, k1)
 #pragma unroll
-            for (int n1 = 0; n1 < C::R1y; ++n1) {
-              const int y = n2 + C::R2y * n1;
-              const int oy = ty * a.QY + y - (a.my - 1);
-              if (y >= a.my - 1 && oy < a.OH) dst[(size_t)oy * a.OW + ox] = w[n1];
+      for (int g = 0; g < C::G_yB; ++g) {
+        const int i = tid + NT * g;
+        const int xp = i % C::XP, k1 = i / C::XP;
+        if (xp < xp_min) continue;
+        float2 wa[C::R2y], wb[C::R2y];
+#pragma unroll
+        for (int k2 = 0; k2 < C::R2y; ++k2) {
+          const float4 p = ld2(k2 + C::R2y * k1, 2 * xp);
+          wa[k2] = make_float2(p.x, p.y);
+          wb[k2] = make_float2(p.z, p.w);
+        }
+        dft<C::R2y, true>(wa);
+        dft<C::R2y, true>(wb);
+#pragma unroll
+        for (int n2 = 0; n2 < C::R2y; ++n2) st2(n2 + C::R2y * k1, 2 * xp, wa[n2], wb[n2]);
+      }
+      __syncthreads();
+      // ---------------- inverse y, pass A + store of the valid window: item (xp, n2)
+      float2* dst = a.chat + ((size_t)img * a.K + k) * (size_t)a.OH * a.OW;
+#pragma unroll
+      for (int g = 0; g < C::G_yA; ++g) {
+        const int i = tid + NT * g;
+        const int xp = i % C::XP, n2 = i / C::XP;
+        if (xp < xp_min) continue;
+        float2 wa[C::R1y], wb[C::R1y];
+#pragma unroll
+        for (int k1 = 0; k1 < C::R1y; ++k1) {
+          const float4 p = ld2(n2 + C::R2y * k1, 2 * xp);
+          wa[k1] = make_float2(p.x, p.y);
+          wb[k1] = make_float2(p.z, p.w);
+          if (k1 != 0) {
+            const float2 w = c_tw[TwOff<PY>::v + n2 * k1];
+            wa[k1] = cmulc(wa[k1], w);
+            wb[k1] = cmulc(wb[k1], w);
+          }
+        }
+        dft<C::R1y, true>(wa);
+        dft<C::R1y, true>(wb);
+        const int x = 2 * xp;
+        const int ox = tx * a.QX + x - (a.mx - 1);
+        const bool va = x >= a.mx - 1 && ox < a.OW;
+        const bool vb = x + 1 >= a.mx - 1 && ox + 1 < a.OW;
+#pragma unroll
+        for (int n1 = 0; n1 < C::R1y; ++n1) {
+          const int y = n2 + C::R2y * n1;
+          const int oy = ty * a.QY + y - (a.my - 1);
+          if (y >= a.my - 1 && oy < a.OH) {
+            const size_t o = (size_t)oy * a.OW + ox;
+            float2* row = dst + o;
+            if (va && vb && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+              *reinterpret_cast<float4*>(row) = make_float4(wa[n1].x, wa[n1].y, wb[n1].x, wb[n1].y);
+            } else {
+              if (va) row[0] = wa[n1];
+              if (vb) row[1] = wb[n1];
             }
           }
         }
-        __syncthreads();
       }
+      __syncthreads();
     }
   }
 }
