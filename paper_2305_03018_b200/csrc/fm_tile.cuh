@@ -384,8 +384,8 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
         }
       }
     }
-    __syncthreads();
     if constexpr (TWO_D) {
+      __syncthreads();
       // column pairs entirely left of the valid window are not needed any more
       const int xp_min = (a.mx - 1) / 2;
       // ---------------- inverse y, pass B: item (xp, k1)
@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
           }
         }
       }
-      __syncthreads();
+      // no barrier: the next plane's y pass A writes exactly the positions this
+      // thread just read (same item partition), and no other thread reads them
     }
   }
 }

@@ -1,0 +1,13 @@
+#!/bin/bash
+# usage: bash scripts/gpu_profile.sh TAG  -> full bench line, launch list and one ncu --set full capture
+TAG=${1:-run}
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench_full_$TAG.log 2>&1; echo bench_rc=$? >> gpurun_out/bench_full_$TAG.log
+timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/plain_$TAG.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
+   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launches_$TAG.log 2>&1
+echo launches_rc=$? >> gpurun_out/ncu_launches_$TAG.log
+timeout 300 python bench.py --images 4 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/bench_small_$TAG.log 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tile_conv_kernel|tonal_kernel_t" -s 5 -c 2 -o gpurun_out/prof_$TAG \
+   python bench.py --images 4 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_$TAG.log 2>&1
+echo ncu_rc=$? >> gpurun_out/ncu_$TAG.log
