@@ -98,6 +98,11 @@ struct TileCfg {
   static_assert(G_xA >= 1 && G_xA * NT == PY * (R2x / 2) && G_xB >= 1 && G_xB * NT == PY * R1x,
                 "x-axis item split");
   static_assert(PX >= 16, "min tile edge 16");
+  // x-axis passes: warp w owns rows [w*RPW, (w+1)*RPW), so the x pass A <-> B
+  // exchanges stay inside one warp (__syncwarp instead of a CTA barrier)
+  static constexpr int NW = NT / 32;
+  static constexpr int RPW = PY / NW;
+  static_assert(RPW * NW == PY && RPW * (R2x / 2) == 32 && G_xA == 1, "x pass A: one item per lane");
   static constexpr int kBufBytes = PY * RS * 8;
   static constexpr int kSpecPairs = NPTS / 2;           // float4 per tonal plane
   static constexpr int SQ = R2x / 2;                    // float4 per x-pass-B item
@@ -105,7 +110,13 @@ struct TileCfg {
   static constexpr int NBUF = G_xB >= 2 ? 2 : 1;
   static constexpr int kSpecBytes = NBUF * kChunkF4 * 16;
   static constexpr int kTvBytes = ((NPTS * 2 + 15) / 16) * 16;
-  static constexpr int kSmemFixed = kBufBytes + kSpecBytes + kTvBytes;
+  // x pass A twiddle pairs (W^{n2 k1}, W^{(n2+1) k1}) for the R2x/2 pair columns:
+  // 16-byte slots, stride R1x+1 (conflict-free for the 4..8 distinct n2 of a
+  // warp).  In 2-D they live in the row padding (free), in 1-D after the tiles.
+  static constexpr int kTwxSlots = (R2x / 2) * (R1x + 1);
+  static constexpr bool kTwxInPad = kTwxSlots <= PY;
+  static constexpr int kTwxBytes = kTwxInPad ? 0 : kTwxSlots * 16;
+  static constexpr int kSmemFixed = kBufBytes + kSpecBytes + kTvBytes + kTwxBytes;
 };
 
 __device__ __forceinline__ int load_img(const void* img, int dtype, int64_t i) {
@@ -143,6 +154,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   };
 
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int img = SPEC ? 0 : blockIdx.z;
   const int T = a.T;
 
@@ -188,6 +200,18 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
       tv[p] = t;
     }
     if (!SPEC && bad) atomicOr(a.err, 1);
+  }
+  // x pass A twiddle pairs
+  auto twx_slot = [&](int j) -> float4* {
+    if constexpr (C::kTwxInPad) return reinterpret_cast<float4*>(buf + j * RS + PX);
+    else return reinterpret_cast<float4*>(smem_raw + C::kBufBytes + C::kSpecBytes + C::kTvBytes) + j;
+  };
+  for (int j = tid; j < C::kTwxSlots; j += NT) {
+    const int n2p = j / (C::R1x + 1), k1 = j - n2p * (C::R1x + 1);
+    const int n2 = 2 * n2p;
+    const float2 w0 = c_tw[TwOff<PX>::v + (n2 * k1) % PX];
+    const float2 w1 = c_tw[TwOff<PX>::v + ((n2 + 1) * k1) % PX];
+    *twx_slot(j) = make_float4(w0.x, w0.y, w1.x, w1.y);
   }
   __syncthreads();
   const int ty = (TWO_D && !SPEC) ? blockIdx.x / a.tiles_x : 0;
@@ -274,8 +298,8 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     // ---------------- forward x, pass A: item (y, n2 pair); 1-D: with encode
 #pragma unroll
     for (int g = 0; g < C::G_xA; ++g) {
-      const int i = tid + NT * g;
-      const int y = i % PY, n2 = 2 * (i / PY);
+      const int i = lane + 32 * g;
+      const int y = warp * C::RPW + i % C::RPW, n2 = 2 * (i / C::RPW);
       float2 wa[C::R1x], wb[C::R1x];
 #pragma unroll
       for (int n1 = 0; n1 < C::R1x; ++n1) {
@@ -295,21 +319,22 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
       for (int k1 = 0; k1 < C::R1x; ++k1) {
         float2 za = wa[k1], zb = wb[k1];
         if (k1 != 0) {
-          za = cmul(za, c_tw[TwOff<PX>::v + n2 * k1]);
-          zb = cmul(zb, c_tw[TwOff<PX>::v + (n2 + 1) * k1]);
+          const float4 w = *twx_slot((n2 / 2) * (C::R1x + 1) + k1);
+          za = cmul(za, make_float2(w.x, w.y));
+          zb = cmul(zb, make_float2(w.z, w.w));
         }
         st2(y, n2 + C::R2x * k1, za, zb);
       }
     }
-    __syncthreads();
+    __syncwarp();   // x pass B reads only rows owned by this warp
 
     // ---------------- forward x, pass B (+ spectral product + inverse x pass B): item (y, k1)
     {
       float4* so = SPEC ? a.spec_out + (size_t)k * C::kSpecPairs : nullptr;
 #pragma unroll
       for (int g = 0; g < C::G_xB; ++g) {
-        const int i = tid + NT * g;
-        const int y = i % PY, k1 = i / PY;
+        const int i = lane + 32 * g;
+        const int y = warp * C::RPW + i % C::RPW, k1 = i / C::RPW;
         float2 w[C::R2x];
 #pragma unroll
         for (int q = 0; q < C::SQ; ++q) {
@@ -345,14 +370,17 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
         }
       }
     }
-    __syncthreads();
-    if constexpr (SPEC) continue;
+    if constexpr (SPEC) {
+      __syncthreads();
+      continue;
+    }
+    __syncwarp();   // inverse x pass A reads only rows owned by this warp
 
     // ---------------- inverse x, pass A: item (y, n2 pair); 1-D: output store
 #pragma unroll
     for (int g = 0; g < C::G_xA; ++g) {
-      const int i = tid + NT * g;
-      const int y = i % PY, n2 = 2 * (i / PY);
+      const int i = lane + 32 * g;
+      const int y = warp * C::RPW + i % C::RPW, n2 = 2 * (i / C::RPW);
       float2 wa[C::R1x], wb[C::R1x];
 #pragma unroll
       for (int k1 = 0; k1 < C::R1x; ++k1) {
@@ -360,8 +388,9 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
         wa[k1] = make_float2(p.x, p.y);
         wb[k1] = make_float2(p.z, p.w);
         if (k1 != 0) {
-          wa[k1] = cmulc(wa[k1], c_tw[TwOff<PX>::v + n2 * k1]);
-          wb[k1] = cmulc(wb[k1], c_tw[TwOff<PX>::v + (n2 + 1) * k1]);
+          const float4 w = *twx_slot((n2 / 2) * (C::R1x + 1) + k1);
+          wa[k1] = cmulc(wa[k1], make_float2(w.x, w.y));
+          wb[k1] = cmulc(wb[k1], make_float2(w.z, w.w));
         }
       }
       dft<C::R1x, true>(wa);
