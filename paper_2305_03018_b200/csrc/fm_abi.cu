@@ -19,6 +19,7 @@
 
 #include "fftmorph_b200.h"
 #include "fm_naive.cuh"
+#include "fm_range.cuh"
 #include "fm_tile.cuh"
 #include "fm_tonal.cuh"
 
@@ -219,7 +220,20 @@ struct fm_plan {
   std::vector<std::pair<int, int>> pending_conv, pending_tonal;  // (start, stop) indices into ev_pool
   size_t ev_next = 0;
   fm_timing acc{};
-  double conv_bytes_per_img = 0, tonal_bytes_per_img = 0, conv_flops_per_img = 0;
+  double conv_flops_per_plane = 0;  // per unit and plane
+  // per-unit tonal length: ladder of supported N (ascending), one SE spectrum each
+  std::vector<int> ladder;
+  std::vector<int64_t> spec_off;          // float4 offsets into spec
+  std::vector<const TonalVariant*> ladder_var;
+  int units = 1, wpx = 1, win_y = 1, win_x = 1, unit_step_x = 0;
+  int* d_ladder = nullptr;
+  int64_t* d_spec_off = nullptr;
+  int4* unit_param = nullptr;             // [ipc][units]
+  int* bucket_count = nullptr;            // [L]
+  int2* bucket_list = nullptr;            // [L][ipc*units]
+  int* h_counts = nullptr;                // pinned [L]
+  cudaEvent_t count_ev = nullptr;
+  int64_t planes_done = 0, units_done = 0; // for the plan's mean planes per unit
 };
 
 namespace {
@@ -241,6 +255,13 @@ void free_plan(fm_plan* p) {
   cudaFree(p->h_out);
   cudaFree(p->h_valid);
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+  cudaFree(p->d_ladder);
+  cudaFree(p->d_spec_off);
+  cudaFree(p->unit_param);
+  cudaFree(p->bucket_count);
+  cudaFree(p->bucket_list);
+  if (p->h_counts) cudaFreeHost(p->h_counts);
+  if (p->count_ev) cudaEventDestroy(p->count_ev);
   cudaSetDevice(prev);
   delete p;
 }
@@ -434,33 +455,56 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   p->conv_smem = bv->smem_fixed;
   if (p->conv_smem > kSmemLimit) { free_plan(p); return fail(FM_EUNSUPPORTED, "tile too large for shared memory"); }
 
-  // tonal kernel geometry
-  p->tonal_var = find_tonal(p->N);
+  // tonal ladder: each conv unit uses the smallest N_t of the ladder with
+  // 2 N_t > its own l_R (fm_range.cuh); a forced tonal_len pins a single entry
+  if (d.tonal_len > 0) {
+    p->ladder = {p->N};
+  } else {
+    for (int i = 0; i < kTonalCount; ++i)
+      if (kTonalNs[i] < p->N) p->ladder.push_back(kTonalNs[i]);
+    p->ladder.push_back(p->N);
+  }
+  for (int n : p->ladder) p->ladder_var.push_back(find_tonal(n));
+  // generic tonal kernel (N beyond the compiled set): geometry for N_global
   p->tonal_stride = (p->N + 1) | 1;
   int nt = 128;
   while (nt > 32 && (size_t)(2 * p->N + 2 * (size_t)nt * p->tonal_stride) * 8 > 200 * 1024) nt -= 32;
   p->tonal_threads = nt;
   p->tonal_smem = (size_t)(2 * p->N + 2 * (size_t)nt * p->tonal_stride) * 8;
-  if (p->tonal_smem > kSmemLimit) { free_plan(p); return fail(FM_EUNSUPPORTED, "tonal length too large for the tonal kernel"); }
+  if (!p->ladder_var.back() && p->tonal_smem > kSmemLimit) {
+    free_plan(p);
+    return fail(FM_EUNSUPPORTED, "tonal length too large for the tonal kernel");
+  }
+
+  // conv units: one 2-D tile, or PY consecutive 1-D tiles (one CTA)
+  if (p->two_d) {
+    p->units = p->tiles_total;
+    p->wpx = p->QY * p->QX;
+    p->win_y = p->PY;
+    p->win_x = p->PX;
+  } else {
+    p->units = p->tile_ctas;
+    p->wpx = p->PY * p->QX;
+    p->win_y = 1;
+    p->win_x = (p->PY - 1) * p->QX + p->PX;
+    p->unit_step_x = p->PY * p->QX;
+  }
 
   // spectral scratch and launch chunking
-  const int64_t per_img = (int64_t)p->K * p->OH * p->OW * 8;
+  const int64_t per_img = (int64_t)p->units * p->K * p->wpx * 8;
   const int64_t budget = d.scratch_bytes > 0 ? d.scratch_bytes : (int64_t)4 << 30;
   p->ipc = std::max<int64_t>(1, std::min<int64_t>(p->batch, budget / std::max<int64_t>(per_img, 1)));
+  if (p->ipc > 65535) p->ipc = 65535;
   const int occ = p->two_d ? std::max(1, (kSmemLimit) / (int)(p->conv_smem + 1024)) : 2;
   const int64_t target = 148LL * 2 * occ;
   const int64_t base = (int64_t)p->tile_ctas * p->ipc;
   int kch = (int)std::min<int64_t>(p->K, std::max<int64_t>(1, (target + base - 1) / base));
   p->k_chunk = (p->K + kch - 1) / kch;
   p->kchunks = (p->K + p->k_chunk - 1) / p->k_chunk;
-
   {
-    const double npx = (double)p->OH * p->OW;
-    const double in_b = (double)p->H * p->W * dtype_size(d.img_dtype);
-    p->conv_bytes_per_img = in_b + (double)p->K * npx * 8.0;
-    p->tonal_bytes_per_img = (double)p->K * npx * 8.0 + npx * 4.0;
     const double pts = p->two_d ? (double)p->PY * p->PX : (double)p->PX;
-    p->conv_flops_per_img = (double)p->tiles_total * p->K * (2.0 * 5.0 * pts * std::log2(pts) + 6.0 * pts);
+    const double tiles_per_unit = p->two_d ? 1.0 : (double)p->PY;
+    p->conv_flops_per_plane = tiles_per_unit * (2.0 * 5.0 * pts * std::log2(pts) + 6.0 * pts);
   }
   DeviceGuard dg(p->device);
   rc = ensure_twiddles(p->device);
@@ -472,7 +516,23 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   cudaError_t e;
 
   const size_t npts = (size_t)p->PY * p->PX;
-  if ((e = cudaMalloc(&p->spec, sizeof(float2) * npts * p->K)) != cudaSuccess) return cfail(e, "spec alloc");
+  const int L = (int)p->ladder.size();
+  int64_t spec_f4 = 0;
+  for (int n : p->ladder) {
+    p->spec_off.push_back(spec_f4);
+    spec_f4 += (int64_t)(n + 1) * (int64_t)(npts / 2);
+  }
+  const int64_t cap = p->ipc * p->units;
+  if ((e = cudaMalloc(&p->spec, sizeof(float4) * spec_f4)) != cudaSuccess) return cfail(e, "spec alloc");
+  if ((e = cudaMalloc(&p->d_ladder, sizeof(int) * L)) != cudaSuccess) return cfail(e, "ladder alloc");
+  if ((e = cudaMalloc(&p->d_spec_off, sizeof(int64_t) * L)) != cudaSuccess) return cfail(e, "ladder alloc");
+  if ((e = cudaMalloc(&p->unit_param, sizeof(int4) * cap)) != cudaSuccess) return cfail(e, "unit alloc");
+  if ((e = cudaMalloc(&p->bucket_count, sizeof(int) * L)) != cudaSuccess) return cfail(e, "bucket alloc");
+  if ((e = cudaMalloc(&p->bucket_list, sizeof(int2) * cap * L)) != cudaSuccess) return cfail(e, "bucket alloc");
+  if ((e = cudaMallocHost(&p->h_counts, sizeof(int) * L)) != cudaSuccess) return cfail(e, "pinned alloc");
+  if ((e = cudaEventCreateWithFlags(&p->count_ev, cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+  cudaMemcpy(p->d_ladder, p->ladder.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
+  cudaMemcpy(p->d_spec_off, p->spec_off.data(), sizeof(int64_t) * L, cudaMemcpyHostToDevice);
   if ((e = cudaMalloc(&p->twN, sizeof(float2) * std::max(1, p->N))) != cudaSuccess) return cfail(e, "table alloc");
   if ((e = cudaMalloc(&p->wT, sizeof(float2) * std::max(1, p->N))) != cudaSuccess) return cfail(e, "table alloc");
   if ((e = cudaMalloc(&p->stats, sizeof(int) * 4)) != cudaSuccess) return cfail(e, "stats alloc");
@@ -494,32 +554,36 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   cudaMemcpy(p->se_def_d, sd.data(), se_n, cudaMemcpyHostToDevice);
   cudaMemset(p->stats, 0, sizeof(int) * 4);
 
-  // SE spectrum: same encode + forward passes as the image tiles, scaled by
-  // 1/(PY_eff * PX * T) so the inverse transforms need no normalisation.
-  TileArgs a{};
-  a.se_vals = p->se_vals_d;
-  a.se_def = p->se_def_d;
-  a.H = 1;
-  a.W = 1;
-  a.my = p->my;
-  a.mx = p->mx;
-  a.T = T;
-  a.K = p->K;
-  a.magicT = (uint32_t)((1ull << 32) / (uint64_t)T);
-  a.k_chunk = 1;
-  a.enc_sign = 1;
-  a.enc_bias = -smin;
-  a.vmax = 1 << 30;
-  a.two_pi_over_T = (float)(2.0 * kPi / T);
-  a.spec = p->spec;
-  a.spec_out = p->spec;
-  a.spec_scale = (float)(1.0 / ((double)(p->two_d ? p->PY : 1) * p->PX * T));
-  a.tiles_x = 1;
-  a.tiles_total = 1;
-  a.err = p->stats + 1;
-  bv->spec(dim3(1, p->K, 1), p->conv_smem, 0, a);
-  g_launches++;
-  if ((e = cudaGetLastError()) != cudaSuccess) return cfail(e, "SE spectrum launch");
+  // SE spectra, one per ladder entry: same encode + forward passes as the image
+  // tiles, scaled by 1/(PY_eff * PX * T) so the inverse transforms need no
+  // normalisation.
+  for (int li = 0; li < L; ++li) {
+    const int Tl = 2 * p->ladder[li];
+    TileArgs a{};
+    a.se_vals = p->se_vals_d;
+    a.se_def = p->se_def_d;
+    a.H = 1;
+    a.W = 1;
+    a.my = p->my;
+    a.mx = p->mx;
+    a.T = Tl;
+    a.K = p->ladder[li] + 1;
+    a.magicT = (uint32_t)((1ull << 32) / (uint64_t)Tl);
+    a.k_chunk = 1;
+    a.enc_sign = 1;
+    a.enc_bias = -smin;
+    a.vmax = 1 << 30;
+    a.two_pi_over_T = (float)(2.0 * kPi / Tl);
+    a.spec = p->spec + p->spec_off[li];
+    a.spec_out = p->spec + p->spec_off[li];
+    a.spec_scale = (float)(1.0 / ((double)(p->two_d ? p->PY : 1) * p->PX * Tl));
+    a.tiles_x = 1;
+    a.tiles_total = 1;
+    a.err = p->stats + 1;
+    bv->spec(dim3(1, a.K, 1), p->conv_smem, 0, a);
+    g_launches++;
+    if ((e = cudaGetLastError()) != cudaSuccess) return cfail(e, "SE spectrum launch");
+  }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cfail(e, "SE spectrum");
   *out_plan = p;
   return FM_OK;
@@ -543,7 +607,7 @@ int fm_plan_query(const fm_plan* p, fm_plan_info* info) {
   info->out_lo_offset[0] = p->two_d ? p->off_y : p->off_x;
   info->out_lo_offset[1] = p->two_d ? p->off_x : 0;
   info->images_per_launch = p->ipc;
-  info->scratch_bytes = (int64_t)p->K * p->OH * p->OW * 8 * p->ipc;
+  info->scratch_bytes = (int64_t)p->units * p->K * p->wpx * 8 * p->ipc;
   info->se_min = p->se_min;
   info->se_max = p->se_max;
   info->se_count = p->se_count;
@@ -566,8 +630,45 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
   const int64_t npix = p->OH * p->OW;
   const int64_t img_elems = p->H * p->W;
   const int dsz = dtype_size(p->d.img_dtype);
+  const int L = (int)p->ladder.size();
+  const int64_t cap = p->ipc * p->units;
   for (int64_t c0 = 0; c0 < p->batch; c0 += p->ipc) {
     const int n = (int)std::min<int64_t>(p->ipc, p->batch - c0);
+    // ---- per-unit tonal range -> ladder entry + work lists (fm_range.cuh)
+    FM_CUDA(cudaMemsetAsync(p->bucket_count, 0, sizeof(int) * L, s));
+    RangeArgs r{};
+    r.img = reinterpret_cast<const char*>(img) + (size_t)c0 * img_elems * dsz;
+    r.img_def = img_defined ? img_defined + (size_t)c0 * img_elems : nullptr;
+    r.img_dtype = p->d.img_dtype;
+    r.H = (int)p->H;
+    r.W = (int)p->W;
+    r.two_d = p->two_d ? 1 : 0;
+    r.DY = p->DY;
+    r.DX = p->DX;
+    r.QY = p->QY;
+    r.QX = p->QX;
+    r.win_y = p->win_y;
+    r.win_x = p->win_x;
+    r.tiles_x = p->tiles_x;
+    r.units = p->units;
+    r.unit_step_x = p->unit_step_x;
+    r.img_min = p->d.img_min;
+    r.img_max = p->d.img_max;
+    r.enc_sign = p->enc_sign;
+    r.lr_se = p->se_max - p->se_min;
+    r.ladder = p->d_ladder;
+    r.L = L;
+    r.unit_param = p->unit_param;
+    r.bucket_count = p->bucket_count;
+    r.bucket_list = p->bucket_list;
+    r.cap = (int)cap;
+    r.err = p->stats + 1;
+    range_kernel<<<dim3((unsigned)p->units, n), 256, 0, s>>>(r);
+    g_launches++;
+    FM_CUDA(cudaGetLastError());
+    FM_CUDA(cudaMemcpyAsync(p->h_counts, p->bucket_count, sizeof(int) * L, cudaMemcpyDeviceToHost, s));
+    FM_CUDA(cudaEventRecord(p->count_ev, s));
+
     TileArgs a{};
     a.img = reinterpret_cast<const char*>(img) + (size_t)c0 * img_elems * dsz;
     a.img_def = img_defined ? img_defined + (size_t)c0 * img_elems : nullptr;
@@ -595,6 +696,11 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
     a.spec = p->spec;
     a.chat = p->chat;
     a.err = p->stats + 1;
+    a.unit_param = p->unit_param;
+    a.spec_off = p->d_spec_off;
+    a.units = p->units;
+    a.K_max = p->K;
+    a.wpx = p->wpx;
     int e0 = -1;
     if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
     p->var->conv(dim3(p->tile_ctas, p->kchunks, n), p->conv_smem, s, a);
@@ -603,42 +709,66 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
     if (p->timing) {
       FM_CUDA(cudaEventRecord(next_event(p), s));
       p->pending_conv.push_back({e0, e0 + 1});
-      p->acc.conv_bytes += p->conv_bytes_per_img * n;
-      p->acc.conv_flops += p->conv_flops_per_img * n;
     }
 
+    // ---- the tonal kernels need the per-ladder unit counts (ready long before
+    // the conv kernel finishes; the host waits only for the small copy)
+    FM_CUDA(cudaEventSynchronize(p->count_ev));
     TonalArgs t{};
     t.chat = p->chat;
-    t.npix = npix;
-    t.K = p->K;
-    t.N = p->N;
-    t.T = p->T;
-    t.nstages = (int)p->radix.size();
-    for (size_t i = 0; i < p->radix.size(); ++i) t.radix[i] = p->radix[i];
-    t.twN = p->twN;
-    t.wT = p->wT;
+    t.K_max = p->K;
+    t.unit_param = p->unit_param;
+    t.units = p->units;
+    t.wpx = p->wpx;
+    t.two_d = p->two_d ? 1 : 0;
+    t.QY = p->QY;
+    t.QX = p->QX;
+    t.OH = (int)p->OH;
+    t.OW = (int)p->OW;
+    t.tiles_x = p->tiles_x;
+    t.unit_step_x = p->unit_step_x;
     t.out = out + (size_t)c0 * npix;
     t.valid = valid ? valid + (size_t)c0 * npix : nullptr;
     t.out_sign = p->out_sign;
-    t.out_bias = p->out_bias;
+    t.se_min = p->se_min;
     t.fill = p->d.fill;
-    t.stride = p->tonal_stride;
     t.dev_max = reinterpret_cast<float*>(p->stats);
     int e1 = -1;
     if (p->timing) { e1 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
-    if (p->tonal_var) {
-      const int nt = p->tonal_var->nt;
-      p->tonal_var->fn(dim3((unsigned)((npix + nt - 1) / nt), n), nt, p->tonal_var->smem, s, t);
-    } else {
-      const int nt = p->tonal_threads;
-      tonal_kernel<<<dim3((unsigned)((npix + nt - 1) / nt), n), nt, p->tonal_smem, s>>>(t);
+    double planes = 0, tonal_b = 0;
+    for (int li = 0; li < L; ++li) {
+      const int cnt = p->h_counts[li];
+      if (cnt <= 0) continue;
+      const int N = p->ladder[li];
+      t.N = N;
+      t.T = 2 * N;
+      t.list = p->bucket_list + (size_t)li * cap;
+      const TonalVariant* tv = p->ladder_var[li];
+      if (tv) {
+        const int nt = tv->nt;
+        tv->fn(dim3((unsigned)cnt, (unsigned)((p->wpx + nt - 1) / nt)), nt, tv->smem, s, t);
+      } else {
+        t.nstages = (int)p->radix.size();
+        for (size_t i = 0; i < p->radix.size(); ++i) t.radix[i] = p->radix[i];
+        t.twN = p->twN;
+        t.wT = p->wT;
+        t.stride = p->tonal_stride;
+        const int nt = p->tonal_threads;
+        tonal_kernel<<<dim3((unsigned)cnt, (unsigned)((p->wpx + nt - 1) / nt)), nt, p->tonal_smem, s>>>(t);
+      }
+      g_launches++;
+      FM_CUDA(cudaGetLastError());
+      planes += (double)cnt * (N + 1);
+      tonal_b += (double)cnt * ((N + 1) * (double)p->wpx * 8.0 + (double)p->wpx * (4.0 + (valid ? 1.0 : 0.0)));
     }
-    g_launches++;
-    FM_CUDA(cudaGetLastError());
+    p->planes_done += (int64_t)planes;
+    p->units_done += (int64_t)n * p->units;
     if (p->timing) {
       FM_CUDA(cudaEventRecord(next_event(p), s));
       p->pending_tonal.push_back({e1, e1 + 1});
-      p->acc.tonal_bytes += (p->tonal_bytes_per_img + (valid ? (double)npix : 0.0)) * n;
+      p->acc.conv_bytes += (double)n * img_elems * dsz + planes * (double)p->wpx * 8.0;
+      p->acc.conv_flops += planes * p->conv_flops_per_plane;
+      p->acc.tonal_bytes += tonal_b;
     }
   }
   return FM_OK;

@@ -75,8 +75,14 @@ struct TileArgs {
   const float4* spec;         // [K][thread order] SE spectrum, pairs (CONV reads)
   float4* spec_out;           // SPEC writes
   float spec_scale;           // SPEC: 1 / (PY_eff * PX * T)
-  float2* chat;               // CONV: [imgs][K][OH*OW]
+  float2* chat;               // CONV: [imgs][units][K_max][wpx] (window-local pixels)
   int* err;                   // value-range error flag
+  // per-unit tonal length (CONV): a unit is one 2-D tile or one group of PY 1-D tiles
+  const int4* unit_param;     // [imgs][units]: x = anchor (min f, or max f for erosion), y = N_t, z = ladder index
+  const int64_t* spec_off;    // [ladder] offset of the SE spectrum for N = ladder[i] (float4 units)
+  int units;                  // units per image
+  int K_max;                  // chat planes per unit (N_global + 1)
+  int wpx;                    // window pixels per unit (QY*QX, or PY*QX in 1-D)
 };
 
 __constant__ float2 c_tw[kTwTotal];
@@ -156,7 +162,22 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int img = SPEC ? 0 : blockIdx.z;
-  const int T = a.T;
+  // tonal length of this unit: the SPEC launch is per ladder entry; a CONV unit
+  // uses the smallest ladder length that holds its own value range
+  int T = a.T, K = a.K, enc_bias = a.enc_bias;
+  uint32_t magicT = a.magicT;
+  float two_pi_over_T = a.two_pi_over_T;
+  const float4* spec_base = a.spec;
+  if constexpr (!SPEC) {
+    const int4 up = a.unit_param[(size_t)img * a.units + blockIdx.x];
+    K = up.y + 1;
+    if ((int)blockIdx.y * a.k_chunk >= K) return;   // this k-chunk is beyond the unit's planes
+    T = 2 * up.y;
+    magicT = (uint32_t)(0x100000000ull / (uint64_t)T);
+    two_pi_over_T = 6.28318530717958647692f / (float)T;
+    enc_bias = a.enc_sign > 0 ? -up.x : up.x;
+    spec_base = a.spec + a.spec_off[up.z];
+  }
 
   // ---- stage the tile's tonal indices v(x) (kSent = no entry)
   {
@@ -191,8 +212,8 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
         if (rowok && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
           const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
           if (a.img_def == nullptr || a.img_def[gi]) {
-            const int v = a.enc_sign * load_img(a.img, a.img_dtype, gi) + a.enc_bias;
-            if (v < 0 || v > a.vmax) bad = 1;
+            const int v = a.enc_sign * load_img(a.img, a.img_dtype, gi) + enc_bias;
+            if (v < 0 || v >= T) bad = 1;
             else t = (uint16_t)v;
           }
         }
@@ -217,11 +238,13 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   const int ty = (TWO_D && !SPEC) ? blockIdx.x / a.tiles_x : 0;
   const int tx = (TWO_D && !SPEC) ? blockIdx.x - ty * a.tiles_x : 0;
   const int k_begin = blockIdx.y * a.k_chunk;
-  const int k_end = min(a.K, k_begin + a.k_chunk);
+  const int k_end = min(K, k_begin + a.k_chunk);
+  // window-local output planes of this unit
+  float2* chat_unit = SPEC ? nullptr : a.chat + ((size_t)img * a.units + blockIdx.x) * a.K_max * (size_t)a.wpx;
 
   // per-thread spectrum chunk copy: item g of plane k -> buffer g % NBUF (own slots only)
   auto spec_fetch = [&](int k, int g) {
-    const float4* src = a.spec + (size_t)k * C::kSpecPairs + (size_t)g * C::kChunkF4 + tid;
+    const float4* src = spec_base + (size_t)k * C::kSpecPairs + (size_t)g * C::kChunkF4 + tid;
     float4* dst = sbuf + (g % C::NBUF) * C::kChunkF4 + tid;
 #pragma unroll
     for (int q = 0; q < C::SQ; ++q) cp_async16(dst + q * NT, src + q * NT);
@@ -239,11 +262,11 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     // Branch-free: the sentinel's (meaningless) angle is computed and then masked.
     auto enc = [&](uint32_t t) -> float2 {
       const uint32_t n = (uint32_t)k * t;
-      uint32_t r = n - __umulhi(n, a.magicT) * (uint32_t)T;
+      uint32_t r = n - __umulhi(n, magicT) * (uint32_t)T;
       r = (r >= (uint32_t)T) ? r - (uint32_t)T : r;
       const int rr = (2 * r > (uint32_t)T) ? (int)r - T : (int)r;
       float sn, cs;
-      __sincosf((float)rr * a.two_pi_over_T, &sn, &cs);
+      __sincosf((float)rr * two_pi_over_T, &sn, &cs);
       const bool live = t != kSent;
       return make_float2(live ? cs : 0.f, live ? -sn : 0.f);
     };
@@ -399,16 +422,17 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
 #pragma unroll
         for (int n1 = 0; n1 < C::R1x; ++n1) st2(y, n2 + C::R2x * n1, wa[n1], wb[n1]);
       } else {
-        // 1-D output: row y is tile (blockIdx.x*PY + y); positions x >= mx-1 are valid
+        // 1-D output: row y is tile (blockIdx.x*PY + y); positions x >= mx-1 are valid;
+        // window pixel p = y*QX + (x - (mx-1))
         const int tile = blockIdx.x * PY + y;
         if (tile < a.tiles_total) {
-          float2* dst = a.chat + ((size_t)img * a.K + k) * (size_t)a.OW;
+          float2* dst = chat_unit + ((ptrdiff_t)k * a.wpx + (ptrdiff_t)y * a.QX - (a.mx - 1));
 #pragma unroll
           for (int n1 = 0; n1 < C::R1x; ++n1) {
             const int x = n2 + C::R2x * n1;
             const int ox = tile * a.QX + x - (a.mx - 1);
-            if (x >= a.mx - 1 && ox < a.OW) dst[ox] = wa[n1];
-            if (x + 1 >= a.mx - 1 && ox + 1 < a.OW) dst[ox + 1] = wb[n1];
+            if (x >= a.mx - 1 && ox < a.OW) dst[x] = wa[n1];
+            if (x + 1 >= a.mx - 1 && ox + 1 < a.OW) dst[x + 1] = wb[n1];
           }
         }
       }
@@ -437,7 +461,8 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
       }
       __syncthreads();
       // ---------------- inverse y, pass A + store of the valid window: item (xp, n2)
-      float2* dst = a.chat + ((size_t)img * a.K + k) * (size_t)a.OH * a.OW;
+      // window pixel p = (y - (my-1)) * QX + (x - (mx-1))
+      float2* dst = chat_unit + ((ptrdiff_t)k * a.wpx - (ptrdiff_t)(a.my - 1) * a.QX - (a.mx - 1));
 #pragma unroll
       for (int g = 0; g < C::G_yA; ++g) {
         const int i = tid + NT * g;
@@ -466,8 +491,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
           const int y = n2 + C::R2y * n1;
           const int oy = ty * a.QY + y - (a.my - 1);
           if (y >= a.my - 1 && oy < a.OH) {
-            const size_t o = (size_t)oy * a.OW + ox;
-            float2* row = dst + o;
+            float2* row = dst + (size_t)y * a.QX + x;
             if (va && vb && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
               *reinterpret_cast<float4*>(row) = make_float4(wa[n1].x, wa[n1].y, wb[n1].x, wb[n1].y);
             } else {

@@ -9,7 +9,9 @@
 // (c2r packing), then
 //     value = max{ t : c(t) > 0.5 }   (np.rint(c) >= 1, umbra.py:198)
 //     valid = any t with c(t) > 0.5   (has_any, umbra.py:199)
-// and out = valid ? out_sign*value + out_bias : fill.  max|c - rint(c)| is
+// and out = valid ? out_sign*(value + se_min) + anchor : fill, where the anchor
+// is the unit's min f (dilation) or max f (erosion).  One launch per tonal
+// length of the plan's ladder covers the units that use it.  max|c - rint(c)| is
 // reduced block-wide and atomically into the plan's deviation slot.
 #pragma once
 #include "fm_dft.cuh"
@@ -17,19 +19,50 @@
 namespace fm {
 
 struct TonalArgs {
-  const float2* chat;  // [imgs][K][npix]
-  int64_t npix;        // OH*OW
-  int K, N, T;         // N = T/2
+  const float2* chat;     // [imgs][units][K_max][wpx] window-local planes
+  int K_max;              // planes per unit in chat
+  int N, T;               // this launch's tonal length T = 2N (one ladder entry)
   int nstages;
   int radix[12];
-  const float2* twN;   // [N] exp(+2 pi i j / N)
-  const float2* wT;    // [N] exp(+2 pi i k / T)
-  int32_t* out;        // [imgs][npix]
-  uint8_t* valid;      // nullable
-  int out_sign, out_bias, fill;
-  int stride;          // per-pixel smem stride (float2), odd
-  float* dev_max;      // max |c - rint c| (float bits, atomicMax as int)
+  const float2* twN;      // generic kernel: [N] exp(+2 pi i j / N)
+  const float2* wT;       // generic kernel: [N] exp(+2 pi i k / T)
+  const int2* list;       // units of this ladder entry: (img, unit)
+  const int4* unit_param; // [imgs][units]: x = anchor
+  int units, wpx;
+  int two_d, QY, QX, OH, OW, tiles_x, unit_step_x;
+  int32_t* out;           // [imgs][OH][OW]
+  uint8_t* valid;         // nullable
+  int out_sign, se_min, fill;
+  int stride;             // generic kernel: per-pixel smem stride (float2), odd
+  float* dev_max;         // max |c - rint c| (float bits, atomicMax as int)
 };
+
+// Pixel p of the work unit list[blockIdx.y]: chat offset, output offset, anchor.
+struct TonalPix {
+  bool live;
+  size_t src, dst;
+  int anchor;
+};
+__device__ __forceinline__ TonalPix tonal_pixel(const TonalArgs& a, int p) {
+  const int2 job = a.list[blockIdx.x];   // grid: x = work unit, y = pixel block
+  const int img = job.x, unit = job.y;
+  TonalPix r;
+  int oy, ox;
+  if (a.two_d) {
+    const int ty = unit / a.tiles_x, tx = unit - (unit / a.tiles_x) * a.tiles_x;
+    const int wy = p / a.QX, wx = p - (p / a.QX) * a.QX;
+    oy = ty * a.QY + wy;
+    ox = tx * a.QX + wx;
+  } else {
+    oy = 0;
+    ox = unit * a.unit_step_x + p;
+  }
+  r.live = p < a.wpx && oy < a.OH && ox < a.OW;
+  r.src = ((size_t)img * a.units + unit) * a.K_max * (size_t)a.wpx + p;
+  r.dst = ((size_t)img * a.OH + oy) * a.OW + ox;
+  r.anchor = r.live ? a.unit_param[(size_t)img * a.units + unit].x : 0;
+  return r;
+}
 
 template <int R>
 __device__ __forceinline__ void stockham_stage(const float2* in, float2* out, int N, int Ns,
@@ -163,16 +196,16 @@ __device__ __forceinline__ int tonal_threshold(const A& res, float& dev) {
 template <int N, bool SM, int NT>
 __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
   constexpr int off = tonal_off(N);
-  const int img = blockIdx.y;
-  const int64_t pix = (int64_t)blockIdx.x * NT + threadIdx.x;
+  const TonalPix pp = tonal_pixel(a, blockIdx.y * NT + threadIdx.x);
+  const size_t plane = a.wpx;
   float dev = 0.f;
-  if (pix < a.npix) {
-    const float2* src = a.chat + (size_t)img * a.K * a.npix + pix;
+  if (pp.live) {
+    const float2* src = a.chat + pp.src;
     int top;
     if constexpr (!SM) {
       float2 X[N + 1];
 #pragma unroll
-      for (int k = 0; k <= N; ++k) X[k] = __ldcs(src + (size_t)k * a.npix);
+      for (int k = 0; k <= N; ++k) X[k] = __ldcs(src + (size_t)k * plane);
       float2 A[N], B[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
@@ -187,8 +220,8 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
       SmemArr<NT> A{tsm_t + threadIdx.x}, B{tsm_t + (size_t)N * NT + threadIdx.x};
       // X[0..N-1] -> B, X[N] stays in a register
 #pragma unroll 8
-      for (int k = 0; k < N; ++k) B[k] = __ldcs(src + (size_t)k * a.npix);
-      const float2 xN = __ldcs(src + (size_t)N * a.npix);
+      for (int k = 0; k < N; ++k) B[k] = __ldcs(src + (size_t)k * plane);
+      const float2 xN = __ldcs(src + (size_t)N * plane);
 #pragma unroll 4
       for (int k = 0; k < N; ++k) {
         const float2 xk = B[k];
@@ -199,9 +232,8 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
       if constexpr (num_radices(N) % 2 == 0) top = tonal_threshold<N>(A, dev);
       else top = tonal_threshold<N>(B, dev);
     }
-    const size_t o = (size_t)img * a.npix + pix;
-    a.out[o] = top >= 0 ? a.out_sign * top + a.out_bias : a.fill;
-    if (a.valid) a.valid[o] = top >= 0 ? 1 : 0;
+    a.out[pp.dst] = top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill;
+    if (a.valid) a.valid[pp.dst] = top >= 0 ? 1 : 0;
   }
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
@@ -222,14 +254,14 @@ __global__ void __launch_bounds__(128) tonal_kernel(const TonalArgs a) {
   }
   __syncthreads();
 
-  const int img = blockIdx.y;
-  const int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const TonalPix pp = tonal_pixel(a, blockIdx.y * blockDim.x + threadIdx.x);
+  const size_t plane = a.wpx;
   float dev = 0.f;
-  if (pix < a.npix) {
-    const float2* src = a.chat + (size_t)img * a.K * a.npix + pix;
+  if (pp.live) {
+    const float2* src = a.chat + pp.src;
     float2* A = bufA + (size_t)threadIdx.x * a.stride;
     float2* B = bufB + (size_t)threadIdx.x * a.stride;
-    for (int k = 0; k <= N; ++k) A[k] = __ldcs(src + (size_t)k * a.npix);
+    for (int k = 0; k <= N; ++k) A[k] = __ldcs(src + (size_t)k * plane);
     // c2r packing: Z[k] = (X[k] + X[N-k]^*) + i w_T^{-k}... so that the
     // unnormalised length-N inverse DFT of Z gives z[n] = c(2n) + i c(2n+1).
     for (int k = 0; k < N; ++k) {
@@ -264,9 +296,8 @@ __global__ void __launch_bounds__(128) tonal_kernel(const TonalArgs a) {
       if (z.x > 0.5f) top = 2 * n;
       if (z.y > 0.5f) top = 2 * n + 1;
     }
-    const size_t o = (size_t)img * a.npix + pix;
-    a.out[o] = top >= 0 ? a.out_sign * top + a.out_bias : a.fill;
-    if (a.valid) a.valid[o] = top >= 0 ? 1 : 0;
+    a.out[pp.dst] = top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill;
+    if (a.valid) a.valid[pp.dst] = top >= 0 ? 1 : 0;
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, off));
