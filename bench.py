@@ -46,6 +46,22 @@ def _peaks():
         return {}
 
 
+def _ncu_traffic(images_per_launch):
+    """DRAM bytes per conv launch from the newest committed ncu capture of this workload
+    (profiles/r*_c5_tile_conv_tonal.json, written by scripts/ncu_summary.py)."""
+    files = sorted((ROOT / "profiles").glob("r*_c5_tile_conv_tonal.json"), key=lambda f: f.stat().st_mtime)
+    for f in reversed(files):
+        try:
+            data = json.loads(f.read_text())
+        except Exception:
+            continue
+        for k in data.get("kernels", []):
+            if k["kernel"].startswith("void tile_conv_kernel<128, 128, 512, 1, 0>") and "dram_bytes_per_launch" in k:
+                ipl = data.get("images_per_launch", 3)
+                return k["dram_bytes_per_launch"] * images_per_launch / ipl, f.name
+    return None, None
+
+
 def _gen(i):
     from paper_2305_03018_b200 import workloads as W
     return W.c5_image(i)
@@ -254,6 +270,9 @@ def run_ours(args, rank, world, local_rank):
     fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
     conv_tflops = tim["conv_flops"] / max(tim["conv_launches"], 1) / conv_s / 1e12 if conv_s > 0 else 0.0
     info = plan.info
+    traffic, traffic_src = _ncu_traffic(info["images_per_launch"])
+    fpp = 2.0 * 5.0 * 128 * 128 * math.log2(128 * 128) + 6.0 * 128 * 128
+    mean_planes = tim["conv_flops"] / fpp / (441 * args.images * args.steps) if tim["conv_flops"] else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -261,12 +280,13 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": f"c5: {args.images} x {EDGE}x{EDGE} 6-bit smooth-noise images, 31x31 non-flat SE "
                                "[0,15], exact dilation, sharded by image",
                    "images": args.images, "images_per_gpu": nloc, "tonal_len": info["tonal_len"],
-                   "planes": info["planes"], "tile": [info["tile_y"], info["tile_x"]],
+                   "planes_max": info["planes"], "mean_planes_per_tile": mean_planes,
+                   "tile": [info["tile_y"], info["tile_x"]],
                    "images_per_launch": info["images_per_launch"],
                    "l2": "no flush: inputs 256 MiB and the 1.37 GB/image spectral volume exceed the 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": "tile_conv_kernel (encode + 2-D FFT conv, fm_tile.cuh)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": None, "peak_source": peak_note,
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_note,
                      "bytes_per_launch": conv_bytes, "ms_per_launch": conv_s * 1000.0,
                      "fp32_tflops_nominal": conv_tflops, "fp32_peak_tflops_at_sm_mhz": fp32_peak,
                      "fp32_frac": conv_tflops / fp32_peak if fp32_peak else None,
