@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "fftmorph_b200.h"
+#include "fm_bigtile.cuh"
 #include "fm_naive.cuh"
 #include "fm_range.cuh"
 #include "fm_tile.cuh"
@@ -174,6 +175,11 @@ int set_all_smem_attrs() {
   }
   for (const TonalVariant& v : kTonal) FM_CUDA(v.attr());
   FM_CUDA(cudaFuncSetAttribute(tonal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+  FM_CUDA(cudaFuncSetAttribute(big_rows_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+  FM_CUDA(cudaFuncSetAttribute(big_rows_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+  FM_CUDA(cudaFuncSetAttribute(big_rows_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+  FM_CUDA(cudaFuncSetAttribute(big_cols_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+  FM_CUDA(cudaFuncSetAttribute(big_cols_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
   return FM_OK;
 }
 
@@ -234,6 +240,9 @@ struct fm_plan {
   int* h_counts = nullptr;                // pinned [L]
   cudaEvent_t count_ev = nullptr;
   int64_t planes_done = 0, units_done = 0; // for the plan's mean planes per unit
+  // 256x256 tiles through an HBM scratch (fm_bigtile.cuh) for wide SEs
+  bool big = false;
+  float2* S = nullptr;
 };
 
 namespace {
@@ -260,6 +269,7 @@ void free_plan(fm_plan* p) {
   cudaFree(p->unit_param);
   cudaFree(p->bucket_count);
   cudaFree(p->bucket_list);
+  cudaFree(p->S);
   if (p->h_counts) cudaFreeHost(p->h_counts);
   if (p->count_ev) cudaEventDestroy(p->count_ev);
   cudaSetDevice(prev);
@@ -436,14 +446,26 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
       bv = &v;
     }
   }
-  if (!bv) {
+  // 256x256 tiles (three kernels through HBM) pay ~1.7x per point but win for wide SEs
+  if (p->two_d && p->my <= kBig && p->mx <= kBig && (d.tile == 0 || d.tile == kBig)) {
+    const int q = kBig - p->mx + 1, qy = kBig - p->my + 1;
+    const double tx = std::ceil((double)p->OW / q), ty = std::ceil((double)p->OH / qy);
+    const double pts = (double)kBig * kBig;
+    const double cost = 1.7 * tx * ty * pts * (std::log2(pts) + 2.0) + tx * ty * 2048.0;
+    if (cost < best || d.tile == kBig) {
+      best = cost;
+      p->big = true;
+    }
+  }
+  if (!bv && !p->big) {
     free_plan(p);
     return fail(FM_EUNSUPPORTED, "structuring element larger than the largest FFT tile (" +
-                                     std::string(p->two_d ? "128x128" : "256") + ")");
+                                     std::string(p->two_d ? "256x256" : "256") + ")");
   }
+  if (p->big) bv = nullptr;
   p->var = bv;
-  p->PY = bv->py;
-  p->PX = bv->px;
+  p->PY = p->big ? kBig : bv->py;
+  p->PX = p->big ? kBig : bv->px;
   p->QX = p->PX - p->mx + 1;
   p->QY = p->two_d ? p->PY - p->my + 1 : 1;
   p->tiles_x = (int)((p->OW + p->QX - 1) / p->QX);
@@ -452,7 +474,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   p->tile_ctas = p->two_d ? p->tiles_total : (p->tiles_total + p->PY - 1) / p->PY;
 
   // shared memory (tile buffer + spectrum staging + tonal indices)
-  p->conv_smem = bv->smem_fixed;
+  p->conv_smem = p->big ? kBigColsSmem : bv->smem_fixed;
   if (p->conv_smem > kSmemLimit) { free_plan(p); return fail(FM_EUNSUPPORTED, "tile too large for shared memory"); }
 
   // tonal ladder: each conv unit uses the smallest N_t of the ladder with
@@ -491,7 +513,8 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   }
 
   // spectral scratch and launch chunking
-  const int64_t per_img = (int64_t)p->units * p->K * p->wpx * 8;
+  const int64_t per_img = (int64_t)p->units * p->K * p->wpx * 8 +
+                          (p->big ? (int64_t)p->units * p->K * kBig * kBig * 8 : 0);
   const int64_t budget = d.scratch_bytes > 0 ? d.scratch_bytes : (int64_t)4 << 30;
   p->ipc = std::max<int64_t>(1, std::min<int64_t>(p->batch, budget / std::max<int64_t>(per_img, 1)));
   if (p->ipc > 65535) p->ipc = 65535;
@@ -538,6 +561,12 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   if ((e = cudaMalloc(&p->stats, sizeof(int) * 4)) != cudaSuccess) return cfail(e, "stats alloc");
   if ((e = cudaMalloc(&p->se_vals_d, sizeof(int32_t) * se_n)) != cudaSuccess) return cfail(e, "se alloc");
   if ((e = cudaMalloc(&p->se_def_d, se_n)) != cudaSuccess) return cfail(e, "se alloc");
+  if (p->big &&
+      (e = cudaMalloc(&p->S, (size_t)p->ipc * p->units * p->K * kBig * kBig * 8 + (size_t)p->K * kBig * kBig * 8)) !=
+          cudaSuccess) {
+    free_plan(p);
+    return fail(FM_ENOMEM, std::string("tile scratch alloc: ") + cudaGetErrorString(e));
+  }
   if ((e = cudaMalloc(&p->chat, (size_t)per_img * p->ipc)) != cudaSuccess) {
     free_plan(p);
     return fail(FM_ENOMEM, std::string("spectral scratch alloc: ") + cudaGetErrorString(e));
@@ -557,7 +586,30 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   // SE spectra, one per ladder entry: same encode + forward passes as the image
   // tiles, scaled by 1/(PY_eff * PX * T) so the inverse transforms need no
   // normalisation.
-  for (int li = 0; li < L; ++li) {
+  for (int li = 0; li < L && p->big; ++li) {
+    // 256x256 tiles: forward x (rows kernel) then forward y + scaled store (cols kernel)
+    const int Tl = 2 * p->ladder[li];
+    BigArgs b{};
+    b.se_vals = p->se_vals_d;
+    b.se_def = p->se_def_d;
+    b.my = p->my;
+    b.mx = p->mx;
+    b.T = Tl;
+    b.K = p->ladder[li] + 1;
+    b.enc_sign = 1;
+    b.enc_bias = -smin;
+    b.units = 1;
+    b.K_max = b.K;
+    b.S = p->S + (size_t)p->ipc * p->units * p->K * kBig * kBig;   // spare slab after the batch scratch
+    b.spec = p->spec + p->spec_off[li];
+    b.spec_scale = (float)(1.0 / ((double)kBig * kBig * Tl));
+    b.err = p->stats + 1;
+    big_rows_kernel<true, true><<<dim3(kBig / kBigRows, b.K, 1), kBigNT, kBigRowsSmem>>>(b);
+    big_cols_kernel<true><<<dim3(kBig / kBigCols, b.K, 1), kBigColsNT, kBigColsSmem>>>(b);
+    g_launches += 2;
+    if ((e = cudaGetLastError()) != cudaSuccess) return cfail(e, "SE spectrum launch");
+  }
+  for (int li = 0; li < L && !p->big; ++li) {
     const int Tl = 2 * p->ladder[li];
     TileArgs a{};
     a.se_vals = p->se_vals_d;
@@ -703,8 +755,42 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
     a.wpx = p->wpx;
     int e0 = -1;
     if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
-    p->var->conv(dim3(p->tile_ctas, p->kchunks, n), p->conv_smem, s, a);
-    g_launches++;
+    if (p->big) {
+      BigArgs b{};
+      b.img = a.img;
+      b.img_def = a.img_def;
+      b.img_dtype = a.img_dtype;
+      b.H = a.H;
+      b.W = a.W;
+      b.OH = a.OH;
+      b.OW = a.OW;
+      b.DY = a.DY;
+      b.DX = a.DX;
+      b.QY = a.QY;
+      b.QX = a.QX;
+      b.my = a.my;
+      b.mx = a.mx;
+      b.tiles_x = a.tiles_x;
+      b.enc_sign = a.enc_sign;
+      b.unit_param = p->unit_param;
+      b.units = p->units;
+      b.K_max = p->K;
+      b.S = p->S;
+      b.spec = p->spec;
+      b.spec_off = p->d_spec_off;
+      b.chat = p->chat;
+      b.wpx = p->wpx;
+      b.err = p->stats + 1;
+      const unsigned z = (unsigned)(p->units * n);
+      const unsigned inv_blocks = (unsigned)((kBig - (p->my - 1) + kBigRows - 1) / kBigRows);
+      big_rows_kernel<true, false><<<dim3(kBig / kBigRows, p->K, z), kBigNT, kBigRowsSmem, s>>>(b);
+      big_cols_kernel<false><<<dim3(kBig / kBigCols, p->K, z), kBigColsNT, kBigColsSmem, s>>>(b);
+      big_rows_kernel<false, false><<<dim3(inv_blocks, p->K, z), kBigNT, kBigRowsSmem, s>>>(b);
+      g_launches += 3;
+    } else {
+      p->var->conv(dim3(p->tile_ctas, p->kchunks, n), p->conv_smem, s, a);
+      g_launches++;
+    }
     FM_CUDA(cudaGetLastError());
     if (p->timing) {
       FM_CUDA(cudaEventRecord(next_event(p), s));

@@ -58,17 +58,20 @@ __global__ void __launch_bounds__(256) range_kernel(const RangeArgs a) {
   }
   const int ya = max(y0, 0), yb = min(y0 + a.win_y, a.H);
   const int xa = max(x0, 0), xb = min(x0 + a.win_x, a.W);
-  const int w = max(xb - xa, 0);
-  const int n = max(yb - ya, 0) * w;
   int lo = INT32_MAX, hi = INT32_MIN, bad = 0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int yy = ya + i / w, xx = xa + i - (i / w) * w;
-    const int64_t gi = ((int64_t)img * a.H + yy) * a.W + xx;
-    if (a.img_def && !a.img_def[gi]) continue;
-    const int v = range_load(a.img, a.img_dtype, gi);
-    lo = min(lo, v);
-    hi = max(hi, v);
-    bad |= (v < a.img_min) | (v > a.img_max);
+  // warps stride over rows, lanes over columns: coalesced, no index division
+  const int nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int yy = ya + (int)(threadIdx.x >> 5); yy < yb; yy += nw) {
+    const int64_t rowbase = ((int64_t)img * a.H + yy) * a.W;
+#pragma unroll 4
+    for (int xx = xa + lane; xx < xb; xx += 32) {
+      const int64_t gi = rowbase + xx;
+      if (a.img_def && !a.img_def[gi]) continue;
+      const int v = range_load(a.img, a.img_dtype, gi);
+      lo = min(lo, v);
+      hi = max(hi, v);
+      bad |= (v < a.img_min) | (v > a.img_max);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

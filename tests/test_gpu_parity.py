@@ -296,7 +296,7 @@ def test_tile_and_tonal_length_invariance():
     sd[4, 6] = True
     w = W.Workload("x", img, se, sd, (-4, -2), 31, 5)
     ref, refv = cnaive.naive(img[0], None, se, sd, (-4, -2), crop=True, fill=0)
-    for tile in (16, 32, 64, 128):
+    for tile in (16, 32, 64, 128, 256):
         v, valid, dev, plan = _plan_run(w, "dilate", tile=tile)
         assert plan.info["tile_x"] == tile
         assert np.array_equal(v[0], ref) and np.array_equal(valid[0].astype(bool), refv), tile
@@ -304,6 +304,30 @@ def test_tile_and_tonal_length_invariance():
         v, valid, dev, plan = _plan_run(w, "dilate", tonal_len=T)
         assert plan.info["tonal_len"] == T
         assert np.array_equal(v[0], ref), T
+
+
+def test_wide_se_big_tiles():
+    """SEs wider than the 128 SMEM tile run on 256x256 tiles through HBM (fm_bigtile.cuh)."""
+    from paper_2305_03018_b200 import workloads as W
+    rng = np.random.default_rng(77)
+    img = rng.integers(0, 10, (2, 300, 283)).astype(np.uint8)
+    se = rng.integers(0, 3, (150, 141))
+    sd = rng.random((150, 141)) > 0.6
+    sd[75, 70] = True
+    w = W.Workload("x", img, se, sd, (-75, -60), 9, 4)
+    for mode in ("dilate", "erode"):
+        v, valid, dev, plan = _plan_run(w, mode)
+        assert plan.info["tile_x"] == 256
+        for i in range(2):
+            ref, refv = cnaive.naive(img[i], None, se, sd, (-75, -60), erode=(mode == "erode"), crop=True,
+                                     fill=0 if mode == "dilate" else 9)
+            assert np.array_equal(v[i], ref) and np.array_equal(valid[i].astype(bool), refv), (mode, i)
+    # drop-in API, gaps in the image, uncropped
+    f = random_grid(rng, (140, 170), 12, gap_p=0.1)
+    b = random_grid(rng, (131, 9), 3, gap_p=0.5, lo=(-70, -4))
+    d, dv = M().dilate_fft(f, b, crop=False, return_validity=True)
+    rv, rvv, lo = _naive_ref(f, b, crop=False)
+    assert d.lo == lo and np.array_equal(d.values, rv) and np.array_equal(dv, rvv)
 
 
 def test_batch_chunking_and_host_path():
