@@ -232,6 +232,7 @@ struct fm_plan {
   std::vector<int64_t> spec_off;          // float4 offsets into spec
   std::vector<const TonalVariant*> ladder_var;
   int units = 1, wpx = 1, win_y = 1, win_x = 1, unit_step_x = 0;
+  int upl = 1;                            // units per launch (chat slots per image)
   int* d_ladder = nullptr;
   int64_t* d_spec_off = nullptr;
   int4* unit_param = nullptr;             // [ipc][units]
@@ -513,14 +514,21 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   }
 
   // spectral scratch and launch chunking
-  const int64_t per_img = (int64_t)p->units * p->K * p->wpx * 8 +
-                          (p->big ? (int64_t)p->units * p->K * kBig * kBig * 8 : 0);
+  // scratch per unit: its K_max spectral planes (+ the 256^2 tile slab on the big path).
+  // Whole images per launch when they fit the budget, else chunks of units of one image.
+  const int64_t per_unit = (int64_t)p->K * p->wpx * 8 + (p->big ? (int64_t)p->K * kBig * kBig * 8 : 0);
   const int64_t budget = d.scratch_bytes > 0 ? d.scratch_bytes : (int64_t)4 << 30;
-  p->ipc = std::max<int64_t>(1, std::min<int64_t>(p->batch, budget / std::max<int64_t>(per_img, 1)));
-  if (p->ipc > 65535) p->ipc = 65535;
+  p->upl = (int)std::max<int64_t>(1, std::min<int64_t>(p->units, budget / std::max<int64_t>(per_unit, 1)));
+  if (p->upl < p->units) {
+    p->ipc = 1;
+  } else {
+    p->ipc = std::max<int64_t>(1, std::min<int64_t>(p->batch, budget / std::max<int64_t>(per_unit * p->units, 1)));
+    if (p->ipc > 65535) p->ipc = 65535;
+  }
+  const int64_t slots = p->ipc * p->upl;
   const int occ = p->two_d ? std::max(1, (kSmemLimit) / (int)(p->conv_smem + 1024)) : 2;
   const int64_t target = 148LL * 2 * occ;
-  const int64_t base = (int64_t)p->tile_ctas * p->ipc;
+  const int64_t base = (int64_t)p->upl * p->ipc;
   int kch = (int)std::min<int64_t>(p->K, std::max<int64_t>(1, (target + base - 1) / base));
   p->k_chunk = (p->K + kch - 1) / kch;
   p->kchunks = (p->K + p->k_chunk - 1) / p->k_chunk;
@@ -545,11 +553,11 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     p->spec_off.push_back(spec_f4);
     spec_f4 += (int64_t)(n + 1) * (int64_t)(npts / 2);
   }
-  const int64_t cap = p->ipc * p->units;
+  const int64_t cap = slots;
   if ((e = cudaMalloc(&p->spec, sizeof(float4) * spec_f4)) != cudaSuccess) return cfail(e, "spec alloc");
   if ((e = cudaMalloc(&p->d_ladder, sizeof(int) * L)) != cudaSuccess) return cfail(e, "ladder alloc");
   if ((e = cudaMalloc(&p->d_spec_off, sizeof(int64_t) * L)) != cudaSuccess) return cfail(e, "ladder alloc");
-  if ((e = cudaMalloc(&p->unit_param, sizeof(int4) * cap)) != cudaSuccess) return cfail(e, "unit alloc");
+  if ((e = cudaMalloc(&p->unit_param, sizeof(int4) * p->ipc * p->units)) != cudaSuccess) return cfail(e, "unit alloc");
   if ((e = cudaMalloc(&p->bucket_count, sizeof(int) * L)) != cudaSuccess) return cfail(e, "bucket alloc");
   if ((e = cudaMalloc(&p->bucket_list, sizeof(int2) * cap * L)) != cudaSuccess) return cfail(e, "bucket alloc");
   if ((e = cudaMallocHost(&p->h_counts, sizeof(int) * L)) != cudaSuccess) return cfail(e, "pinned alloc");
@@ -562,12 +570,12 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   if ((e = cudaMalloc(&p->se_vals_d, sizeof(int32_t) * se_n)) != cudaSuccess) return cfail(e, "se alloc");
   if ((e = cudaMalloc(&p->se_def_d, se_n)) != cudaSuccess) return cfail(e, "se alloc");
   if (p->big &&
-      (e = cudaMalloc(&p->S, (size_t)p->ipc * p->units * p->K * kBig * kBig * 8 + (size_t)p->K * kBig * kBig * 8)) !=
+      (e = cudaMalloc(&p->S, (size_t)slots * p->K * kBig * kBig * 8 + (size_t)p->K * kBig * kBig * 8)) !=
           cudaSuccess) {
     free_plan(p);
     return fail(FM_ENOMEM, std::string("tile scratch alloc: ") + cudaGetErrorString(e));
   }
-  if ((e = cudaMalloc(&p->chat, (size_t)per_img * p->ipc)) != cudaSuccess) {
+  if ((e = cudaMalloc(&p->chat, (size_t)slots * p->K * p->wpx * 8)) != cudaSuccess) {
     free_plan(p);
     return fail(FM_ENOMEM, std::string("spectral scratch alloc: ") + cudaGetErrorString(e));
   }
@@ -600,7 +608,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     b.enc_bias = -smin;
     b.units = 1;
     b.K_max = b.K;
-    b.S = p->S + (size_t)p->ipc * p->units * p->K * kBig * kBig;   // spare slab after the batch scratch
+    b.S = p->S + (size_t)slots * p->K * kBig * kBig;   // spare slab after the batch scratch
     b.spec = p->spec + p->spec_off[li];
     b.spec_scale = (float)(1.0 / ((double)kBig * kBig * Tl));
     b.err = p->stats + 1;
@@ -659,7 +667,8 @@ int fm_plan_query(const fm_plan* p, fm_plan_info* info) {
   info->out_lo_offset[0] = p->two_d ? p->off_y : p->off_x;
   info->out_lo_offset[1] = p->two_d ? p->off_x : 0;
   info->images_per_launch = p->ipc;
-  info->scratch_bytes = (int64_t)p->units * p->K * p->wpx * 8 * p->ipc;
+  info->scratch_bytes = (int64_t)p->upl * p->K * p->wpx * 8 * p->ipc +
+                        (p->big ? (int64_t)p->upl * p->K * kBig * kBig * 8 * p->ipc : 0);
   info->se_min = p->se_min;
   info->se_max = p->se_max;
   info->se_count = p->se_count;
@@ -683,9 +692,11 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
   const int64_t img_elems = p->H * p->W;
   const int dsz = dtype_size(p->d.img_dtype);
   const int L = (int)p->ladder.size();
-  const int64_t cap = p->ipc * p->units;
+  const int64_t cap = p->ipc * p->upl;
   for (int64_t c0 = 0; c0 < p->batch; c0 += p->ipc) {
-    const int n = (int)std::min<int64_t>(p->ipc, p->batch - c0);
+   const int n = (int)std::min<int64_t>(p->ipc, p->batch - c0);
+   for (int u0 = 0; u0 < p->units; u0 += p->upl) {
+    const int nu = std::min(p->upl, p->units - u0);
     // ---- per-unit tonal range -> ladder entry + work lists (fm_range.cuh)
     FM_CUDA(cudaMemsetAsync(p->bucket_count, 0, sizeof(int) * L, s));
     RangeArgs r{};
@@ -703,6 +714,7 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
     r.win_x = p->win_x;
     r.tiles_x = p->tiles_x;
     r.units = p->units;
+    r.unit0 = u0;
     r.unit_step_x = p->unit_step_x;
     r.img_min = p->d.img_min;
     r.img_max = p->d.img_max;
@@ -715,7 +727,7 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
     r.bucket_list = p->bucket_list;
     r.cap = (int)cap;
     r.err = p->stats + 1;
-    range_kernel<<<dim3((unsigned)p->units, n), 256, 0, s>>>(r);
+    range_kernel<<<dim3((unsigned)nu, n), 256, 0, s>>>(r);
     g_launches++;
     FM_CUDA(cudaGetLastError());
     FM_CUDA(cudaMemcpyAsync(p->h_counts, p->bucket_count, sizeof(int) * L, cudaMemcpyDeviceToHost, s));
@@ -751,6 +763,8 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
     a.unit_param = p->unit_param;
     a.spec_off = p->d_spec_off;
     a.units = p->units;
+    a.unit0 = u0;
+    a.upl = p->upl;
     a.K_max = p->K;
     a.wpx = p->wpx;
     int e0 = -1;
@@ -774,6 +788,9 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
       b.enc_sign = a.enc_sign;
       b.unit_param = p->unit_param;
       b.units = p->units;
+      b.unit0 = u0;
+      b.upl = p->upl;
+      b.nu = nu;
       b.K_max = p->K;
       b.S = p->S;
       b.spec = p->spec;
@@ -781,14 +798,14 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
       b.chat = p->chat;
       b.wpx = p->wpx;
       b.err = p->stats + 1;
-      const unsigned z = (unsigned)(p->units * n);
+      const unsigned z = (unsigned)(nu * n);
       const unsigned inv_blocks = (unsigned)((kBig - (p->my - 1) + kBigRows - 1) / kBigRows);
       big_rows_kernel<true, false><<<dim3(kBig / kBigRows, p->K, z), kBigNT, kBigRowsSmem, s>>>(b);
       big_cols_kernel<false><<<dim3(kBig / kBigCols, p->K, z), kBigColsNT, kBigColsSmem, s>>>(b);
       big_rows_kernel<false, false><<<dim3(inv_blocks, p->K, z), kBigNT, kBigRowsSmem, s>>>(b);
       g_launches += 3;
     } else {
-      p->var->conv(dim3(p->tile_ctas, p->kchunks, n), p->conv_smem, s, a);
+      p->var->conv(dim3((unsigned)nu, p->kchunks, n), p->conv_smem, s, a);
       g_launches++;
     }
     FM_CUDA(cudaGetLastError());
@@ -805,6 +822,8 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
     t.K_max = p->K;
     t.unit_param = p->unit_param;
     t.units = p->units;
+    t.unit0 = u0;
+    t.upl = p->upl;
     t.wpx = p->wpx;
     t.two_d = p->two_d ? 1 : 0;
     t.QY = p->QY;
@@ -848,14 +867,15 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
       tonal_b += (double)cnt * ((N + 1) * (double)p->wpx * 8.0 + (double)p->wpx * (4.0 + (valid ? 1.0 : 0.0)));
     }
     p->planes_done += (int64_t)planes;
-    p->units_done += (int64_t)n * p->units;
+    p->units_done += (int64_t)n * nu;
     if (p->timing) {
       FM_CUDA(cudaEventRecord(next_event(p), s));
       p->pending_tonal.push_back({e1, e1 + 1});
-      p->acc.conv_bytes += (double)n * img_elems * dsz + planes * (double)p->wpx * 8.0;
+      p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->wpx * 8.0;
       p->acc.conv_flops += planes * p->conv_flops_per_plane;
       p->acc.tonal_bytes += tonal_b;
     }
+   }
   }
   return FM_OK;
 }

@@ -36,6 +36,7 @@ struct BigArgs {
   int T, K;                   // SPEC launch: the ladder entry
   const int4* unit_param;     // CONV: [imgs][units]
   int units;
+  int unit0, upl, nu;         // first unit, slots per image, units in this launch (grid z = imgs * nu)
   int K_max;
   float2* S;                  // [imgs][units][K_max][256][256] (CONV) or [K][256][256] (SPEC)
   const float4* spec;         // CONV: ladder base; SPEC: output
@@ -60,8 +61,9 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = blockIdx.y;
-  const int unit = SPEC ? 0 : (int)(blockIdx.z % a.units);
-  const int img = SPEC ? 0 : (int)(blockIdx.z / a.units);
+  const int lu = SPEC ? 0 : (int)(blockIdx.z % a.nu);
+  const int unit = SPEC ? 0 : a.unit0 + lu;
+  const int img = SPEC ? 0 : (int)(blockIdx.z / a.nu);
   int T = a.T, K = a.K, enc_bias = a.enc_bias;
   if constexpr (!SPEC) {
     const int4 up = a.unit_param[(size_t)img * a.units + unit];
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
   const int row0 = FWD ? blockIdx.x * kBigRows : (a.my - 1) + blockIdx.x * kBigRows;
   if (row0 >= kBig) return;
   const int ty = unit / max(a.tiles_x, 1), tx = unit - ty * max(a.tiles_x, 1);
-  float2* Sitem = a.S + (((size_t)img * a.units + unit) * a.K_max + k) * (size_t)(kBig * kBig);
+  float2* Sitem = a.S + (((size_t)img * a.upl + lu) * a.K_max + k) * (size_t)(kBig * kBig);
   if constexpr (SPEC) Sitem = a.S + (size_t)k * (kBig * kBig);
 
   auto ld2 = [&](int y, int x) -> float4 { return *reinterpret_cast<const float4*>(buf + y * RS + x); };
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
     }
     __syncthreads();
     // valid window store: tile row ty_row = row0 + y (>= my-1), columns x >= mx-1
-    float2* dst = a.chat + (((size_t)img * a.units + unit) * a.K_max + k) * (size_t)a.wpx;
+    float2* dst = a.chat + (((size_t)img * a.upl + lu) * a.K_max + k) * (size_t)a.wpx;
     const int vx = kBig - (a.mx - 1);   // valid columns per row
     for (int i = tid; i < kBigRows * vx; i += kBigNT) {
       const int y = i / vx, c = i - (i / vx) * vx;
@@ -246,8 +248,9 @@ __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a
 
   const int tid = threadIdx.x;
   const int cb = blockIdx.x, k = blockIdx.y;
-  const int unit = SPEC ? 0 : (int)(blockIdx.z % a.units);
-  const int img = SPEC ? 0 : (int)(blockIdx.z / a.units);
+  const int lu = SPEC ? 0 : (int)(blockIdx.z % a.nu);
+  const int unit = SPEC ? 0 : a.unit0 + lu;
+  const int img = SPEC ? 0 : (int)(blockIdx.z / a.nu);
   int K = a.K;
   const float4* spec_plane = nullptr;
   if constexpr (!SPEC) {
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a
     cp_async_commit();
   }
   float2* Sitem = SPEC ? a.S + (size_t)k * (kBig * kBig)
-                       : a.S + (((size_t)img * a.units + unit) * a.K_max + k) * (size_t)(kBig * kBig);
+                       : a.S + (((size_t)img * a.upl + lu) * a.K_max + k) * (size_t)(kBig * kBig);
   auto ld2 = [&](int y, int x) -> float4 { return *reinterpret_cast<const float4*>(buf + y * RS + x); };
   auto st2 = [&](int y, int x, float2 p, float2 q) {
     *reinterpret_cast<float4*>(buf + y * RS + x) = make_float4(p.x, p.y, q.x, q.y);

@@ -26,6 +26,7 @@ struct RangeArgs {
   int win_y, win_x;       // input window extent of one unit
   int tiles_x;            // 2-D tile grid width
   int units;              // units per image
+  int unit0;              // first unit of this launch
   int unit_step_x;        // 1-D: output pixels per unit (tiles_per_unit * QX)
   int img_min, img_max;
   int enc_sign;           // +1 dilation, -1 erosion
@@ -46,7 +47,7 @@ __device__ __forceinline__ int range_load(const void* img, int dtype, int64_t i)
 }
 
 __global__ void __launch_bounds__(256) range_kernel(const RangeArgs a) {
-  const int unit = blockIdx.x, img = blockIdx.y;
+  const int unit = a.unit0 + blockIdx.x, img = blockIdx.y;
   int y0, x0;
   if (a.two_d) {
     const int ty = unit / a.tiles_x, tx = unit - (unit / a.tiles_x) * a.tiles_x;

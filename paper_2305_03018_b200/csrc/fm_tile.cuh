@@ -81,6 +81,7 @@ struct TileArgs {
   const int4* unit_param;     // [imgs][units]: x = anchor (min f, or max f for erosion), y = N_t, z = ladder index
   const int64_t* spec_off;    // [ladder] offset of the SE spectrum for N = ladder[i] (float4 units)
   int units;                  // units per image
+  int unit0, upl;             // first unit of this launch, chat slots per image (units per launch)
   int K_max;                  // chat planes per unit (N_global + 1)
   int wpx;                    // window pixels per unit (QY*QX, or PY*QX in 1-D)
 };
@@ -168,8 +169,9 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   uint32_t magicT = a.magicT;
   float two_pi_over_T = a.two_pi_over_T;
   const float4* spec_base = a.spec;
+  const int unit = a.unit0 + blockIdx.x;   // absolute unit (tile, or group of 1-D tiles)
   if constexpr (!SPEC) {
-    const int4 up = a.unit_param[(size_t)img * a.units + blockIdx.x];
+    const int4 up = a.unit_param[(size_t)img * a.units + unit];
     K = up.y + 1;
     if ((int)blockIdx.y * a.k_chunk >= K) return;   // this k-chunk is beyond the unit's planes
     T = 2 * up.y;
@@ -183,8 +185,8 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   {
     int ty = 0, tx = 0;
     if (TWO_D && !SPEC) {
-      ty = blockIdx.x / a.tiles_x;
-      tx = blockIdx.x - ty * a.tiles_x;
+      ty = unit / a.tiles_x;
+      tx = unit - ty * a.tiles_x;
     }
     int bad = 0;
     for (int p = tid; p < C::NPTS; p += NT) {
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
           ix = tx * a.QX + a.DX + px;
           rowok = true;
         } else {
-          const int tile = blockIdx.x * PY + py;
+          const int tile = unit * PY + py;
           iy = 0;
           ix = tile * a.QX + a.DX + px;
           rowok = tile < a.tiles_total;
@@ -235,12 +237,12 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     *twx_slot(j) = make_float4(w0.x, w0.y, w1.x, w1.y);
   }
   __syncthreads();
-  const int ty = (TWO_D && !SPEC) ? blockIdx.x / a.tiles_x : 0;
-  const int tx = (TWO_D && !SPEC) ? blockIdx.x - ty * a.tiles_x : 0;
+  const int ty = (TWO_D && !SPEC) ? unit / a.tiles_x : 0;
+  const int tx = (TWO_D && !SPEC) ? unit - ty * a.tiles_x : 0;
   const int k_begin = blockIdx.y * a.k_chunk;
   const int k_end = min(K, k_begin + a.k_chunk);
-  // window-local output planes of this unit
-  float2* chat_unit = SPEC ? nullptr : a.chat + ((size_t)img * a.units + blockIdx.x) * a.K_max * (size_t)a.wpx;
+  // window-local output planes of this unit (slot = launch-local unit index)
+  float2* chat_unit = SPEC ? nullptr : a.chat + ((size_t)img * a.upl + blockIdx.x) * a.K_max * (size_t)a.wpx;
 
   // per-thread spectrum chunk copy: item g of plane k -> buffer g % NBUF (own slots only)
   auto spec_fetch = [&](int k, int g) {
@@ -424,7 +426,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
       } else {
         // 1-D output: row y is tile (blockIdx.x*PY + y); positions x >= mx-1 are valid;
         // window pixel p = y*QX + (x - (mx-1))
-        const int tile = blockIdx.x * PY + y;
+        const int tile = unit * PY + y;
         if (tile < a.tiles_total) {
           float2* dst = chat_unit + ((ptrdiff_t)k * a.wpx + (ptrdiff_t)y * a.QX - (a.mx - 1));
 #pragma unroll

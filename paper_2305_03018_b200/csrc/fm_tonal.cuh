@@ -29,6 +29,7 @@ struct TonalArgs {
   const int2* list;       // units of this ladder entry: (img, unit)
   const int4* unit_param; // [imgs][units]: x = anchor
   int units, wpx;
+  int unit0, upl;         // first unit of this launch, chat slots per image
   int two_d, QY, QX, OH, OW, tiles_x, unit_step_x;
   int32_t* out;           // [imgs][OH][OW]
   uint8_t* valid;         // nullable
@@ -58,7 +59,7 @@ __device__ __forceinline__ TonalPix tonal_pixel(const TonalArgs& a, int p) {
     ox = unit * a.unit_step_x + p;
   }
   r.live = p < a.wpx && oy < a.OH && ox < a.OW;
-  r.src = ((size_t)img * a.units + unit) * a.K_max * (size_t)a.wpx + p;
+  r.src = ((size_t)img * a.upl + (unit - a.unit0)) * a.K_max * (size_t)a.wpx + p;
   r.dst = ((size_t)img * a.OH + oy) * a.OW + ox;
   r.anchor = r.live ? a.unit_param[(size_t)img * a.units + unit].x : 0;
   return r;

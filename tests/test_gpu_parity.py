@@ -339,6 +339,7 @@ def test_batch_chunking_and_host_path():
     plan = MorphPlan(shape=(70, 90), se_values=se, se_lo=(-3, -3), img_dtype=torch.uint8, img_min=0,
                      img_max=15, batch=5, scratch_bytes=1)   # forces one image per launch
     assert plan.info["images_per_launch"] == 1
+    assert plan.info["scratch_bytes"] < 70 * 90 * 8 * 64   # one tile's planes per launch (unit chunking)
     out, valid = plan.execute(torch.from_numpy(imgs).cuda())
     host_out, host_valid = plan.execute_host(imgs)
     for i in range(5):
