@@ -244,6 +244,10 @@ struct fm_plan {
   // 256x256 tiles through an HBM scratch (fm_bigtile.cuh) for wide SEs
   bool big = false;
   float2* S = nullptr;
+  // host-buffer pipeline
+  cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_done = nullptr;
+  std::vector<cudaEvent_t> ev_chunks;     // per chunk: input landed, compute done
 };
 
 namespace {
@@ -271,6 +275,11 @@ void free_plan(fm_plan* p) {
   cudaFree(p->bucket_count);
   cudaFree(p->bucket_list);
   cudaFree(p->S);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
+  for (cudaEvent_t e : p->ev_chunks) cudaEventDestroy(e);
+  if (p->ev_in) cudaEventDestroy(p->ev_in);
+  if (p->ev_done) cudaEventDestroy(p->ev_done);
   if (p->h_counts) cudaFreeHost(p->h_counts);
   if (p->count_ev) cudaEventDestroy(p->count_ev);
   cudaSetDevice(prev);
@@ -682,19 +691,18 @@ int fm_reset_stats(fm_plan* p, void* stream) {
   return FM_OK;
 }
 
-int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t* out, uint8_t* valid,
-               void* stream) {
-  if (!p || !img || !out) return fail(FM_EINVAL, "null argument");
-  DeviceGuard dg(p->device);
-  cudaStream_t s = (cudaStream_t)stream;
+// Images [cbeg, cend) of the batch (device pointers address image 0), in
+// launch chunks of ipc images and upl units.
+static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t* out, uint8_t* valid,
+                      cudaStream_t s, int64_t cbeg, int64_t cend) {
   p->last_stream = s;
   const int64_t npix = p->OH * p->OW;
   const int64_t img_elems = p->H * p->W;
   const int dsz = dtype_size(p->d.img_dtype);
   const int L = (int)p->ladder.size();
   const int64_t cap = p->ipc * p->upl;
-  for (int64_t c0 = 0; c0 < p->batch; c0 += p->ipc) {
-   const int n = (int)std::min<int64_t>(p->ipc, p->batch - c0);
+  for (int64_t c0 = cbeg; c0 < cend; c0 += p->ipc) {
+   const int n = (int)std::min<int64_t>(p->ipc, cend - c0);
    for (int u0 = 0; u0 < p->units; u0 += p->upl) {
     const int nu = std::min(p->upl, p->units - u0);
     // ---- per-unit tonal range -> ladder entry + work lists (fm_range.cuh)
@@ -880,6 +888,13 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t*
   return FM_OK;
 }
 
+int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t* out, uint8_t* valid,
+               void* stream) {
+  if (!p || !img || !out) return fail(FM_EINVAL, "null argument");
+  DeviceGuard dg(p->device);
+  return run_images(p, img, img_defined, out, valid, (cudaStream_t)stream, 0, p->batch);
+}
+
 int fm_set_timing(fm_plan* p, int enable) {
   if (!p) return fail(FM_EINVAL, "null plan");
   p->timing = enable != 0;
@@ -945,13 +960,46 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, i
     FM_CUDA(cudaMalloc(&p->h_def, in_n));
     FM_CUDA(cudaMalloc(&p->h_out, out_n * sizeof(int32_t)));
     FM_CUDA(cudaMalloc(&p->h_valid, out_n));
+    FM_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    FM_CUDA(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
+    const int64_t nchunks = (p->batch + p->ipc - 1) / p->ipc;
+    p->ev_chunks.resize(2 * nchunks);
+    for (auto& ev : p->ev_chunks) FM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    FM_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
   }
-  FM_CUDA(cudaMemcpyAsync(p->h_img, img_host, in_n * dsz, cudaMemcpyHostToDevice, s));
-  if (def_host) FM_CUDA(cudaMemcpyAsync(p->h_def, def_host, in_n, cudaMemcpyHostToDevice, s));
-  int rc = fm_execute(p, p->h_img, def_host ? p->h_def : nullptr, p->h_out, valid_host ? p->h_valid : nullptr, stream);
-  if (rc) return rc;
-  FM_CUDA(cudaMemcpyAsync(out_host, p->h_out, out_n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  if (valid_host) FM_CUDA(cudaMemcpyAsync(valid_host, p->h_valid, out_n, cudaMemcpyDeviceToHost, s));
+  // Chunk pipeline: every H2D is queued up front on one copy stream, each
+  // chunk's compute on `s` waits only for its own input, and its D2H runs on a
+  // second copy stream while later chunks compute (pinned host memory).
+  const size_t img_e = (size_t)p->H * p->W, out_e = (size_t)p->OH * p->OW;
+  const char* hin = reinterpret_cast<const char*>(img_host);
+  char* din = reinterpret_cast<char*>(p->h_img);
+  cudaStream_t hs = p->copy_stream, ds = p->d2h_stream;
+  FM_CUDA(cudaEventRecord(p->ev_in, s));          // order after prior work on s
+  FM_CUDA(cudaStreamWaitEvent(hs, p->ev_in, 0));
+  FM_CUDA(cudaStreamWaitEvent(ds, p->ev_in, 0));
+  int64_t ci = 0;
+  for (int64_t c0 = 0; c0 < p->batch; c0 += p->ipc, ++ci) {
+    const int64_t n = std::min<int64_t>(p->ipc, p->batch - c0);
+    FM_CUDA(cudaMemcpyAsync(din + c0 * img_e * dsz, hin + c0 * img_e * dsz, n * img_e * dsz, cudaMemcpyHostToDevice, hs));
+    if (def_host)
+      FM_CUDA(cudaMemcpyAsync(p->h_def + c0 * img_e, def_host + c0 * img_e, n * img_e, cudaMemcpyHostToDevice, hs));
+    FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci], hs));
+  }
+  ci = 0;
+  for (int64_t c0 = 0; c0 < p->batch; c0 += p->ipc, ++ci) {
+    const int64_t n = std::min<int64_t>(p->ipc, p->batch - c0);
+    FM_CUDA(cudaStreamWaitEvent(s, p->ev_chunks[2 * ci], 0));
+    int rc = run_images(p, p->h_img, def_host ? p->h_def : nullptr, p->h_out, valid_host ? p->h_valid : nullptr, s,
+                        c0, c0 + n);
+    if (rc) return rc;
+    FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci + 1], s));
+    FM_CUDA(cudaStreamWaitEvent(ds, p->ev_chunks[2 * ci + 1], 0));
+    FM_CUDA(cudaMemcpyAsync(out_host + c0 * out_e, p->h_out + c0 * out_e, n * out_e * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, ds));
+    if (valid_host)
+      FM_CUDA(cudaMemcpyAsync(valid_host + c0 * out_e, p->h_valid + c0 * out_e, n * out_e, cudaMemcpyDeviceToHost, ds));
+  }
+  FM_CUDA(cudaStreamSynchronize(ds));
   FM_CUDA(cudaStreamSynchronize(s));
   return FM_OK;
 }
