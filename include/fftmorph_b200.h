@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FM_ABI_VERSION 1
+#define FM_ABI_VERSION 2
 
 typedef enum fm_status {
   FM_OK = 0,
@@ -46,6 +46,9 @@ typedef enum fm_status {
 typedef enum fm_mode { FM_DILATE = 0, FM_ERODE = 1 } fm_mode;
 
 typedef enum fm_dtype { FM_U8 = 0, FM_U16 = 1, FM_I32 = 2 } fm_dtype;
+
+/* Output element type (the plan checks that every possible output value fits). */
+typedef enum fm_out_dtype { FM_OUT_I32 = 0, FM_OUT_U8 = 1, FM_OUT_U16 = 2, FM_OUT_I16 = 3 } fm_out_dtype;
 
 /* Plan description.  1-D signals use ndim=1 and shape[0]/se_shape[0]/se_lo[0]. */
 typedef struct fm_plan_desc {
@@ -67,6 +70,7 @@ typedef struct fm_plan_desc {
   int64_t scratch_bytes; /* spectral scratch budget (0 = default 4 GiB) */
   int32_t tile;          /* 0 = auto, else forced FFT tile edge (16..256) */
   int32_t tonal_len;     /* 0 = auto, else forced tonal length T (even, > l_R) */
+  int32_t out_dtype;     /* fm_out_dtype of the output values (0 = int32) */
 } fm_plan_desc;
 
 /* Read-only facts about a plan (for stats / bench / tests). */
@@ -121,15 +125,15 @@ int fm_plan_create(fm_plan** plan, const fm_plan_desc* desc,
  * build_umbra(f) + rfftn(f) + product + irfftn + rint/deviation + project_with_validity
  * + _paste (umbra.py:177-205, fft_conv.py:128-150, morphology.py:51-62).
  * img: device [batch, shape] of img_dtype; img_defined: device uint8 [batch, shape] or NULL;
- * out: device int32 [batch, out_shape]; valid: device uint8 [batch, out_shape] or NULL.
+ * out: device [batch, out_shape] of the plan's out_dtype; valid: device uint8 [batch, out_shape] or NULL.
  * Asynchronous on `stream`; deviation/value errors are read with fm_read_stats. */
 int fm_execute(fm_plan* plan, const void* img, const uint8_t* img_defined,
-               int32_t* out, uint8_t* valid, void* stream);
+               void* out, uint8_t* valid, void* stream);
 
 /* Same as fm_execute but with HOST buffers; copies in and out on `stream` and
  * synchronizes before returning (the reference-facing call with host memory). */
 int fm_execute_host(fm_plan* plan, const void* img_host, const uint8_t* img_defined_host,
-                    int32_t* out_host, uint8_t* valid_host, void* stream);
+                    void* out_host, uint8_t* valid_host, void* stream);
 
 /* Synchronize the plan's last stream, return the stats accumulated since the last
  * fm_reset_stats, and map them to a status: FM_EINVAL on a value error,

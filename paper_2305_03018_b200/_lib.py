@@ -18,6 +18,7 @@ LIB_PATH = _PKG / "_build" / "libfftmorph_b200.so"
 FM_OK, FM_EINVAL, FM_EPRECISION, FM_EDEVIATION, FM_ECUDA, FM_EUNSUPPORTED, FM_ENOMEM = range(7)
 FM_DILATE, FM_ERODE = 0, 1
 FM_U8, FM_U16, FM_I32 = 0, 1, 2
+FM_OUT_I32, FM_OUT_U8, FM_OUT_U16, FM_OUT_I16 = 0, 1, 2, 3
 
 # every symbol the header declares (checked by the CPU test-suite)
 EXPORTED = (
@@ -44,6 +45,7 @@ class PlanDesc(ctypes.Structure):
         ("scratch_bytes", ctypes.c_int64),
         ("tile", ctypes.c_int32),
         ("tonal_len", ctypes.c_int32),
+        ("out_dtype", ctypes.c_int32),
     ]
 
 

@@ -399,6 +399,18 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     p->out_bias = d.img_max - smin;
   }
   p->vmax = d.img_max - d.img_min;
+  {
+    // every possible output value must fit the requested output type
+    const int64_t lo = d.mode == FM_DILATE ? (int64_t)d.img_min + smin : (int64_t)d.img_min - smax;
+    const int64_t hi = d.mode == FM_DILATE ? (int64_t)d.img_max + smax : (int64_t)d.img_max - smin;
+    const int64_t vlo = std::min<int64_t>(lo, d.fill), vhi = std::max<int64_t>(hi, d.fill);
+    int64_t tlo = INT32_MIN, thi = INT32_MAX;
+    if (d.out_dtype == FM_OUT_U8) { tlo = 0; thi = 255; }
+    else if (d.out_dtype == FM_OUT_U16) { tlo = 0; thi = 65535; }
+    else if (d.out_dtype == FM_OUT_I16) { tlo = -32768; thi = 32767; }
+    else if (d.out_dtype != FM_OUT_I32) { free_plan(p); return fail(FM_EINVAL, "bad out_dtype"); }
+    if (vlo < tlo || vhi > thi) { free_plan(p); return fail(FM_EINVAL, "output values do not fit out_dtype"); }
+  }
 
   // tonal length: even, > l_R, with T/2 5-smooth
   int T = d.tonal_len;
@@ -693,7 +705,9 @@ int fm_reset_stats(fm_plan* p, void* stream) {
 
 // Images [cbeg, cend) of the batch (device pointers address image 0), in
 // launch chunks of ipc images and upl units.
-static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t* out, uint8_t* valid,
+static int out_size(int od) { return od == FM_OUT_U8 ? 1 : (od == FM_OUT_U16 || od == FM_OUT_I16) ? 2 : 4; }
+
+static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, void* out, uint8_t* valid,
                       cudaStream_t s, int64_t cbeg, int64_t cend) {
   p->last_stream = s;
   const int64_t npix = p->OH * p->OW;
@@ -840,7 +854,8 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, i
     t.OW = (int)p->OW;
     t.tiles_x = p->tiles_x;
     t.unit_step_x = p->unit_step_x;
-    t.out = out + (size_t)c0 * npix;
+    t.out = reinterpret_cast<char*>(out) + (size_t)c0 * npix * out_size(p->d.out_dtype);
+    t.out_dtype = p->d.out_dtype;
     t.valid = valid ? valid + (size_t)c0 * npix : nullptr;
     t.out_sign = p->out_sign;
     t.se_min = p->se_min;
@@ -888,7 +903,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, i
   return FM_OK;
 }
 
-int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, int32_t* out, uint8_t* valid,
+int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, void* out, uint8_t* valid,
                void* stream) {
   if (!p || !img || !out) return fail(FM_EINVAL, "null argument");
   DeviceGuard dg(p->device);
@@ -947,18 +962,20 @@ int fm_read_stats(fm_plan* p, fm_stats* st) {
   return FM_OK;
 }
 
-int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, int32_t* out_host,
+int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, void* out_host_v,
                     uint8_t* valid_host, void* stream) {
-  if (!p || !img_host || !out_host) return fail(FM_EINVAL, "null argument");
+  if (!p || !img_host || !out_host_v) return fail(FM_EINVAL, "null argument");
   DeviceGuard dg(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t in_n = (size_t)p->batch * p->H * p->W;
   const size_t out_n = (size_t)p->batch * p->OH * p->OW;
   const size_t dsz = dtype_size(p->d.img_dtype);
+  const size_t osz = out_size(p->d.out_dtype);
+  char* out_host = reinterpret_cast<char*>(out_host_v);
   if (!p->h_img) {
     FM_CUDA(cudaMalloc(&p->h_img, in_n * dsz));
     FM_CUDA(cudaMalloc(&p->h_def, in_n));
-    FM_CUDA(cudaMalloc(&p->h_out, out_n * sizeof(int32_t)));
+    FM_CUDA(cudaMalloc(&p->h_out, out_n * osz));
     FM_CUDA(cudaMalloc(&p->h_valid, out_n));
     FM_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
     FM_CUDA(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
@@ -994,8 +1011,8 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, i
     if (rc) return rc;
     FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci + 1], s));
     FM_CUDA(cudaStreamWaitEvent(ds, p->ev_chunks[2 * ci + 1], 0));
-    FM_CUDA(cudaMemcpyAsync(out_host + c0 * out_e, p->h_out + c0 * out_e, n * out_e * sizeof(int32_t),
-                            cudaMemcpyDeviceToHost, ds));
+    FM_CUDA(cudaMemcpyAsync(out_host + c0 * out_e * osz, reinterpret_cast<char*>(p->h_out) + c0 * out_e * osz,
+                            n * out_e * osz, cudaMemcpyDeviceToHost, ds));
     if (valid_host)
       FM_CUDA(cudaMemcpyAsync(valid_host + c0 * out_e, p->h_valid + c0 * out_e, n * out_e, cudaMemcpyDeviceToHost, ds));
   }

@@ -31,12 +31,22 @@ struct TonalArgs {
   int units, wpx;
   int unit0, upl;         // first unit of this launch, chat slots per image
   int two_d, QY, QX, OH, OW, tiles_x, unit_step_x;
-  int32_t* out;           // [imgs][OH][OW]
+  void* out;              // [imgs][OH][OW] of out_dtype
+  int out_dtype;          // 0 int32, 1 uint8, 2 uint16, 3 int16
   uint8_t* valid;         // nullable
   int out_sign, se_min, fill;
   int stride;             // generic kernel: per-pixel smem stride (float2), odd
   float* dev_max;         // max |c - rint c| (float bits, atomicMax as int)
 };
+
+__device__ __forceinline__ void store_out(const TonalArgs& a, size_t i, int v) {
+  switch (a.out_dtype) {
+    case 1: reinterpret_cast<uint8_t*>(a.out)[i] = (uint8_t)v; break;
+    case 2: reinterpret_cast<uint16_t*>(a.out)[i] = (uint16_t)v; break;
+    case 3: reinterpret_cast<int16_t*>(a.out)[i] = (int16_t)v; break;
+    default: reinterpret_cast<int32_t*>(a.out)[i] = v; break;
+  }
+}
 
 // Pixel p of the work unit list[blockIdx.y]: chat offset, output offset, anchor.
 struct TonalPix {
@@ -233,7 +243,7 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
       if constexpr (num_radices(N) % 2 == 0) top = tonal_threshold<N>(A, dev);
       else top = tonal_threshold<N>(B, dev);
     }
-    a.out[pp.dst] = top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill;
+    store_out(a, pp.dst, top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill);
     if (a.valid) a.valid[pp.dst] = top >= 0 ? 1 : 0;
   }
 #pragma unroll
@@ -297,7 +307,7 @@ __global__ void __launch_bounds__(128) tonal_kernel(const TonalArgs a) {
       if (z.x > 0.5f) top = 2 * n;
       if (z.y > 0.5f) top = 2 * n + 1;
     }
-    a.out[pp.dst] = top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill;
+    store_out(a, pp.dst, top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill);
     if (a.valid) a.valid[pp.dst] = top >= 0 ? 1 : 0;
   }
 #pragma unroll

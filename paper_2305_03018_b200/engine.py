@@ -19,7 +19,8 @@ import torch
 from . import _lib
 from ._lib import FM_DILATE, FM_ERODE, FM_I32, FM_U8, FM_U16
 
-_DTYPES = {torch.uint8: FM_U8, torch.int16: None, torch.int32: FM_I32}
+# output element types (fm_out_dtype)
+_OUT_CODES = {torch.int32: 0, torch.uint8: 1, torch.uint16: 2, torch.int16: 3}
 
 
 def _torch_dtype_code(t: torch.Tensor) -> int:
@@ -49,7 +50,7 @@ class MorphPlan:
 
     def __init__(self, *, shape, se_values, se_lo, se_defined=None, mode="dilate",
                  crop=True, img_dtype=torch.uint8, img_min=0, img_max=255, fill=0,
-                 batch=1, device=None, scratch_bytes=0, tile=0, tonal_len=0):
+                 batch=1, device=None, scratch_bytes=0, tile=0, tonal_len=0, out_dtype=torch.int32):
         L = _lib.load()
         shape = tuple(int(s) for s in shape)
         se_values = np.ascontiguousarray(np.asarray(se_values, dtype=np.int64))
@@ -81,6 +82,8 @@ class MorphPlan:
         d.scratch_bytes = int(scratch_bytes)
         d.tile = int(tile)
         d.tonal_len = int(tonal_len)
+        d.out_dtype = _OUT_CODES[out_dtype]
+        self.out_dtype = out_dtype
         self.desc = d
         self.shape = shape
         self.batch = int(batch)
@@ -104,7 +107,7 @@ class MorphPlan:
     def execute(self, img: torch.Tensor, defined: torch.Tensor | None = None, *,
                 out: torch.Tensor | None = None, valid: torch.Tensor | None = None,
                 want_valid: bool = True, stream=None):
-        """Run on a device batch ``img[batch, *shape]``; returns (out int32, valid uint8|None)."""
+        """Run on a device batch ``img[batch, *shape]``; returns (out of out_dtype, valid uint8|None)."""
         L = _lib.load()
         if img.device != self.device:
             raise ValueError(f"image on {img.device}, plan on {self.device}")
@@ -118,7 +121,7 @@ class MorphPlan:
             defined = defined.to(device=self.device, dtype=torch.uint8).reshape(exp).contiguous()
         oshape = (self.batch, *self.out_shape)
         if out is None:
-            out = torch.empty(oshape, dtype=torch.int32, device=self.device)
+            out = torch.empty(oshape, dtype=self.out_dtype, device=self.device)
         if valid is None and want_valid:
             valid = torch.empty(oshape, dtype=torch.uint8, device=self.device)
         rc = L.fm_execute(self._h, ctypes.c_void_p(img.data_ptr()),
@@ -142,7 +145,7 @@ class MorphPlan:
         def_t = None if defined is None else host(defined, torch.uint8)
         oshape = (self.batch, *self.out_shape)
         if out is None:
-            out = torch.empty(oshape, dtype=torch.int32)
+            out = torch.empty(oshape, dtype=self.out_dtype)
         if valid is None and want_valid:
             valid = torch.empty(oshape, dtype=torch.uint8)
         rc = L.fm_execute_host(self._h, ctypes.c_void_p(img_t.data_ptr()),

@@ -35,7 +35,7 @@ def test_header_and_binding_agree():
 def test_library_exports_every_symbol(lib):
     for name in _declared_functions():
         assert hasattr(lib, name), name
-    assert lib.fm_abi_version() == 1
+    assert lib.fm_abi_version() == 2
 
 
 def test_dynamic_symbol_table():
