@@ -205,7 +205,8 @@ class _PlanCache:
         key = (tuple(kw["shape"]), sev.shape, hsh.hexdigest(), tuple(kw["se_lo"]), kw.get("mode", "dilate"),
                bool(kw.get("crop", True)), str(kw.get("img_dtype")), int(kw.get("img_min", 0)),
                int(kw.get("img_max", 255)), int(kw.get("fill", 0)), int(kw.get("batch", 1)),
-               str(kw.get("device")), int(kw.get("tile", 0)), int(kw.get("tonal_len", 0)))
+               str(kw.get("device")), int(kw.get("tile", 0)), int(kw.get("tonal_len", 0)),
+               str(kw.get("out_dtype", torch.int32)), int(kw.get("scratch_bytes", 0)))
         with self._mu:
             p = self._d.get(key)
             if p is not None:
