@@ -107,6 +107,8 @@ typedef struct fm_timing {
   double conv_bytes;       /* image read + spectral volume written */
   double tonal_bytes;      /* spectral volume read + int32 values (+ validity) written */
   double conv_flops;       /* nominal FFT flops: per tile and plane 2*5*P^2*log2(P^2) + 6*P^2 */
+  double range_ms;         /* per-unit range + clamp bound kernel (fm_range.cuh) */
+  int64_t range_launches;
 } fm_timing;
 
 typedef struct fm_plan fm_plan;

@@ -75,7 +75,8 @@ class Timing(ctypes.Structure):
     _fields_ = [("conv_ms", ctypes.c_double), ("tonal_ms", ctypes.c_double),
                 ("conv_launches", ctypes.c_int64), ("tonal_launches", ctypes.c_int64),
                 ("conv_bytes", ctypes.c_double), ("tonal_bytes", ctypes.c_double),
-                ("conv_flops", ctypes.c_double)]
+                ("conv_flops", ctypes.c_double), ("range_ms", ctypes.c_double),
+                ("range_launches", ctypes.c_int64)]
 
 
 class Stats(ctypes.Structure):

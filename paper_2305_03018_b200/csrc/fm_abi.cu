@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -175,6 +176,9 @@ int set_all_smem_attrs() {
   }
   for (const TonalVariant& v : kTonal) FM_CUDA(v.attr());
   FM_CUDA(cudaFuncSetAttribute(tonal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+  FM_CUDA(cudaFuncSetAttribute(range_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
+  FM_CUDA(cudaFuncSetAttribute(range_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
+  FM_CUDA(cudaFuncSetAttribute(range_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
   FM_CUDA(cudaFuncSetAttribute(big_rows_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
   FM_CUDA(cudaFuncSetAttribute(big_rows_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
   FM_CUDA(cudaFuncSetAttribute(big_rows_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
@@ -223,7 +227,7 @@ struct fm_plan {
   // event timing
   bool timing = false;
   std::vector<cudaEvent_t> ev_pool;                  // reusable events
-  std::vector<std::pair<int, int>> pending_conv, pending_tonal;  // (start, stop) indices into ev_pool
+  std::vector<std::pair<int, int>> pending_conv, pending_tonal, pending_range;  // (start, stop) indices into ev_pool
   size_t ev_next = 0;
   fm_timing acc{};
   double conv_flops_per_plane = 0;  // per unit and plane
@@ -232,6 +236,8 @@ struct fm_plan {
   std::vector<int64_t> spec_off;          // float4 offsets into spec
   std::vector<const TonalVariant*> ladder_var;
   int units = 1, wpx = 1, win_y = 1, win_x = 1, unit_step_x = 0;
+  std::vector<int2> taps;                 // clamp-bound taps of fm_range.cuh, best first
+  int* range_part = nullptr;              // [ipc*units][8] split partials of fm_range.cuh
   int upl = 1;                            // units per launch (chat slots per image)
   int* d_ladder = nullptr;
   int64_t* d_spec_off = nullptr;
@@ -271,6 +277,7 @@ void free_plan(fm_plan* p) {
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   cudaFree(p->d_ladder);
   cudaFree(p->d_spec_off);
+  cudaFree(p->range_part);
   cudaFree(p->unit_param);
   cudaFree(p->bucket_count);
   cudaFree(p->bucket_list);
@@ -534,6 +541,32 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     p->unit_step_x = p->PY * p->QX;
   }
 
+  // clamp-bound taps (fm_range.cuh): the highest SE entries, ties spread over
+  // the SE by a multiplicative hash; offsets index the staged input window;
+  // padded to a multiple of 8 with taps that never win.
+  // FM_RANGE_TAPS=<n> caps the count (0 disables the clamp).
+  {
+    int cap_taps = kMaxBoundTaps;
+    if (const char* env = std::getenv("FM_RANGE_TAPS")) cap_taps = std::max(0, std::min(kMaxBoundTaps, std::atoi(env)));
+    const size_t wsm = (size_t)p->win_y * p->win_x * sizeof(int16_t);
+    const bool fits = p->vmax <= 32767 && (p->se_max - p->se_min) < 32768 && wsm <= kRangeSmemMax;
+    if (fits && cap_taps > 0) {
+      std::vector<std::pair<int64_t, int2>> cand;
+      for (int py = 0; py < p->my; ++py)
+        for (int px = 0; px < p->mx; ++px) {
+          const int64_t i = (int64_t)py * p->mx + px;
+          if (!sd[i]) continue;
+          const int off = (p->my - 1 - py) * p->win_x + (p->mx - 1 - px);
+          const int bv = sv[i] - p->se_min;
+          const uint32_t h = (uint32_t)(i * 2654435761u);
+          cand.push_back({((int64_t)(p->se_max - sv[i]) << 32) | h, make_int2(off, bv)});
+        }
+      std::sort(cand.begin(), cand.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+      for (size_t i = 0; i < cand.size() && (int)i < cap_taps; ++i) p->taps.push_back(cand[i].second);
+      while (p->taps.size() % 8) p->taps.push_back(make_int2(0, kTapPadB));
+    }
+  }
+
   // spectral scratch and launch chunking
   // scratch per unit: its K_max spectral planes (+ the 256^2 tile slab on the big path).
   // Whole images per launch when they fit the budget, else chunks of units of one image.
@@ -583,6 +616,17 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   if ((e = cudaMalloc(&p->bucket_list, sizeof(int2) * cap * L)) != cudaSuccess) return cfail(e, "bucket alloc");
   if ((e = cudaMallocHost(&p->h_counts, sizeof(int) * L)) != cudaSuccess) return cfail(e, "pinned alloc");
   if ((e = cudaEventCreateWithFlags(&p->count_ev, cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+  {
+    const size_t np = (size_t)p->ipc * p->units;
+    if ((e = cudaMalloc(&p->range_part, sizeof(int) * 8 * np)) != cudaSuccess) return cfail(e, "range alloc");
+    std::vector<int> init(8 * np, 0);
+    for (size_t i = 0; i < np; ++i) {
+      init[8 * i + 0] = INT32_MAX;
+      init[8 * i + 1] = INT32_MIN;
+      init[8 * i + 2] = INT32_MAX;
+    }
+    cudaMemcpy(p->range_part, init.data(), sizeof(int) * 8 * np, cudaMemcpyHostToDevice);
+  }
   cudaMemcpy(p->d_ladder, p->ladder.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
   cudaMemcpy(p->d_spec_off, p->spec_off.data(), sizeof(int64_t) * L, cudaMemcpyHostToDevice);
   if ((e = cudaMalloc(&p->twN, sizeof(float2) * std::max(1, p->N))) != cudaSuccess) return cfail(e, "table alloc");
@@ -724,7 +768,6 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     RangeArgs r{};
     r.img = reinterpret_cast<const char*>(img) + (size_t)c0 * img_elems * dsz;
     r.img_def = img_defined ? img_defined + (size_t)c0 * img_elems : nullptr;
-    r.img_dtype = p->d.img_dtype;
     r.H = (int)p->H;
     r.W = (int)p->W;
     r.two_d = p->two_d ? 1 : 0;
@@ -734,14 +777,37 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     r.QX = p->QX;
     r.win_y = p->win_y;
     r.win_x = p->win_x;
+    r.my = p->my;
+    r.mx = p->mx;
     r.tiles_x = p->tiles_x;
     r.units = p->units;
     r.unit0 = u0;
     r.unit_step_x = p->unit_step_x;
-    r.img_min = p->d.img_min;
-    r.img_max = p->d.img_max;
+    r.OH = (int)p->OH;
+    r.OW = (int)p->OW;
     r.enc_sign = p->enc_sign;
+    r.enc_bias = p->enc_bias;
+    r.vmax = p->vmax;
     r.lr_se = p->se_max - p->se_min;
+    r.cy = p->two_d ? (p->my - 1) / 2 : 0;
+    r.cx = (p->mx - 1) / 2;
+    r.ntaps = (int)p->taps.size();
+    for (int i = 0; i < r.ntaps; ++i) r.taps[i] = p->taps[i];
+    // split units between CTAs when there are too few of them to fill the GPU
+    int S = 1;
+    if (r.ntaps > 0) {
+      const int64_t ctas = (int64_t)nu * n;
+      const int max_s = p->two_d ? std::max(1, p->QY / 4) : std::max(1, p->unit_step_x / 256);
+      S = (int)std::min<int64_t>(std::min(max_s, 32), std::max<int64_t>(1, (4 * 148 + ctas - 1) / ctas));
+    }
+    r.splits = S;
+    size_t rsm = 0;
+    if (r.ntaps > 0) {
+      rsm = p->two_d ? (size_t)((p->QY + S - 1) / S + p->my - 1) * p->win_x * 2
+                     : (size_t)((p->unit_step_x + S - 1) / S + p->mx - 1) * 2;
+      rsm = (rsm + 15) & ~(size_t)15;
+    }
+    r.part = p->range_part;
     r.ladder = p->d_ladder;
     r.L = L;
     r.unit_param = p->unit_param;
@@ -749,9 +815,20 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     r.bucket_list = p->bucket_list;
     r.cap = (int)cap;
     r.err = p->stats + 1;
-    range_kernel<<<dim3((unsigned)nu, n), 256, 0, s>>>(r);
+    int er = -1;
+    if (p->timing) { er = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
+    {
+      const dim3 rg((unsigned)(nu * S), n);
+      if (p->d.img_dtype == FM_U8) range_kernel<0><<<rg, kRangeNT, rsm, s>>>(r);
+      else if (p->d.img_dtype == FM_U16) range_kernel<1><<<rg, kRangeNT, rsm, s>>>(r);
+      else range_kernel<2><<<rg, kRangeNT, rsm, s>>>(r);
+    }
     g_launches++;
     FM_CUDA(cudaGetLastError());
+    if (p->timing) {
+      FM_CUDA(cudaEventRecord(next_event(p), s));
+      p->pending_range.push_back({er, er + 1});
+    }
     FM_CUDA(cudaMemcpyAsync(p->h_counts, p->bucket_count, sizeof(int) * L, cudaMemcpyDeviceToHost, s));
     FM_CUDA(cudaEventRecord(p->count_ev, s));
 
@@ -933,8 +1010,15 @@ int fm_get_timing(fm_plan* p, fm_timing* out, int reset) {
     p->acc.tonal_ms += ms;
     p->acc.tonal_launches++;
   }
+  for (auto& pr : p->pending_range) {
+    float ms = 0.f;
+    FM_CUDA(cudaEventElapsedTime(&ms, p->ev_pool[pr.first], p->ev_pool[pr.second]));
+    p->acc.range_ms += ms;
+    p->acc.range_launches++;
+  }
   p->pending_conv.clear();
   p->pending_tonal.clear();
+  p->pending_range.clear();
   p->ev_next = 0;
   if (out) *out = p->acc;
   if (reset) p->acc = fm_timing{};

@@ -107,8 +107,9 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
         if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
           const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
           if (a.img_def == nullptr || a.img_def[gi]) {
-            const int v = a.enc_sign * load_img(a.img, a.img_dtype, gi) + enc_bias;
-            if (v < 0 || v >= T) bad = 1;
+            // values below the unit's clamp level encode as the clamp (fm_range.cuh)
+            const int v = max(a.enc_sign * load_img(a.img, a.img_dtype, gi) + enc_bias, 0);
+            if (v >= T) bad = 1;
             else t = (uint16_t)v;
           }
         }

@@ -3,34 +3,59 @@
 // The reference sizes the tonal axis from the global data maxima
 // (required_lr, umbra.py:172-174).  Exactness only needs, for every output
 // pixel, a tonal length larger than the spread of the degrees that can meet
-// there: (max f - min f over the pixel's input window) + (max b - min b).
-// This kernel computes min/max of the defined values over every conv unit's
-// input window (one 2-D tile, or a group of 1-D tiles), picks the smallest
-// tonal length T_t = 2 N_t of the plan's ladder with T_t > l_R,t, records the
-// unit's anchor value (min f for dilation, max f for erosion), and appends the
-// unit to the work list of its ladder entry (the tonal kernel is specialised
-// per N).  Values outside the plan's [img_min, img_max] raise the error flag.
+// there.  Two reductions of that spread are exact:
+//
+//  * shift: dilation commutes with constant shifts of f, so a unit encodes
+//    v = f - min f over its input window (erosion: max f - f);
+//  * clamp: if D is a lower bound of the dilation over the unit's output
+//    pixels, replacing f(z) by max(f(z), D - max b) changes no output —
+//    every raised pair sums to at most D, which never exceeds the true
+//    maximum, and no pair is removed.  So values below c = D - max b may be
+//    clamped to c, and the unit needs T_t > (max f - max(min f, c)) + (max b - min b).
+//
+// D = min over the unit's output pixels x of max over a small set S of SE
+// taps (the highest-valued entries) of f(x - y) + b(y) — a lower bound of
+// the dilation at x.  It is found by branch and bound: each pixel stops
+// scanning taps as soon as its partial maximum reaches the running minimum,
+// so most pixels touch only a few taps.  The input window is staged once in
+// shared memory as int16 (out-of-image / undefined = -32768, which keeps any
+// sum with b below every real candidate).
+//
+// The kernel then picks the smallest T_t = 2 N_t of the plan's ladder,
+// records the unit's anchor (the clamp value in the image's own units) and
+// appends the unit to the work list of its ladder entry (the tonal kernel is
+// specialised per N).  Values outside [img_min, img_max] raise the error flag.
 #pragma once
 #include <stdint.h>
 #include <cuda_runtime.h>
 
 namespace fm {
 
+constexpr int kRangeNT = 256;
+constexpr int kMaxBoundTaps = 128;
+constexpr int16_t kWinUndef = -32768;
+constexpr int kTapPadB = -(1 << 20);  // padding taps: never win a max
+constexpr int kRangeSmemMax = 160 * 1024;
+
 struct RangeArgs {
   const void* img;
   const uint8_t* img_def;
-  int img_dtype;
   int H, W;
   int two_d;
   int DY, DX, QY, QX;
   int win_y, win_x;       // input window extent of one unit
+  int my, mx;             // SE extent (rows / columns of a split's window beyond its outputs)
   int tiles_x;            // 2-D tile grid width
   int units;              // units per image
   int unit0;              // first unit of this launch
   int unit_step_x;        // 1-D: output pixels per unit (tiles_per_unit * QX)
-  int img_min, img_max;
-  int enc_sign;           // +1 dilation, -1 erosion
+  int OH, OW;             // output extent (valid outputs of the last units are clipped)
+  int enc_sign, enc_bias; // v = enc_sign * f + enc_bias in [0, vmax] (plan-wide)
+  int vmax;
   int lr_se;              // se_max - se_min
+  int cy, cx;             // SE centre, for the seed pixels
+  int splits;             // CTAs per unit (output rows, or columns in 1-D, split between them)
+  int ntaps;              // 0: no clamp; else a multiple of 8 (padded with kTapPadB taps)
   const int* ladder;      // ascending N values
   int L;
   int4* unit_param;       // [imgs][units]
@@ -38,76 +63,211 @@ struct RangeArgs {
   int2* bucket_list;      // [L][cap]
   int cap;
   int* err;
+  int* part;              // splits > 1: [imgs*units][8] partial results + arrival count (self-resetting)
+  int2 taps[kMaxBoundTaps];  // (offset in the unit window, b - se_min), best first: read from the
+                             // constant bank, so a tap costs one add, one LDS and one add-max
 };
 
-__device__ __forceinline__ int range_load(const void* img, int dtype, int64_t i) {
-  if (dtype == 0) return (int)__ldg(reinterpret_cast<const uint8_t*>(img) + i);
-  if (dtype == 1) return (int)__ldg(reinterpret_cast<const uint16_t*>(img) + i);
+template <int DT>
+__device__ __forceinline__ int range_ld(const void* img, int64_t i) {
+  if (DT == 0) return (int)__ldg(reinterpret_cast<const uint8_t*>(img) + i);
+  if (DT == 1) return (int)__ldg(reinterpret_cast<const uint16_t*>(img) + i);
   return __ldg(reinterpret_cast<const int32_t*>(img) + i);
 }
 
-__global__ void __launch_bounds__(256) range_kernel(const RangeArgs a) {
-  const int unit = a.unit0 + blockIdx.x, img = blockIdx.y;
-  int y0, x0;
+__device__ __forceinline__ void unit_finish(const RangeArgs& a, int img, int unit, int lo, int hi, int bound) {
+  const bool any = lo <= hi;
+  int c = any ? lo : 0;
+  // bound: INT32_MAX = not computed, INT32_MIN = unknown (no clamp)
+  if (any && bound != INT32_MAX && bound != INT32_MIN && (int64_t)bound - a.lr_se > c)
+    c = (int)min((int64_t)bound - a.lr_se, (int64_t)hi);
+  const int lr = any ? (hi - c) + a.lr_se : a.lr_se;
+  int li = a.L - 1;
+  for (int i = 0; i < a.L; ++i)
+    if (2 * a.ladder[i] >= lr + 1) {
+      li = i;
+      break;
+    }
+  // anchor in image units: v = f - anchor (dilation) / anchor - f (erosion)
+  const int anchor = a.enc_sign * (c - a.enc_bias);
+  a.unit_param[(size_t)img * a.units + unit] = make_int4(anchor, a.ladder[li], li, any ? 1 : 0);
+  const int slot = atomicAdd(&a.bucket_count[li], 1);
+  a.bucket_list[(size_t)li * a.cap + slot] = make_int2(img, unit);
+}
+
+// grid (units_in_launch * splits, images); split s of a unit handles output
+// rows [s*QY/S, (s+1)*QY/S) (1-D: columns of the unit) and stages only the
+// input rows those outputs read.
+template <int DT>
+__global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
+  extern __shared__ int16_t swin[];
+  __shared__ int red[4][kRangeNT / 32];
+  __shared__ int s_lo, s_hi, s_key, s_bound, s_last;
+  constexpr int NW = kRangeNT / 32;
+  const int S = a.splits;
+  const int lu = blockIdx.x / S, sp = blockIdx.x - lu * S;
+  const int unit = a.unit0 + lu, img = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool stage = a.ntaps > 0;
+  // geometry: window origin, this split's outputs [j0, j1) and staged window part
+  int y0, x0, ny, nx, j0, j1, wy0, wy, wx0, wx;
   if (a.two_d) {
-    const int ty = unit / a.tiles_x, tx = unit - (unit / a.tiles_x) * a.tiles_x;
+    const int ty = unit / a.tiles_x, tx = unit - ty * a.tiles_x;
     y0 = ty * a.QY + a.DY;
     x0 = tx * a.QX + a.DX;
+    ny = min(a.QY, a.OH - ty * a.QY);
+    nx = min(a.QX, a.OW - tx * a.QX);
+    j0 = (int)((int64_t)sp * a.QY / S);
+    j1 = (int)((int64_t)(sp + 1) * a.QY / S);
+    wy0 = j0;
+    wy = (j1 - j0) + a.my - 1;
+    wx0 = 0;
+    wx = a.win_x;
   } else {
     y0 = 0;
     x0 = unit * a.unit_step_x + a.DX;
+    ny = 1;
+    nx = min(a.unit_step_x, a.OW - unit * a.unit_step_x);
+    j0 = (int)((int64_t)sp * a.unit_step_x / S);
+    j1 = (int)((int64_t)(sp + 1) * a.unit_step_x / S);
+    wy0 = 0;
+    wy = 1;
+    wx0 = j0;
+    wx = (j1 - j0) + a.mx - 1;
   }
-  const int ya = max(y0, 0), yb = min(y0 + a.win_y, a.H);
-  const int xa = max(x0, 0), xb = min(x0 + a.win_x, a.W);
-  int lo = INT32_MAX, hi = INT32_MIN, bad = 0;
-  // warps stride over rows, lanes over columns: coalesced, no index division
-  const int nw = blockDim.x >> 5, lane = threadIdx.x & 31;
-  for (int yy = ya + (int)(threadIdx.x >> 5); yy < yb; yy += nw) {
-    const int64_t rowbase = ((int64_t)img * a.H + yy) * a.W;
-#pragma unroll 4
-    for (int xx = xa + lane; xx < xb; xx += 32) {
-      const int64_t gi = rowbase + xx;
-      if (a.img_def && !a.img_def[gi]) continue;
-      const int v = range_load(a.img, a.img_dtype, gi);
-      lo = min(lo, v);
-      hi = max(hi, v);
-      bad |= (v < a.img_min) | (v > a.img_max);
+  if (tid == 0) s_bound = INT32_MAX;
+
+  // ---- stage the window part (int16), min / max of v and the position of the minimum
+  int lo = INT32_MAX, hi = INT32_MIN, bad = 0, key = INT32_MAX;
+  auto take = [&](int iy, int ix, int pos) {
+    int16_t sv = kWinUndef;
+    if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
+      const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
+      if (a.img_def == nullptr || a.img_def[gi]) {
+        const int v = a.enc_sign * range_ld<DT>(a.img, gi) + a.enc_bias;
+        lo = min(lo, v);
+        hi = max(hi, v);
+        bad |= (v < 0) | (v > a.vmax);
+        sv = (int16_t)min(max(v, 0), 32767);
+        key = min(key, ((int)sv << 16) | (pos & 0xFFFF));
+      }
     }
+    if (stage) swin[pos] = sv;
+  };
+  if (a.two_d) {
+    for (int r = warp; r < wy; r += NW) {
+#pragma unroll 4
+      for (int c = lane; c < wx; c += 32) take(y0 + wy0 + r, x0 + c, r * wx + c);
+    }
+  } else {
+#pragma unroll 4
+    for (int c = tid; c < wx; c += kRangeNT) take(y0, x0 + wx0 + c, c);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
   }
-  __shared__ int slo[8], shi[8], sbad[8];
-  const int wid = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    slo[wid] = lo;
-    shi[wid] = hi;
-    sbad[wid] = bad;
+  if (lane == 0) {
+    red[0][warp] = lo;
+    red[1][warp] = hi;
+    red[2][warp] = bad;
+    red[3][warp] = key;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
-      lo = min(lo, slo[i]);
-      hi = max(hi, shi[i]);
-      bad |= sbad[i];
+  if (tid == 0) {
+    for (int i = 1; i < NW; ++i) {
+      lo = min(lo, red[0][i]);
+      hi = max(hi, red[1][i]);
+      bad |= red[2][i];
+      key = min(key, red[3][i]);
     }
     if (bad) atomicOr(a.err, 1);
-    const bool any = lo <= hi;
-    if (!any) lo = hi = 0;
-    const int lr = (hi - lo) + a.lr_se;
-    int li = a.L - 1;
-    for (int i = 0; i < a.L; ++i)
-      if (2 * a.ladder[i] >= lr + 1) {
-        li = i;
-        break;
+    s_lo = lo;
+    s_hi = hi;
+    s_key = key;
+  }
+  __syncthreads();
+  lo = s_lo;
+  hi = s_hi;
+
+  // ---- lower bound D of the dilation over this split's outputs (branch and bound)
+  const int jy_end = a.two_d ? min(j1, ny) : 1;
+  const int jx_beg = a.two_d ? 0 : j0, jx_end = a.two_d ? nx : min(j1, nx);
+  const int oy0 = a.two_d ? j0 : 0;  // first output row of the split (window row 0 of swin)
+  if (stage && lo <= hi && oy0 < jy_end && jx_beg < jx_end) {
+    const int floor_d = lo + a.lr_se;  // D <= floor_d gives no clamp
+    {
+      // seed: every warp evaluates one pixel exactly (lanes over taps), placed
+      // around the part's minimum, where the smallest g is likely
+      const int pos = s_key & 0xFFFF;
+      const int zr = pos / wx, zc = pos - zr * wx;
+      const int sy = (warp & 1) ? 3 : -3, sx = (warp & 2) ? 3 : -3, sc = warp >> 2;
+      const int jy = min(max(zr - a.cy + sy * sc, 0), jy_end - 1 - oy0);
+      const int jx = min(max(zc - a.cx + sx * sc, 0), jx_end - 1 - (a.two_d ? 0 : wx0));
+      const int base = jy * wx + jx;
+      int g = INT32_MIN;
+      for (int t = lane; t < a.ntaps; t += 32) g = max(g, (int)swin[base + a.taps[t].x] + a.taps[t].y);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) g = max(g, __shfl_xor_sync(0xffffffffu, g, o));
+      if (lane == 0) atomicMin(&s_bound, g);
+    }
+    __syncthreads();
+    volatile int* vb = &s_bound;
+    const int rows = jy_end - oy0, cols = jx_end - jx_beg;
+    const int npx = rows * cols;
+    for (int q = tid; q < npx; q += kRangeNT) {
+      int jy = 0, jx = q;
+      if (rows > 1) {
+        jy = q / cols;
+        jx = q - jy * cols;
       }
-    const int anchor = a.enc_sign > 0 ? lo : hi;
-    a.unit_param[(size_t)img * a.units + unit] = make_int4(anchor, a.ladder[li], li, any ? 1 : 0);
-    const int slot = atomicAdd(&a.bucket_count[li], 1);
-    a.bucket_list[(size_t)li * a.cap + slot] = make_int2(img, unit);
+      const int base = jy * wx + jx + (a.two_d ? 0 : jx_beg - wx0);
+      int g = INT32_MIN;
+      bool done = true;
+#pragma unroll
+      for (int t0 = 0; t0 < kMaxBoundTaps; t0 += 8) {
+        if (t0 >= a.ntaps) break;
+        if (g >= *vb) {  // this pixel cannot lower the minimum
+          done = false;
+          break;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) g = max(g, (int)swin[base + a.taps[t0 + u].x] + a.taps[t0 + u].y);
+      }
+      if (done && g < *vb) atomicMin(&s_bound, g);
+      if (*vb <= floor_d) break;  // no clamp possible: stop (D is then only an upper bound)
+    }
+    __syncthreads();
+  }
+  const int bound = (stage && lo <= hi) ? s_bound : INT32_MAX;
+
+  if (S == 1) {
+    if (tid == 0) unit_finish(a, img, unit, lo, hi, bound);
+    return;
+  }
+  // ---- combine the splits: the last CTA to arrive finishes the unit
+  if (tid == 0) {
+    int* pr = a.part + ((size_t)img * a.units + unit) * 8;
+    atomicMin(pr + 0, lo);
+    atomicMax(pr + 1, hi);
+    // a split cut at its own floor only knows D <= its floor: no clamp then
+    const int pb = (bound <= lo + a.lr_se) ? INT32_MIN : bound;
+    atomicMin(pr + 2, pb);
+    __threadfence();
+    s_last = atomicAdd(pr + 3, 1) == S - 1;
+  }
+  __syncthreads();
+  if (s_last && tid == 0) {
+    __threadfence();
+    int* pr = a.part + ((size_t)img * a.units + unit) * 8;
+    const int glo = atomicExch(pr + 0, INT32_MAX);
+    const int ghi = atomicExch(pr + 1, INT32_MIN);
+    const int gb = atomicExch(pr + 2, INT32_MAX);
+    atomicExch(pr + 3, 0);
+    unit_finish(a, img, unit, glo, ghi, gb);
   }
 }
 

@@ -78,7 +78,7 @@ struct TileArgs {
   float2* chat;               // CONV: [imgs][units][K_max][wpx] (window-local pixels)
   int* err;                   // value-range error flag
   // per-unit tonal length (CONV): a unit is one 2-D tile or one group of PY 1-D tiles
-  const int4* unit_param;     // [imgs][units]: x = anchor (min f, or max f for erosion), y = N_t, z = ladder index
+  const int4* unit_param;     // [imgs][units]: x = anchor (clamp level: v = f - anchor, or anchor - f for erosion), y = N_t, z = ladder index
   const int64_t* spec_off;    // [ladder] offset of the SE spectrum for N = ladder[i] (float4 units)
   int units;                  // units per image
   int unit0, upl;             // first unit of this launch, chat slots per image (units per launch)
@@ -214,8 +214,9 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
         if (rowok && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
           const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
           if (a.img_def == nullptr || a.img_def[gi]) {
-            const int v = a.enc_sign * load_img(a.img, a.img_dtype, gi) + enc_bias;
-            if (v < 0 || v >= T) bad = 1;
+            // values below the unit's clamp level encode as the clamp (fm_range.cuh)
+            const int v = max(a.enc_sign * load_img(a.img, a.img_dtype, gi) + enc_bias, 0);
+            if (v >= T) bad = 1;
             else t = (uint16_t)v;
           }
         }

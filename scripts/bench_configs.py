@@ -44,21 +44,28 @@ def run(w, mode, reps):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     dev = plan.read_stats()
+    plan.set_timing(True)
+    plan.execute(x, out=out, valid=valid)
+    t = plan.get_timing(reset=True)
+    plan.set_timing(False)
     px = int(np.prod(imgs.shape))
     return {"ms": ms, "mpix_s": px / ms / 1e3, "tile": plan.info["tile_x"], "T": plan.info["tonal_len"],
-            "max_dev": dev}
+            "max_dev": dev, "range_ms": t["range_ms"], "conv_ms": t["conv_ms"], "tonal_ms": t["tonal_ms"],
+            "conv_launches": t["conv_launches"], "tonal_launches": t["tonal_launches"]}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--images", type=int, default=8)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--only", default="c1,c2,c3,c4,c5")
+    ap.add_argument("--modes", default="dilate,erode")
     args = ap.parse_args()
     build.build()
     res = {}
-    for name in ("c1", "c2", "c3", "c4", "c5"):
+    for name in args.only.split(","):
         w = W.c5(n_images=args.images) if name == "c5" else W.CONFIGS[name]()
-        for mode in ("dilate", "erode"):
+        for mode in args.modes.split(","):
             r = run(w, mode, args.reps)
             res[f"{name}_{mode}"] = r
             print(name, mode, json.dumps(r), flush=True)

@@ -225,3 +225,119 @@ def model_dilate(img, defined, se, se_def, se_lo, *, mode="dilate", crop=True, f
     if not two_d:
         out, valid = out[0], valid[0]
     return out, valid, maxdev
+
+
+# ---------------------------------------------------------------------------
+# Per-unit tonal length with the clamp bound (fm_range.cuh), modelled with
+# exact integer circular counts: the tonal axis of a unit is a length-T_t
+# cyclic group, so c(t) is the number of pairs whose degree is t mod T_t.
+
+TONAL_NS = (1, 2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16, 18, 20, 24, 25, 27, 30, 32, 36, 40, 45, 48, 50,
+            54, 60, 64, 72, 75, 80, 81, 90, 96, 100, 108, 120, 125, 128, 135, 144, 150, 160)
+
+
+def bound_taps(se, se_def, cap=128):
+    """Tap order of fm_abi.cu: highest value first, ties by a multiplicative hash of the index."""
+    my, mx = se.shape
+    smax = int(se[se_def].max())
+    cand = []
+    for py in range(my):
+        for px in range(mx):
+            i = py * mx + px
+            if se_def[py, px]:
+                h = (i * 2654435761) & 0xFFFFFFFF
+                cand.append((((smax - int(se[py, px])) << 32) | h, (my - 1 - py, mx - 1 - px)))
+    cand.sort()
+    return [c[1] for c in cand[:cap]]
+
+
+def model_clamped_units(img, defined, se, se_def, se_lo, *, mode="dilate", crop=True, fill=0, P=None,
+                        cap=128):
+    """Per-unit (anchor, T_t) of fm_range.cuh and the exact result through circular counts.
+
+    Returns (out, valid, mean_planes) for one 2-D image (1-D: pass shape (1, W) arrays)."""
+    img = np.asarray(img, dtype=np.int64)
+    defined = np.ones(img.shape, bool) if defined is None else np.asarray(defined, bool)
+    se = np.asarray(se, dtype=np.int64)
+    se_def = np.ones(se.shape, bool) if se_def is None else np.asarray(se_def, bool)
+    lo_y, lo_x = se_lo
+    if mode == "erode":
+        se, se_def = se[::-1, ::-1], se_def[::-1, ::-1]
+        lo_y, lo_x = -(lo_y + se.shape[0] - 1), -(lo_x + se.shape[1] - 1)
+    H, W = img.shape
+    my, mx = se.shape
+    fv = img[defined]
+    img_min, img_max = int(fv.min()), int(fv.max())
+    smin, smax = int(se[se_def].min()), int(se[se_def].max())
+    lr_se = smax - smin
+    N_glob = choose_T((img_max - img_min) + lr_se) // 2
+    ladder = [n for n in TONAL_NS if n < N_glob] + [N_glob]
+    enc_sign, enc_bias = (1, -img_min) if mode == "dilate" else (-1, img_max)
+    out_sign = 1 if mode == "dilate" else -1
+    vg = np.where(defined, enc_sign * img + enc_bias, -1)
+    bp = se - smin
+    hi_y, hi_x = lo_y + my - 1, lo_x + mx - 1
+    if crop:
+        off_y, off_x, OH, OW = 0, 0, H, W
+    else:
+        off_y, off_x, OH, OW = lo_y, lo_x, H + my - 1, W + mx - 1
+    DY, DX = off_y - hi_y, off_x - hi_x
+    if P is None:
+        P = next(p for p in (16, 32, 64, 128, 256) if p >= max(my, mx) + 1)
+    PY = P if H > 1 or my > 1 else 1
+    QY, QX = PY - my + 1, P - mx + 1
+    taps = bound_taps(se, se_def, cap)
+    out = np.zeros((OH, OW), np.int64)
+    valid = np.zeros((OH, OW), bool)
+    planes = []
+    for ty in range(-(-OH // QY)):
+        for tx in range(-(-OW // QX)):
+            y0, x0 = ty * QY + DY, tx * QX + DX
+            win = np.full((PY, P), -1, np.int64)
+            for r in range(PY):
+                for c in range(P):
+                    iy, ix = y0 + r, x0 + c
+                    if 0 <= iy < H and 0 <= ix < W:
+                        win[r, c] = vg[iy, ix]
+            vals = win[win >= 0]
+            if vals.size == 0:
+                lo = hi = 0
+                any_ = False
+            else:
+                lo, hi, any_ = int(vals.min()), int(vals.max()), True
+            ny, nx = min(QY, OH - ty * QY), min(QX, OW - tx * QX)
+            c = lo
+            if any_:
+                D = None
+                for jy in range(ny):
+                    for jx in range(nx):
+                        g = -(1 << 40)
+                        for (dy, dx) in taps:
+                            s = win[jy + dy, jx + dx]
+                            g = max(g, (s if s >= 0 else -32768) + int(bp[my - 1 - dy, mx - 1 - dx]))
+                        D = g if D is None else min(D, g)
+                if D is not None and D - lr_se > c:
+                    c = min(D - lr_se, hi)
+            lr = (hi - c) + lr_se if any_ else lr_se
+            N = next((n for n in ladder if 2 * n >= lr + 1), ladder[-1])
+            T = 2 * N
+            planes.append(N + 1)
+            anchor = enc_sign * (c - enc_bias)
+            for jy in range(ny):
+                for jx in range(nx):
+                    cnt = np.zeros(T, np.int64)
+                    for py in range(my):
+                        for px in range(mx):
+                            if not se_def[py, px]:
+                                continue
+                            s = win[jy + (my - 1 - py), jx + (mx - 1 - px)]
+                            if s >= 0:
+                                cnt[(max(s - c, 0) + bp[py, px]) % T] += 1
+                    nz = np.flatnonzero(cnt)
+                    oy, ox = ty * QY + jy, tx * QX + jx
+                    if len(nz):
+                        valid[oy, ox] = True
+                        out[oy, ox] = out_sign * (int(nz[-1]) + smin) + anchor
+                    else:
+                        out[oy, ox] = fill
+    return out, valid, float(np.mean(planes))

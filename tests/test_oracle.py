@@ -186,3 +186,41 @@ def test_c_oracle_matches_reference_digests(key):
     assert _digest(v, valid) == dg[key]["dilate"]
     v, valid = cnaive.naive(img, None, se, sd, lo, erode=True, crop=True, fill=tm)
     assert _digest(v, valid) == dg[key]["erode"]
+
+
+def test_clamped_unit_model_matches_oracle():
+    """fm_range.cuh's clamp bound + per-unit tonal length is exact (integer model, tiny T)."""
+    import kernel_model as KM
+    rng = np.random.default_rng(11)
+    checked = 0
+    for trial in range(24):
+        H, Wd = int(rng.integers(5, 40)), int(rng.integers(5, 40))
+        my, mx = int(rng.integers(1, 8)), int(rng.integers(1, 8))
+        smooth = trial % 3 == 0
+        if smooth:   # smooth images give strong clamps (small T_t)
+            yy, xx = np.mgrid[0:H, 0:Wd]
+            img = (20 + 10 * np.sin(yy / 4.0) + 10 * np.cos(xx / 5.0)).astype(np.int64)
+        else:
+            img = rng.integers(0, int(rng.integers(2, 60)), (H, Wd))
+        fdef = rng.random((H, Wd)) > (0.3 if trial % 4 == 1 else 0.0)
+        if not fdef.any():
+            fdef[0, 0] = True
+        se = rng.integers(0, int(rng.integers(1, 12)), (my, mx))
+        sdef = rng.random((my, mx)) > (0.4 if trial % 2 else 0.0)
+        sdef[0, 0] = True
+        lo = (int(rng.integers(-my, 2)), int(rng.integers(-mx, 2)))
+        crop = trial % 5 != 4
+        cap = (4, 16, 128)[trial % 3]
+        for mode in ("dilate", "erode"):
+            fill = 0 if mode == "dilate" else int(img[fdef].max())
+            ecrop = crop if mode == "dilate" else True
+            v, valid, _ = KM.model_clamped_units(img, fdef, se, sdef, lo, mode=mode, crop=ecrop,
+                                                 fill=fill, P=16, cap=cap)
+            if mode == "dilate":
+                rv, rvalid, _ = port.dilate_naive(img, fdef, (0, 0), se, sdef, lo, crop=crop)
+            else:
+                rv, rvalid, _ = port.erode_naive(img, fdef, (0, 0), se, sdef, lo, crop=True, neutral=fill)
+            assert np.array_equal(valid, rvalid), (trial, mode)
+            assert np.array_equal(np.where(valid, v, 0), np.where(rvalid, rv, 0)), (trial, mode)
+            checked += 1
+    assert checked == 48
