@@ -143,14 +143,37 @@ struct TonalVariant {
   int n, nt, smem;
   tonal_launch_fn fn;
   cudaError_t (*attr)();
+  // pipelined persistent kernel (register variants): threads, dynamic smem, launcher
+  int pipe_nt, pipe_smem;
+  tonal_launch_fn pipe_fn;
+  cudaError_t (*pipe_attr)(int*);   // sets the smem attribute, returns CTAs per SM
 };
+template <int N>
+void launch_tonal_pipe(dim3 grid, int nt, size_t smem, cudaStream_t s, const TonalArgs& a) {
+  if constexpr (N <= kTonalRegMax)
+    tonal_kernel_pipe<N, tonal_pipe_nt<N>(), tonal_pipe_st<N>()><<<grid, tonal_pipe_nt<N>() + 32, smem, s>>>(a);
+}
+template <int N>
+cudaError_t tonal_pipe_attr(int* occ) {
+  *occ = 0;
+  if constexpr (N <= kTonalRegMax) {
+    auto k = tonal_kernel_pipe<N, tonal_pipe_nt<N>(), tonal_pipe_st<N>()>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tonal_pipe_smem<N>());
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, tonal_pipe_nt<N>() + 32, tonal_pipe_smem<N>());
+  }
+  return cudaSuccess;
+}
 template <int N>
 cudaError_t tonal_attr() {
   return cudaFuncSetAttribute(tonal_kernel_t<N, tonal_sm<N>(), tonal_nt<N>()>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
-#define FM_TV(N) \
-  TonalVariant { N, tonal_nt<N>(), tonal_sm<N>() ? 2 * N * tonal_nt<N>() * 8 : 0, &launch_tonal<N, tonal_sm<N>(), tonal_nt<N>()>, &tonal_attr<N> }
+#define FM_TV(N)                                                                                             \
+  TonalVariant {                                                                                             \
+    N, tonal_nt<N>(), tonal_sm<N>() ? 2 * N * tonal_nt<N>() * 8 : 0, &launch_tonal<N, tonal_sm<N>(), tonal_nt<N>()>, \
+        &tonal_attr<N>, tonal_pipe_nt<N>(), tonal_pipe_smem<N>(), &launch_tonal_pipe<N>, &tonal_pipe_attr<N>      \
+  }
 const TonalVariant kTonal[] = {
     FM_TV(1),  FM_TV(2),  FM_TV(3),  FM_TV(4),  FM_TV(5),   FM_TV(6),   FM_TV(8),   FM_TV(9),   FM_TV(10),
     FM_TV(12), FM_TV(15), FM_TV(16), FM_TV(18), FM_TV(20),  FM_TV(24),  FM_TV(25),  FM_TV(27),  FM_TV(30),
@@ -158,6 +181,13 @@ const TonalVariant kTonal[] = {
     FM_TV(72), FM_TV(75), FM_TV(80), FM_TV(81), FM_TV(90),  FM_TV(96),  FM_TV(100), FM_TV(108), FM_TV(120),
     FM_TV(125), FM_TV(128), FM_TV(135), FM_TV(144), FM_TV(150), FM_TV(160)};
 static_assert(sizeof(kTonal) / sizeof(TonalVariant) == kTonalCount, "tonal variant table");
+
+int g_tonal_pipe_occ[kTonalCount];   // CTAs per SM of each pipelined variant (0: not pipelined)
+int g_num_sms = 148;
+const bool g_tonal_nopipe = std::getenv("FM_TONAL_NOPIPE") != nullptr;  // A/B switch for measurements
+// largest N served by the pipelined tonal kernel (beyond it the register
+// pressure of the per-pixel FFT leaves too few warps to cover the stream)
+const int g_tonal_pipe_max = std::getenv("FM_TONAL_PIPE_MAX") ? std::atoi(std::getenv("FM_TONAL_PIPE_MAX")) : 40;
 
 const TonalVariant* find_tonal(int n) {
   for (const TonalVariant& v : kTonal)
@@ -174,7 +204,15 @@ int set_all_smem_attrs() {
     FM_CUDA(v.attr_conv(kSmemLimit));
     FM_CUDA(v.attr_spec(kSmemLimit));
   }
-  for (const TonalVariant& v : kTonal) FM_CUDA(v.attr());
+  for (int i = 0; i < kTonalCount; ++i) {
+    FM_CUDA(kTonal[i].attr());
+    FM_CUDA(kTonal[i].pipe_attr(&g_tonal_pipe_occ[i]));
+  }
+  {
+    int dev = 0;
+    FM_CUDA(cudaGetDevice(&dev));
+    FM_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
   FM_CUDA(cudaFuncSetAttribute(tonal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
   FM_CUDA(cudaFuncSetAttribute(range_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
   FM_CUDA(cudaFuncSetAttribute(range_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
@@ -235,7 +273,7 @@ struct fm_plan {
   std::vector<int> ladder;
   std::vector<int64_t> spec_off;          // float4 offsets into spec
   std::vector<const TonalVariant*> ladder_var;
-  int units = 1, wpx = 1, win_y = 1, win_x = 1, unit_step_x = 0;
+  int units = 1, wpx = 1, npx = 1, win_y = 1, win_x = 1, unit_step_x = 0;  // wpx: even plane stride
   std::vector<int2> taps;                 // clamp-bound taps of fm_range.cuh, best first
   int* range_part = nullptr;              // [ipc*units][8] split partials of fm_range.cuh
   int upl = 1;                            // units per launch (chat slots per image)
@@ -530,16 +568,18 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   // conv units: one 2-D tile, or PY consecutive 1-D tiles (one CTA)
   if (p->two_d) {
     p->units = p->tiles_total;
-    p->wpx = p->QY * p->QX;
+    p->npx = p->QY * p->QX;
     p->win_y = p->PY;
     p->win_x = p->PX;
   } else {
     p->units = p->tile_ctas;
-    p->wpx = p->PY * p->QX;
+    p->npx = p->PY * p->QX;
     p->win_y = 1;
     p->win_x = (p->PY - 1) * p->QX + p->PX;
     p->unit_step_x = p->PY * p->QX;
   }
+
+  p->wpx = (p->npx + 1) & ~1;  // even plane stride: 16-byte aligned bulk copies of pixel blocks
 
   // clamp-bound taps (fm_range.cuh): the highest SE entries, ties spread over
   // the SE by a multiplicative hash; offsets index the staged input window;
@@ -924,6 +964,9 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     t.unit0 = u0;
     t.upl = p->upl;
     t.wpx = p->wpx;
+    t.npx = p->npx;
+    t.qx_magic = p->QX > 1 ? (uint32_t)((0x100000000ull + p->QX - 1) / p->QX) : 0u;
+    t.tx_magic = p->tiles_x > 1 ? (uint32_t)((0x100000000ull + p->tiles_x - 1) / p->tiles_x) : 0u;
     t.two_d = p->two_d ? 1 : 0;
     t.QY = p->QY;
     t.QX = p->QX;
@@ -949,9 +992,15 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       t.T = 2 * N;
       t.list = p->bucket_list + (size_t)li * cap;
       const TonalVariant* tv = p->ladder_var[li];
-      if (tv) {
+      const int occ = tv ? g_tonal_pipe_occ[tv - kTonal] : 0;
+      if (tv && occ > 0 && !g_tonal_nopipe && N <= g_tonal_pipe_max) {
+        t.njobs = cnt;
+        const int64_t items = (int64_t)cnt * ((p->npx + tv->pipe_nt - 1) / tv->pipe_nt);
+        const int grid = (int)std::min<int64_t>(items, (int64_t)g_num_sms * occ);
+        tv->pipe_fn(dim3((unsigned)grid), tv->pipe_nt, tv->pipe_smem, s, t);
+      } else if (tv) {
         const int nt = tv->nt;
-        tv->fn(dim3((unsigned)cnt, (unsigned)((p->wpx + nt - 1) / nt)), nt, tv->smem, s, t);
+        tv->fn(dim3((unsigned)cnt, (unsigned)((p->npx + nt - 1) / nt)), nt, tv->smem, s, t);
       } else {
         t.nstages = (int)p->radix.size();
         for (size_t i = 0; i < p->radix.size(); ++i) t.radix[i] = p->radix[i];
@@ -959,19 +1008,20 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         t.wT = p->wT;
         t.stride = p->tonal_stride;
         const int nt = p->tonal_threads;
-        tonal_kernel<<<dim3((unsigned)cnt, (unsigned)((p->wpx + nt - 1) / nt)), nt, p->tonal_smem, s>>>(t);
+        tonal_kernel<<<dim3((unsigned)cnt, (unsigned)((p->npx + nt - 1) / nt)), nt, p->tonal_smem, s>>>(t);
       }
       g_launches++;
       FM_CUDA(cudaGetLastError());
       planes += (double)cnt * (N + 1);
-      tonal_b += (double)cnt * ((N + 1) * (double)p->wpx * 8.0 + (double)p->wpx * (4.0 + (valid ? 1.0 : 0.0)));
+      tonal_b += (double)cnt * ((N + 1) * (double)p->npx * 8.0 +
+                                (double)p->npx * (out_size(p->d.out_dtype) + (valid ? 1.0 : 0.0)));
     }
     p->planes_done += (int64_t)planes;
     p->units_done += (int64_t)n * nu;
     if (p->timing) {
       FM_CUDA(cudaEventRecord(next_event(p), s));
       p->pending_tonal.push_back({e1, e1 + 1});
-      p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->wpx * 8.0;
+      p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->npx * 8.0;
       p->acc.conv_flops += planes * p->conv_flops_per_plane;
       p->acc.tonal_bytes += tonal_b;
     }

@@ -28,7 +28,9 @@ struct TonalArgs {
   const float2* wT;       // generic kernel: [N] exp(+2 pi i k / T)
   const int2* list;       // units of this ladder entry: (img, unit)
   const int4* unit_param; // [imgs][units]: x = anchor
-  int units, wpx;
+  int units, wpx;         // wpx: plane stride (even), npx: pixels per unit
+  int npx, njobs;         // njobs: units in list (pipelined kernel)
+  uint32_t qx_magic, tx_magic;  // ceil(2^32 / QX), ceil(2^32 / tiles_x) (0 for a divisor of 1): exact quotients below 2^16
   int unit0, upl;         // first unit of this launch, chat slots per image
   int two_d, QY, QX, OH, OW, tiles_x, unit_step_x;
   void* out;              // [imgs][OH][OW] of out_dtype
@@ -54,25 +56,28 @@ struct TonalPix {
   size_t src, dst;
   int anchor;
 };
-__device__ __forceinline__ TonalPix tonal_pixel(const TonalArgs& a, int p) {
-  const int2 job = a.list[blockIdx.x];   // grid: x = work unit, y = pixel block
+__device__ __forceinline__ TonalPix tonal_pixel_job(const TonalArgs& a, int2 job, int p) {
   const int img = job.x, unit = job.y;
   TonalPix r;
   int oy, ox;
   if (a.two_d) {
-    const int ty = unit / a.tiles_x, tx = unit - (unit / a.tiles_x) * a.tiles_x;
-    const int wy = p / a.QX, wx = p - (p / a.QX) * a.QX;
+    // magic 0 encodes a divisor of 1 (2^32 does not fit)
+    const int ty = a.tx_magic ? (int)__umulhi((uint32_t)unit, a.tx_magic) : unit, tx = unit - ty * a.tiles_x;
+    const int wy = a.qx_magic ? (int)__umulhi((uint32_t)p, a.qx_magic) : p, wx = p - wy * a.QX;
     oy = ty * a.QY + wy;
     ox = tx * a.QX + wx;
   } else {
     oy = 0;
     ox = unit * a.unit_step_x + p;
   }
-  r.live = p < a.wpx && oy < a.OH && ox < a.OW;
+  r.live = p < a.npx && oy < a.OH && ox < a.OW;
   r.src = ((size_t)img * a.upl + (unit - a.unit0)) * a.K_max * (size_t)a.wpx + p;
   r.dst = ((size_t)img * a.OH + oy) * a.OW + ox;
   r.anchor = r.live ? a.unit_param[(size_t)img * a.units + unit].x : 0;
   return r;
+}
+__device__ __forceinline__ TonalPix tonal_pixel(const TonalArgs& a, int p) {
+  return tonal_pixel_job(a, a.list[blockIdx.x], p);   // grid: x = work unit, y = pixel block
 }
 
 template <int R>
@@ -196,8 +201,9 @@ __device__ __forceinline__ int tonal_threshold(const A& res, float& dev) {
 #pragma unroll U
   for (int n = 0; n < N; ++n) {
     const float2 z = res[n];
-    dev = fmaxf(dev, fabsf(z.x - rintf(z.x)));
-    dev = fmaxf(dev, fabsf(z.y - rintf(z.y)));
+    // rint via the 1.5*2^23 magic (round-to-nearest-even, |c| < 2^22): FMA pipe, not XU
+    dev = fmaxf(dev, fabsf(z.x - ((z.x + 12582912.0f) - 12582912.0f)));
+    dev = fmaxf(dev, fabsf(z.y - ((z.y + 12582912.0f) - 12582912.0f)));
     top = z.x > 0.5f ? 2 * n : top;
     top = z.y > 0.5f ? 2 * n + 1 : top;
   }
@@ -249,6 +255,127 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
   if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined register-variant kernel (N <= kTonalRegMax).  Persistent CTAs walk
+// the (unit, pixel block) items of one ladder entry; the K spectral values of
+// the next ST items are streamed into shared memory by bulk async copies (one
+// cp.async.bulk per plane, issued by one thread, completion on an mbarrier),
+// so HBM reads overlap the FFT and threshold work of the current item.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+
+template <int N>
+constexpr int tonal_pipe_nt() { return (N + 1) * 128 * 8 * 3 > 96 * 1024 ? 64 : 128; }
+template <int N>
+constexpr int tonal_pipe_st() { return (N + 1) * tonal_pipe_nt<N>() * 8 * 3 > 96 * 1024 ? 2 : 3; }
+template <int N>
+constexpr int tonal_pipe_smem() { return (N + 1) * tonal_pipe_nt<N>() * 8 * tonal_pipe_st<N>(); }
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_addr(bar)) : "memory");
+}
+
+// NT consumer threads (one pixel each per item) + one producer warp; full[st]
+// completes when the stage's bulk copies land, empty[st] when every consumer
+// warp has read it.
+template <int N, int NT, int ST>
+__global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a) {
+  constexpr int K = N + 1;
+  constexpr int off = tonal_off(N);
+  constexpr int NCW = NT / 32;
+  extern __shared__ __align__(128) float2 tstg[];   // [ST][K][NT]
+  __shared__ __align__(8) uint64_t full[ST], empty[ST];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int bpj = (a.npx + NT - 1) / NT;
+  const int items = a.njobs * bpj;
+  if (tid == 0) {
+    for (int st = 0; st < ST; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NCW) {
+    // ---- producer
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int i = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++i) {
+        const int st = i % ST;
+        if (i >= ST) mbar_wait(&empty[st], (uint32_t)(((i / ST) - 1) & 1));
+        const int j = item / bpj, blk = item - j * bpj;
+        const int2 job = a.list[j];
+        const float2* src = a.chat + ((size_t)job.x * a.upl + (job.y - a.unit0)) * a.K_max * (size_t)a.wpx +
+                            (size_t)blk * NT;
+        const uint32_t bytes = (uint32_t)min(NT, a.wpx - blk * NT) * 8u;
+        mbar_expect_tx(&full[st], bytes * K);
+        float2* dst = tstg + (size_t)st * K * NT;
+#pragma unroll 1
+        for (int k = 0; k < K; ++k) bulk_g2s(dst + k * NT, src + (size_t)k * a.wpx, bytes, &full[st], pol);
+      }
+    }
+    return;
+  }
+  // ---- consumers
+  float dev = 0.f;
+  int i = 0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x, ++i) {
+    const int st = i % ST;
+    mbar_wait(&full[st], (uint32_t)((i / ST) & 1));
+    const int j = item / bpj, blk = item - j * bpj;
+    const TonalPix pp = tonal_pixel_job(a, a.list[j], blk * NT + tid);
+    const float2* xs = tstg + (size_t)st * K * NT + tid;
+    float2 A[N], B[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const float2 xk = xs[k * NT], xc = conjf2(xs[(N - k) * NT]);
+      A[k] = cadd(cadd(xk, xc), mul_pi(cmul(c_ttw[off + k], csub(xk, xc))));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);   // stage read into registers
+    if (pp.live) {
+      stock_run<N, 0, 1>(A, B);
+      float d = 0.f;
+      int top;
+      if constexpr (num_radices(N) % 2 == 0) top = tonal_threshold<N>(A, d);
+      else top = tonal_threshold<N>(B, d);
+      dev = fmaxf(dev, d);
+      store_out(a, pp.dst, top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill);
+      if (a.valid) a.valid[pp.dst] = top >= 0 ? 1 : 0;
+    }
+  }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
+  if (lane == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
 }
 
 // generic runtime-N fallback (N > 160)

@@ -124,3 +124,13 @@ def test_strip_windows_cover_dependency_cone(mode):
             assert s.in0 <= s.out0 and s.out1 <= s.in1
         for src, dst, r0, r1 in sharding.halo_transfers(plan):
             assert plan[src].out0 <= r0 < r1 <= plan[src].out1
+
+
+def test_umulhi_division_magic():
+    """fm_tonal.cuh divides by QX / tiles_x with ceil(2^32/d) and a high multiply:
+    exact for every divisor 2..4096 and every quotient input below 2^16."""
+    p = np.arange(1 << 16, dtype=np.uint64)
+    for d in list(range(2, 300)) + [511, 1000, 4095, 4096]:
+        magic = np.uint64(((1 << 32) + d - 1) // d)
+        q = (p * magic) >> np.uint64(32)
+        assert np.array_equal(q, p // np.uint64(d)), d
