@@ -28,6 +28,7 @@
 #pragma once
 #include <stdint.h>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 namespace fm {
 
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
   extern __shared__ int16_t swin[];
   __shared__ int red[4][kRangeNT / 32];
   __shared__ int s_lo, s_hi, s_key, s_bound, s_last;
+  __shared__ __align__(16) int s_toff[kMaxBoundTaps], s_tb[kMaxBoundTaps];
   constexpr int NW = kRangeNT / 32;
   const int S = a.splits;
   const int lu = blockIdx.x / S, sp = blockIdx.x - lu * S;
@@ -139,29 +141,87 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
 
   // ---- stage the window part (int16), min / max of v and the position of the minimum
   int lo = INT32_MAX, hi = INT32_MIN, bad = 0, key = INT32_MAX;
-  auto take = [&](int iy, int ix, int pos) {
-    int16_t sv = kWinUndef;
-    if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
-      const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
-      if (a.img_def == nullptr || a.img_def[gi]) {
-        const int v = a.enc_sign * range_ld<DT>(a.img, gi) + a.enc_bias;
-        lo = min(lo, v);
-        hi = max(hi, v);
-        bad |= (v < 0) | (v > a.vmax);
-        sv = (int16_t)min(max(v, 0), 32767);
-        key = min(key, ((int)sv << 16) | (pos & 0xFFFF));
+  for (int i = tid; i < a.ntaps; i += kRangeNT) {
+    s_toff[i] = a.taps[i].x;
+    s_tb[i] = a.taps[i].y;
+  }
+  const int xb = x0 + wx0;  // image column of staged column 0
+  if (a.img_def == nullptr) {
+    // 16-byte vector loads of aligned chunks covering each staged row part;
+    // the window is first filled with "undefined" so that only in-image
+    // columns need writing
+    using T = typename std::conditional<DT == 0, uint8_t, typename std::conditional<DT == 1, uint16_t, int32_t>::type>::type;
+    constexpr int EPC = 16 / (int)sizeof(T);
+    if (stage) {
+      const int n2 = (wy * wx) >> 1;
+      uint32_t* w32 = reinterpret_cast<uint32_t*>(swin);
+      for (int i = tid; i < n2; i += kRangeNT) w32[i] = 0x80008000u;
+      if ((wy * wx) & 1) swin[wy * wx - 1] = kWinUndef;
+      __syncthreads();
+    }
+    const int xs = max(xb, 0), xe = min(xb + wx, a.W);
+    if (xs < xe) {
+      const T* imgT = reinterpret_cast<const T*>(a.img);
+      const int cpr = (xe - xs + 2 * EPC - 2) / EPC;  // chunks per row covering [xs, xe) at any alignment
+      const int total = wy * cpr;
+      const float inv_cpr = 1.0f / (float)cpr;
+#pragma unroll 2
+      for (int it = tid; it < total; it += kRangeNT) {
+        const int r = (int)(((float)it + 0.5f) * inv_cpr);
+        const int ch = it - r * cpr;
+        const int iy = y0 + wy0 + r;
+        if (iy < 0 || iy >= a.H) continue;
+        const T* rowp = imgT + ((int64_t)img * a.H + iy) * a.W;
+        const uintptr_t first = reinterpret_cast<uintptr_t>(rowp + xs) & ~(uintptr_t)15;
+        const uintptr_t cb = first + 16u * (uintptr_t)ch;
+        if (cb >= reinterpret_cast<uintptr_t>(rowp + xe)) continue;
+        const uint4 wv = __ldg(reinterpret_cast<const uint4*>(cb));
+        const int xc0 = (int)((const T*)cb - rowp);  // image column of the chunk's first element
+        const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const int x = xc0 + e;
+          if (x < xs || x >= xe) continue;
+          int f;
+          if (DT == 0) f = (int)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
+          else if (DT == 1) f = (int)((wd[e >> 1] >> (16 * (e & 1))) & 0xFFFFu);
+          else f = (int)wd[e];
+          const int v = a.enc_sign * f + a.enc_bias;
+          lo = min(lo, v);
+          hi = max(hi, v);
+          bad |= (v < 0) | (v > a.vmax);
+          const int sv = min(max(v, 0), 32767);
+          const int pos = r * wx + (x - xb);
+          key = min(key, (sv << 16) | (pos & 0xFFFF));
+          if (stage) swin[pos] = (int16_t)sv;
+        }
       }
     }
-    if (stage) swin[pos] = sv;
-  };
-  if (a.two_d) {
-    for (int r = warp; r < wy; r += NW) {
-#pragma unroll 4
-      for (int c = lane; c < wx; c += 32) take(y0 + wy0 + r, x0 + c, r * wx + c);
-    }
   } else {
+    const int rstep = a.two_d ? NW : 1, cstep = a.two_d ? 32 : kRangeNT;
+    for (int r = a.two_d ? warp : 0; r < wy; r += rstep) {
+      const int iy = y0 + wy0 + r;
+      const bool rok = iy >= 0 && iy < a.H;
+      const int64_t rb = ((int64_t)img * a.H + (rok ? iy : 0)) * a.W;
+      int16_t* srow = swin + r * wx;
 #pragma unroll 4
-    for (int c = tid; c < wx; c += kRangeNT) take(y0, x0 + wx0 + c, c);
+      for (int c = a.two_d ? lane : tid; c < wx; c += cstep) {
+        const int ix = xb + c;
+        int16_t sv = kWinUndef;
+        if (rok && (unsigned)ix < (unsigned)a.W) {
+          const int64_t gi = rb + ix;
+          if (a.img_def[gi]) {
+            const int v = a.enc_sign * range_ld<DT>(a.img, gi) + a.enc_bias;
+            lo = min(lo, v);
+            hi = max(hi, v);
+            bad |= (v < 0) | (v > a.vmax);
+            sv = (int16_t)min(max(v, 0), 32767);
+            key = min(key, ((int)sv << 16) | ((r * wx + c) & 0xFFFF));
+          }
+        }
+        if (stage) srow[c] = sv;
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -209,36 +269,49 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
       const int jx = min(max(zc - a.cx + sx * sc, 0), jx_end - 1 - (a.two_d ? 0 : wx0));
       const int base = jy * wx + jx;
       int g = INT32_MIN;
-      for (int t = lane; t < a.ntaps; t += 32) g = max(g, (int)swin[base + a.taps[t].x] + a.taps[t].y);
+      for (int t = lane; t < a.ntaps; t += 32) g = max(g, (int)swin[base + s_toff[t]] + s_tb[t]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) g = max(g, __shfl_xor_sync(0xffffffffu, g, o));
       if (lane == 0) atomicMin(&s_bound, g);
     }
     __syncthreads();
     volatile int* vb = &s_bound;
+    // every lane walks its own queue of pixels (q += kRangeNT), one 8-tap group
+    // per iteration, so lanes that stop early do not wait for the slowest one
     const int rows = jy_end - oy0, cols = jx_end - jx_beg;
     const int npx = rows * cols;
-    for (int q = tid; q < npx; q += kRangeNT) {
-      int jy = 0, jx = q;
-      if (rows > 1) {
-        jy = q / cols;
-        jx = q - jy * cols;
-      }
-      const int base = jy * wx + jx + (a.two_d ? 0 : jx_beg - wx0);
-      int g = INT32_MIN;
-      bool done = true;
-#pragma unroll
-      for (int t0 = 0; t0 < kMaxBoundTaps; t0 += 8) {
-        if (t0 >= a.ntaps) break;
-        if (g >= *vb) {  // this pixel cannot lower the minimum
-          done = false;
-          break;
+    const int xoff = a.two_d ? 0 : jx_beg - wx0;
+    const float inv_cols = 1.0f / (float)cols;
+    auto base_of = [&](int q) {
+      const int jy = (int)(((float)q + 0.5f) * inv_cols);  // exact for q < 2^22
+      return jy * wx + (q - jy * cols) + xoff;
+    };
+    int q = tid;
+    if (q < npx) {
+      int base = base_of(q), t = 0, g = INT32_MIN;
+      while (true) {
+        const int bnd = *vb;
+        if (bnd <= floor_d) break;  // no clamp possible: stop (D is then only an upper bound)
+        if (t >= a.ntaps || g >= bnd) {
+          if (t >= a.ntaps && g < bnd) atomicMin(&s_bound, g);
+          q += kRangeNT;
+          if (q >= npx) break;
+          base = base_of(q);
+          t = 0;
+          g = INT32_MIN;
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) g = max(g, (int)swin[base + a.taps[t0 + u].x] + a.taps[t0 + u].y);
+        const int4 o0 = *reinterpret_cast<const int4*>(s_toff + t), o1 = *reinterpret_cast<const int4*>(s_toff + t + 4);
+        const int4 b0 = *reinterpret_cast<const int4*>(s_tb + t), b1 = *reinterpret_cast<const int4*>(s_tb + t + 4);
+        g = max(g, (int)swin[base + o0.x] + b0.x);
+        g = max(g, (int)swin[base + o0.y] + b0.y);
+        g = max(g, (int)swin[base + o0.z] + b0.z);
+        g = max(g, (int)swin[base + o0.w] + b0.w);
+        g = max(g, (int)swin[base + o1.x] + b1.x);
+        g = max(g, (int)swin[base + o1.y] + b1.y);
+        g = max(g, (int)swin[base + o1.z] + b1.z);
+        g = max(g, (int)swin[base + o1.w] + b1.w);
+        t += 8;
       }
-      if (done && g < *vb) atomicMin(&s_bound, g);
-      if (*vb <= floor_d) break;  // no clamp possible: stop (D is then only an upper bound)
     }
     __syncthreads();
   }
