@@ -104,8 +104,12 @@ void launch_tile(dim3 grid, size_t smem, cudaStream_t s, const TileArgs& a) {
 
 template <int PY, int PX, int NT, bool TWO_D, bool SPEC>
 cudaError_t set_smem_attr(size_t smem) {
-  return cudaFuncSetAttribute(tile_conv_kernel<PY, PX, NT, TWO_D, SPEC>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // the opt-in limit covers static + dynamic shared memory
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, tile_conv_kernel<PY, PX, NT, TWO_D, SPEC>);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(tile_conv_kernel<PY, PX, NT, TWO_D, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(smem - fa.sharedSizeBytes));
 }
 
 struct Variant {
@@ -906,6 +910,10 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     a.upl = p->upl;
     a.K_max = p->K;
     a.wpx = p->wpx;
+    a.bucket_count = p->bucket_count;
+    a.bucket_list = p->bucket_list;
+    a.cap = (int)cap;
+    a.L = L;
     int e0 = -1;
     if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
     if (p->big) {

@@ -83,7 +83,11 @@ struct TileArgs {
   int units;                  // units per image
   int unit0, upl;             // first unit of this launch, chat slots per image (units per launch)
   int K_max;                  // chat planes per unit (N_global + 1)
-  int wpx;                    // window pixels per unit (QY*QX, or PY*QX in 1-D)
+  int wpx;                    // plane stride of chat (even)
+  // CONV launch order: jobs = the range kernel's work lists, largest tonal length first
+  const int* bucket_count;    // [L]
+  const int2* bucket_list;    // [L][cap] (img, unit)
+  int cap, L;
 };
 
 __constant__ float2 c_tw[kTwTotal];
@@ -162,15 +166,48 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int img = SPEC ? 0 : blockIdx.z;
+  int img = 0;
   // tonal length of this unit: the SPEC launch is per ladder entry; a CONV unit
   // uses the smallest ladder length that holds its own value range
   int T = a.T, K = a.K, enc_bias = a.enc_bias;
   uint32_t magicT = a.magicT;
   float two_pi_over_T = a.two_pi_over_T;
   const float4* spec_base = a.spec;
-  const int unit = a.unit0 + blockIdx.x;   // absolute unit (tile, or group of 1-D tiles)
+  int unit = a.unit0 + blockIdx.x;   // absolute unit (tile, or group of 1-D tiles)
   if constexpr (!SPEC) {
+    // job J of this launch -> (img, unit) from the per-ladder work lists, walked
+    // from the longest tonal length down: the longest units start first, so
+    // the launch ends without a tail of long stragglers
+    __shared__ int s_job[2];
+    if (warp == 0) {
+      int rem = (int)(blockIdx.z * gridDim.x + blockIdx.x), found = -1;
+      for (int top = a.L - 1; top >= 0 && found < 0; top -= 32) {
+        const int li = top - lane;
+        const int c = li >= 0 ? a.bucket_count[li] : 0;
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int nb = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += nb;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, li >= 0 && rem < incl);
+        if (m) {
+          const int l0 = __ffs(m) - 1;
+          rem -= __shfl_sync(0xffffffffu, incl - c, l0);
+          found = top - l0;
+        } else {
+          rem -= __shfl_sync(0xffffffffu, incl, 31);
+        }
+      }
+      if (lane == 0) {
+        const int2 job = a.bucket_list[(size_t)max(found, 0) * a.cap + rem];
+        s_job[0] = job.x;
+        s_job[1] = job.y;
+      }
+    }
+    __syncthreads();
+    img = s_job[0];
+    unit = s_job[1];
     const int4 up = a.unit_param[(size_t)img * a.units + unit];
     K = up.y + 1;
     if ((int)blockIdx.y * a.k_chunk >= K) return;   // this k-chunk is beyond the unit's planes
@@ -243,7 +280,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   const int k_begin = blockIdx.y * a.k_chunk;
   const int k_end = min(K, k_begin + a.k_chunk);
   // window-local output planes of this unit (slot = launch-local unit index)
-  float2* chat_unit = SPEC ? nullptr : a.chat + ((size_t)img * a.upl + blockIdx.x) * a.K_max * (size_t)a.wpx;
+  float2* chat_unit = SPEC ? nullptr : a.chat + ((size_t)img * a.upl + (unit - a.unit0)) * a.K_max * (size_t)a.wpx;
 
   // per-thread spectrum chunk copy: item g of plane k -> buffer g % NBUF (own slots only)
   auto spec_fetch = [&](int k, int g) {
