@@ -49,7 +49,7 @@ def _peaks():
 def _ncu_traffic(images_per_launch):
     """DRAM bytes per conv launch from the newest committed ncu capture of this workload
     (profiles/r*_c5_tile_conv_tonal.json, written by scripts/ncu_summary.py)."""
-    files = sorted((ROOT / "profiles").glob("r*_c5_tile_conv_tonal.json"), key=lambda f: f.stat().st_mtime)
+    files = sorted((ROOT / "profiles").glob("r*_c5_tile_conv_tonal.json"), key=lambda f: f.name)
     for f in reversed(files):
         try:
             data = json.loads(f.read_text())
@@ -285,7 +285,8 @@ def run_ours(args, rank, world, local_rank):
                    "planes_max": info["planes"], "mean_planes_per_tile": mean_planes,
                    "tile": [info["tile_y"], info["tile_x"]],
                    "images_per_launch": info["images_per_launch"],
-                   "l2": "no flush: inputs 256 MiB and the 1.37 GB/image spectral volume exceed the 126 MB L2"},
+                   "l2": "no flush: inputs 256 MiB and the spectral volume (~0.7 GB/image at "
+                         f"{(mean_planes or 0):.1f} planes/tile) exceed the 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": "tile_conv_kernel (encode + 2-D FFT conv, fm_tile.cuh)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_note,
@@ -295,7 +296,8 @@ def run_ours(args, rank, world, local_rank):
                      "tonal_kernel": {"achieved": tonal_bytes / tonal_s / 1e9 if tonal_s > 0 else 0.0,
                                       "unit": "GB/s", "frac": (tonal_bytes / tonal_s / 1e9) / hbm if tonal_s > 0 else 0.0,
                                       "ms_per_launch": tonal_s * 1000.0},
-                     "share_of_step": {"conv": tim["conv_ms"] / max(ms, 1e-9), "tonal": tim["tonal_ms"] / max(ms, 1e-9)}},
+                     "share_of_step": {"conv": tim["conv_ms"] / max(ms, 1e-9), "tonal": tim["tonal_ms"] / max(ms, 1e-9),
+                                       "range": tim["range_ms"] / max(ms, 1e-9)}},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(imgs.nbytes),
                 "d2h_bytes_per_step": int(pin_out.numel() * pin_out.element_size() + pin_valid.numel())},
         "gpu_launches": int(launches),

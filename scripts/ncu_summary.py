@@ -1,6 +1,7 @@
 """Summarise an ncu report (and optionally a launch-list CSV) into profiles/.
 
     python scripts/ncu_summary.py gpurun_out/prof_X.ncu-rep profiles/r1_NAME [--launches gpurun_out/launches.csv]
+        [--images-per-launch N]
 
 Writes <out>.json (per-kernel key metrics, dram bytes per launch = the bench
 `roofline.traffic`) and <out>.md (human summary with stall breakdown).
@@ -83,6 +84,8 @@ def main():
                 wb * scale.get(rec["dram__bytes_write.sum.unit"], 1)
         kernels.append(rec)
     summary = {"report": rep, "kernels": kernels}
+    if "--images-per-launch" in sys.argv:
+        summary["images_per_launch"] = int(sys.argv[sys.argv.index("--images-per-launch") + 1])
     if launches:
         per = defaultdict(list)
         with open(launches) as fh:
