@@ -286,7 +286,8 @@ struct fm_plan {
   int4* unit_param = nullptr;             // [ipc][units]
   int* bucket_count = nullptr;            // [L]
   int2* bucket_list = nullptr;            // [L][ipc*units]
-  int* h_counts = nullptr;                // pinned [L]
+  int* h_counts = nullptr;                // mapped pinned [L], written by publish_counts
+  int* h_counts_dev = nullptr;            // its device alias
   cudaEvent_t count_ev = nullptr;
   int64_t planes_done = 0, units_done = 0; // for the plan's mean planes per unit
   // 256x256 tiles through an HBM scratch (fm_bigtile.cuh) for wide SEs
@@ -658,7 +659,8 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   if ((e = cudaMalloc(&p->unit_param, sizeof(int4) * p->ipc * p->units)) != cudaSuccess) return cfail(e, "unit alloc");
   if ((e = cudaMalloc(&p->bucket_count, sizeof(int) * L)) != cudaSuccess) return cfail(e, "bucket alloc");
   if ((e = cudaMalloc(&p->bucket_list, sizeof(int2) * cap * L)) != cudaSuccess) return cfail(e, "bucket alloc");
-  if ((e = cudaMallocHost(&p->h_counts, sizeof(int) * L)) != cudaSuccess) return cfail(e, "pinned alloc");
+  if ((e = cudaHostAlloc(&p->h_counts, sizeof(int) * L, cudaHostAllocMapped)) != cudaSuccess) return cfail(e, "pinned alloc");
+  if ((e = cudaHostGetDevicePointer(&p->h_counts_dev, p->h_counts, 0)) != cudaSuccess) return cfail(e, "pinned map");
   if ((e = cudaEventCreateWithFlags(&p->count_ev, cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
   {
     const size_t np = (size_t)p->ipc * p->units;
@@ -873,7 +875,12 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       FM_CUDA(cudaEventRecord(next_event(p), s));
       p->pending_range.push_back({er, er + 1});
     }
-    FM_CUDA(cudaMemcpyAsync(p->h_counts, p->bucket_count, sizeof(int) * L, cudaMemcpyDeviceToHost, s));
+    // the counts reach the host through a kernel store to mapped memory, not a
+    // copy-engine D2H: a D2H copy would queue behind any large D2H transfer in
+    // flight on the device (e.g. the previous chunk's outputs)
+    publish_counts<<<1, 64, 0, s>>>(p->bucket_count, p->h_counts_dev, L);
+    g_launches++;
+    FM_CUDA(cudaGetLastError());
     FM_CUDA(cudaEventRecord(p->count_ev, s));
 
     TileArgs a{};
@@ -993,7 +1000,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     if (p->timing) { e1 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
     double planes = 0, tonal_b = 0;
     for (int li = 0; li < L; ++li) {
-      const int cnt = p->h_counts[li];
+      const int cnt = reinterpret_cast<volatile int*>(p->h_counts)[li];
       if (cnt <= 0) continue;
       const int N = p->ladder[li];
       t.N = N;

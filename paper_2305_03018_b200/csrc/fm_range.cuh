@@ -344,4 +344,10 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
   }
 }
 
+// per-ladder unit counts -> mapped host memory (read by the host after an event)
+__global__ void publish_counts(const int* __restrict__ counts, int* host_counts, int L) {
+  for (int i = threadIdx.x; i < L; i += blockDim.x) reinterpret_cast<volatile int*>(host_counts)[i] = counts[i];
+  __threadfence_system();
+}
+
 }  // namespace fm
