@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
   __shared__ int red[4][kRangeNT / 32];
   __shared__ int s_lo, s_hi, s_key, s_bound, s_last;
   __shared__ __align__(16) int s_toff[kMaxBoundTaps], s_tb[kMaxBoundTaps];
+  __shared__ int s_lad[64];
   constexpr int NW = kRangeNT / 32;
   const int S = a.splits;
   const int lu = blockIdx.x / S, sp = blockIdx.x - lu * S;
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
     s_toff[i] = a.taps[i].x;
     s_tb[i] = a.taps[i].y;
   }
+  for (int i = tid; i < a.L && i < 64; i += kRangeNT) s_lad[i] = a.ladder[i];
   const int xb = x0 + wx0;  // image column of staged column 0
   if (a.img_def == nullptr) {
     // 16-byte vector loads of aligned chunks covering each staged row part;
@@ -276,6 +278,14 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
     }
     __syncthreads();
     volatile int* vb = &s_bound;
+    // breakpoints: D >= hi + 2 lr_se - 2 N + 1 lets the unit use ladder length N
+    auto level_of = [&](int d) -> int {
+      for (int i = 0; i < a.L; ++i) {
+        const int th = hi + 2 * a.lr_se - 2 * s_lad[i] + 1;
+        if (th <= d) return th;
+      }
+      return INT32_MIN;
+    };
     // every lane walks its own queue of pixels (q += kRangeNT), one 8-tap group
     // per iteration, so lanes that stop early do not wait for the slowest one
     const int rows = jy_end - oy0, cols = jx_end - jx_beg;
@@ -286,13 +296,20 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
       const int jy = (int)(((float)q + 0.5f) * inv_cols);  // exact for q < 2^22
       return jy * wx + (q - jy * cols) + xoff;
     };
+    // A pixel may stop as soon as g reaches the breakpoint level below the
+    // running minimum: only the interval between ladder breakpoints that D
+    // falls into changes the unit's tonal length.
     int q = tid;
     if (q < npx) {
-      int base = base_of(q), t = 0, g = INT32_MIN;
+      int base = base_of(q), t = 0, g = INT32_MIN, seen = INT32_MIN, lvl = INT32_MIN;
       while (true) {
         const int bnd = *vb;
-        if (bnd <= floor_d) break;  // no clamp possible: stop (D is then only an upper bound)
-        if (t >= a.ntaps || g >= bnd) {
+        if (bnd != seen) {
+          seen = bnd;
+          lvl = level_of(bnd);
+        }
+        if (lvl <= floor_d) break;  // no clamp possible: stop
+        if (t >= a.ntaps || g >= lvl) {
           if (t >= a.ntaps && g < bnd) atomicMin(&s_bound, g);
           q += kRangeNT;
           if (q >= npx) break;
@@ -315,7 +332,18 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
     }
     __syncthreads();
   }
-  const int bound = (stage && lo <= hi) ? s_bound : INT32_MAX;
+  // the unit's lower bound: the breakpoint level of the minimum (INT32_MIN: no clamp)
+  int bound = INT32_MAX;
+  if (stage && lo <= hi && s_bound != INT32_MAX) {
+    bound = INT32_MIN;
+    for (int i = 0; i < a.L; ++i) {
+      const int th = hi + 2 * a.lr_se - 2 * s_lad[i] + 1;
+      if (th <= s_bound) {
+        bound = th > lo + a.lr_se ? th : INT32_MIN;
+        break;
+      }
+    }
+  }
 
   if (S == 1) {
     if (tid == 0) unit_finish(a, img, unit, lo, hi, bound);
@@ -326,9 +354,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
     int* pr = a.part + ((size_t)img * a.units + unit) * 8;
     atomicMin(pr + 0, lo);
     atomicMax(pr + 1, hi);
-    // a split cut at its own floor only knows D <= its floor: no clamp then
-    const int pb = (bound <= lo + a.lr_se) ? INT32_MIN : bound;
-    atomicMin(pr + 2, pb);
+    atomicMin(pr + 2, bound);
     __threadfence();
     s_last = atomicAdd(pr + 3, 1) == S - 1;
   }

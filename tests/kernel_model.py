@@ -316,6 +316,11 @@ def model_clamped_units(img, defined, se, se_def, se_lo, *, mode="dilate", crop=
                             s = win[jy + dy, jx + dx]
                             g = max(g, (s if s >= 0 else -32768) + int(bp[my - 1 - dy, mx - 1 - dx]))
                         D = g if D is None else min(D, g)
+                # fm_range.cuh reports the ladder breakpoint level of the minimum
+                # (hi + 2 lr_se - 2N + 1 for the smallest N whose level is <= D)
+                if D is not None:
+                    lev = next((hi + 2 * lr_se - 2 * n + 1 for n in ladder if hi + 2 * lr_se - 2 * n + 1 <= D), None)
+                    D = lev if lev is not None and lev > lo + lr_se else None
                 if D is not None and D - lr_se > c:
                     c = min(D - lr_se, hi)
             lr = (hi - c) + lr_se if any_ else lr_se
