@@ -186,6 +186,7 @@ const TonalVariant kTonal[] = {
     FM_TV(125), FM_TV(128), FM_TV(135), FM_TV(144), FM_TV(150), FM_TV(160)};
 static_assert(sizeof(kTonal) / sizeof(TonalVariant) == kTonalCount, "tonal variant table");
 
+constexpr int kAuxStreams = 3;
 int g_tonal_pipe_occ[kTonalCount];   // CTAs per SM of each pipelined variant (0: not pipelined)
 int g_num_sms = 148;
 const bool g_tonal_nopipe = std::getenv("FM_TONAL_NOPIPE") != nullptr;  // A/B switch for measurements
@@ -246,6 +247,7 @@ struct fm_plan {
   int DY = 0, DX = 0;
   int64_t OH = 1, OW = 1, off_y = 0, off_x = 0;
   int k_chunk = 1, kchunks = 1;
+  int conv_occ = 1;  // conv CTAs per SM
   int64_t ipc = 1;  // images per launch
   size_t conv_smem = 0, tonal_smem = 0;
   int tonal_threads = 128, tonal_stride = 1;
@@ -289,6 +291,8 @@ struct fm_plan {
   int* h_counts = nullptr;                // mapped pinned [L], written by publish_counts
   int* h_counts_dev = nullptr;            // its device alias
   cudaEvent_t count_ev = nullptr;
+  cudaStream_t aux[kAuxStreams] = {};     // tonal launches side by side
+  cudaEvent_t ev_fork = nullptr, ev_join[kAuxStreams] = {};
   int64_t planes_done = 0, units_done = 0; // for the plan's mean planes per unit
   // 256x256 tiles through an HBM scratch (fm_bigtile.cuh) for wide SEs
   bool big = false;
@@ -332,6 +336,11 @@ void free_plan(fm_plan* p) {
   if (p->ev_done) cudaEventDestroy(p->ev_done);
   if (p->h_counts) cudaFreeHost(p->h_counts);
   if (p->count_ev) cudaEventDestroy(p->count_ev);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  for (int i = 0; i < kAuxStreams; ++i) {
+    if (p->aux[i]) cudaStreamDestroy(p->aux[i]);
+    if (p->ev_join[i]) cudaEventDestroy(p->ev_join[i]);
+  }
   cudaSetDevice(prev);
   delete p;
 }
@@ -631,6 +640,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   int kch = (int)std::min<int64_t>(p->K, std::max<int64_t>(1, (target + base - 1) / base));
   p->k_chunk = (p->K + kch - 1) / kch;
   p->kchunks = (p->K + p->k_chunk - 1) / p->k_chunk;
+  p->conv_occ = occ;
   {
     const double pts = p->two_d ? (double)p->PY * p->PX : (double)p->PX;
     const double tiles_per_unit = p->two_d ? 1.0 : (double)p->PY;
@@ -662,6 +672,11 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   if ((e = cudaHostAlloc(&p->h_counts, sizeof(int) * L, cudaHostAllocMapped)) != cudaSuccess) return cfail(e, "pinned alloc");
   if ((e = cudaHostGetDevicePointer(&p->h_counts_dev, p->h_counts, 0)) != cudaSuccess) return cfail(e, "pinned map");
   if ((e = cudaEventCreateWithFlags(&p->count_ev, cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+  if ((e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+  for (int i = 0; i < kAuxStreams; ++i) {
+    if ((e = cudaStreamCreateWithFlags(&p->aux[i], cudaStreamNonBlocking)) != cudaSuccess) return cfail(e, "stream");
+    if ((e = cudaEventCreateWithFlags(&p->ev_join[i], cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+  }
   {
     const size_t np = (size_t)p->ipc * p->units;
     if ((e = cudaMalloc(&p->range_part, sizeof(int) * 8 * np)) != cudaSuccess) return cfail(e, "range alloc");
@@ -919,11 +934,28 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     a.wpx = p->wpx;
     a.bucket_count = p->bucket_count;
     a.bucket_list = p->bucket_list;
+    a.ladder = p->d_ladder;
     a.cap = (int)cap;
     a.L = L;
+    // Few units (one small image): split every unit's planes into chunks so the
+    // conv grid fills the GPU; that needs the per-ladder counts first.  Many
+    // units: one CTA per unit (all its planes), launched before the host waits.
+    const int64_t conv_target = (int64_t)g_num_sms * p->conv_occ * 2;
+    const bool dyn = !p->big && (int64_t)nu * n < conv_target;
     int e0 = -1;
-    if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
+    auto launch_conv = [&](unsigned grid) -> int {
+      if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
+      p->var->conv(dim3(grid), p->conv_smem, s, a);
+      g_launches++;
+      FM_CUDA(cudaGetLastError());
+      if (p->timing) {
+        FM_CUDA(cudaEventRecord(next_event(p), s));
+        p->pending_conv.push_back({e0, e0 + 1});
+      }
+      return FM_OK;
+    };
     if (p->big) {
+      if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
       BigArgs b{};
       b.img = a.img;
       b.img_def = a.img_def;
@@ -958,19 +990,34 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       big_cols_kernel<false><<<dim3(kBig / kBigCols, p->K, z), kBigColsNT, kBigColsSmem, s>>>(b);
       big_rows_kernel<false, false><<<dim3(inv_blocks, p->K, z), kBigNT, kBigRowsSmem, s>>>(b);
       g_launches += 3;
-    } else {
-      p->var->conv(dim3((unsigned)nu, p->kchunks, n), p->conv_smem, s, a);
-      g_launches++;
-    }
-    FM_CUDA(cudaGetLastError());
-    if (p->timing) {
-      FM_CUDA(cudaEventRecord(next_event(p), s));
-      p->pending_conv.push_back({e0, e0 + 1});
+      FM_CUDA(cudaGetLastError());
+      if (p->timing) {
+        FM_CUDA(cudaEventRecord(next_event(p), s));
+        p->pending_conv.push_back({e0, e0 + 1});
+      }
+    } else if (!dyn) {
+      a.k_chunk = p->K;
+      int rc = launch_conv((unsigned)(nu * n));
+      if (rc) return rc;
     }
 
     // ---- the tonal kernels need the per-ladder unit counts (ready long before
     // the conv kernel finishes; the host waits only for the small copy)
     FM_CUDA(cudaEventSynchronize(p->count_ev));
+    if (dyn) {
+      int64_t planes_tot = 0;
+      for (int li = 0; li < L; ++li)
+        planes_tot += (int64_t)reinterpret_cast<volatile int*>(p->h_counts)[li] * (p->ladder[li] + 1);
+      const int kc = (int)std::max<int64_t>(1, (planes_tot + conv_target - 1) / conv_target);
+      int64_t jobs = 0;
+      for (int li = 0; li < L; ++li)
+        jobs += (int64_t)reinterpret_cast<volatile int*>(p->h_counts)[li] * ((p->ladder[li] + kc) / kc);
+      a.k_chunk = kc;
+      if (jobs > 0) {
+        int rc = launch_conv((unsigned)jobs);
+        if (rc) return rc;
+      }
+    }
     TonalArgs t{};
     t.chat = p->chat;
     t.K_max = p->K;
@@ -999,10 +1046,22 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     int e1 = -1;
     if (p->timing) { e1 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
     double planes = 0, tonal_b = 0;
-    for (int li = 0; li < L; ++li) {
+    // one launch per ladder entry in use, spread over the aux streams so the
+    // small ones (few units each) run side by side; joined back into s
+    int nlaunch = 0;
+    for (int li = 0; li < L; ++li) nlaunch += reinterpret_cast<volatile int*>(p->h_counts)[li] > 0;
+    const int nstreams = std::min(nlaunch, 1 + kAuxStreams);
+    if (nstreams > 1) {
+      FM_CUDA(cudaEventRecord(p->ev_fork, s));
+      for (int i = 0; i < nstreams - 1; ++i) FM_CUDA(cudaStreamWaitEvent(p->aux[i], p->ev_fork, 0));
+    }
+    int launch_i = 0;
+    for (int li = L - 1; li >= 0; --li) {
       const int cnt = reinterpret_cast<volatile int*>(p->h_counts)[li];
       if (cnt <= 0) continue;
       const int N = p->ladder[li];
+      const int si = launch_i++ % nstreams;
+      cudaStream_t ts = si == 0 ? s : p->aux[si - 1];
       t.N = N;
       t.T = 2 * N;
       t.list = p->bucket_list + (size_t)li * cap;
@@ -1012,10 +1071,10 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         t.njobs = cnt;
         const int64_t items = (int64_t)cnt * ((p->npx + tv->pipe_nt - 1) / tv->pipe_nt);
         const int grid = (int)std::min<int64_t>(items, (int64_t)g_num_sms * occ);
-        tv->pipe_fn(dim3((unsigned)grid), tv->pipe_nt, tv->pipe_smem, s, t);
+        tv->pipe_fn(dim3((unsigned)grid), tv->pipe_nt, tv->pipe_smem, ts, t);
       } else if (tv) {
         const int nt = tv->nt;
-        tv->fn(dim3((unsigned)cnt, (unsigned)((p->npx + nt - 1) / nt)), nt, tv->smem, s, t);
+        tv->fn(dim3((unsigned)cnt, (unsigned)((p->npx + nt - 1) / nt)), nt, tv->smem, ts, t);
       } else {
         t.nstages = (int)p->radix.size();
         for (size_t i = 0; i < p->radix.size(); ++i) t.radix[i] = p->radix[i];
@@ -1023,13 +1082,17 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         t.wT = p->wT;
         t.stride = p->tonal_stride;
         const int nt = p->tonal_threads;
-        tonal_kernel<<<dim3((unsigned)cnt, (unsigned)((p->npx + nt - 1) / nt)), nt, p->tonal_smem, s>>>(t);
+        tonal_kernel<<<dim3((unsigned)cnt, (unsigned)((p->npx + nt - 1) / nt)), nt, p->tonal_smem, ts>>>(t);
       }
       g_launches++;
       FM_CUDA(cudaGetLastError());
       planes += (double)cnt * (N + 1);
       tonal_b += (double)cnt * ((N + 1) * (double)p->npx * 8.0 +
                                 (double)p->npx * (out_size(p->d.out_dtype) + (valid ? 1.0 : 0.0)));
+    }
+    for (int i = 0; i < nstreams - 1; ++i) {
+      FM_CUDA(cudaEventRecord(p->ev_join[i], p->aux[i]));
+      FM_CUDA(cudaStreamWaitEvent(s, p->ev_join[i], 0));
     }
     p->planes_done += (int64_t)planes;
     p->units_done += (int64_t)n * nu;

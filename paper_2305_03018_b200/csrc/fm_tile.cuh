@@ -85,8 +85,10 @@ struct TileArgs {
   int K_max;                  // chat planes per unit (N_global + 1)
   int wpx;                    // plane stride of chat (even)
   // CONV launch order: jobs = the range kernel's work lists, largest tonal length first
+  // each unit's planes are split into chunks of k_chunk (one CTA each)
   const int* bucket_count;    // [L]
   const int2* bucket_list;    // [L][cap] (img, unit)
+  const int* ladder;          // [L] N of each ladder entry
   int cap, L;
 };
 
@@ -174,16 +176,18 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   float two_pi_over_T = a.two_pi_over_T;
   const float4* spec_base = a.spec;
   int unit = a.unit0 + blockIdx.x;   // absolute unit (tile, or group of 1-D tiles)
+  int kchunk_idx = blockIdx.y;        // SPEC: grid y; CONV: from the job list
   if constexpr (!SPEC) {
     // job J of this launch -> (img, unit) from the per-ladder work lists, walked
     // from the longest tonal length down: the longest units start first, so
     // the launch ends without a tail of long stragglers
-    __shared__ int s_job[2];
+    __shared__ int s_job[3];
     if (warp == 0) {
-      int rem = (int)(blockIdx.z * gridDim.x + blockIdx.x), found = -1;
+      int rem = (int)blockIdx.x, found = -1, fch = 1;
       for (int top = a.L - 1; top >= 0 && found < 0; top -= 32) {
         const int li = top - lane;
-        const int c = li >= 0 ? a.bucket_count[li] : 0;
+        const int ch = li >= 0 ? (a.ladder[li] + a.k_chunk) / a.k_chunk : 1;   // ceil((N+1)/k_chunk)
+        const int c = li >= 0 ? a.bucket_count[li] * ch : 0;
         int incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -194,23 +198,27 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
         if (m) {
           const int l0 = __ffs(m) - 1;
           rem -= __shfl_sync(0xffffffffu, incl - c, l0);
+          fch = __shfl_sync(0xffffffffu, ch, l0);
           found = top - l0;
         } else {
           rem -= __shfl_sync(0xffffffffu, incl, 31);
         }
       }
       if (lane == 0) {
-        const int2 job = a.bucket_list[(size_t)max(found, 0) * a.cap + rem];
+        const int u = rem / fch;
+        const int2 job = a.bucket_list[(size_t)max(found, 0) * a.cap + u];
         s_job[0] = job.x;
         s_job[1] = job.y;
+        s_job[2] = rem - u * fch;   // plane chunk of the unit
       }
     }
     __syncthreads();
     img = s_job[0];
     unit = s_job[1];
+    kchunk_idx = s_job[2];
     const int4 up = a.unit_param[(size_t)img * a.units + unit];
     K = up.y + 1;
-    if ((int)blockIdx.y * a.k_chunk >= K) return;   // this k-chunk is beyond the unit's planes
+    if (kchunk_idx * a.k_chunk >= K) return;   // this k-chunk is beyond the unit's planes
     T = 2 * up.y;
     magicT = (uint32_t)(0x100000000ull / (uint64_t)T);
     two_pi_over_T = 6.28318530717958647692f / (float)T;
@@ -277,7 +285,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   __syncthreads();
   const int ty = (TWO_D && !SPEC) ? unit / a.tiles_x : 0;
   const int tx = (TWO_D && !SPEC) ? unit - ty * a.tiles_x : 0;
-  const int k_begin = blockIdx.y * a.k_chunk;
+  const int k_begin = kchunk_idx * a.k_chunk;
   const int k_end = min(K, k_begin + a.k_chunk);
   // window-local output planes of this unit (slot = launch-local unit index)
   float2* chat_unit = SPEC ? nullptr : a.chat + ((size_t)img * a.upl + (unit - a.unit0)) * a.K_max * (size_t)a.wpx;
