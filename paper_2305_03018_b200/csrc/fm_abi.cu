@@ -941,7 +941,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     // conv grid fills the GPU; that needs the per-ladder counts first.  Many
     // units: one CTA per unit (all its planes), launched before the host waits.
     const int64_t conv_target = (int64_t)g_num_sms * p->conv_occ * 2;
-    const bool dyn = !p->big && (int64_t)nu * n < conv_target;
+    const bool dyn = !p->big && (int64_t)nu * n < conv_target && p->k_chunk > 1;
     int e0 = -1;
     auto launch_conv = [&](unsigned grid) -> int {
       if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
@@ -996,8 +996,10 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         p->pending_conv.push_back({e0, e0 + 1});
       }
     } else if (!dyn) {
-      a.k_chunk = p->K;
-      int rc = launch_conv((unsigned)(nu * n));
+      // plan-time chunking (one chunk per unit for large launches); CTAs past
+      // the actual job count exit at once
+      a.k_chunk = p->k_chunk;
+      int rc = launch_conv((unsigned)(nu * n * p->kchunks));
       if (rc) return rc;
     }
 

@@ -205,14 +205,19 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
         }
       }
       if (lane == 0) {
-        const int u = rem / fch;
-        const int2 job = a.bucket_list[(size_t)max(found, 0) * a.cap + u];
-        s_job[0] = job.x;
-        s_job[1] = job.y;
-        s_job[2] = rem - u * fch;   // plane chunk of the unit
+        if (found < 0) {
+          s_job[0] = -1;   // grid sized before the counts were known: no job left
+        } else {
+          const int u = rem / fch;
+          const int2 job = a.bucket_list[(size_t)found * a.cap + u];
+          s_job[0] = job.x;
+          s_job[1] = job.y;
+          s_job[2] = rem - u * fch;   // plane chunk of the unit
+        }
       }
     }
     __syncthreads();
+    if (s_job[0] < 0) return;
     img = s_job[0];
     unit = s_job[1];
     kchunk_idx = s_job[2];
