@@ -122,7 +122,7 @@ struct Variant {
 
 #define FM_VARIANT(TD, PY, PX, NT)                                                        \
   Variant {                                                                               \
-    TD, PY, PX, NT, TileCfg<PY, PX, NT, TD>::kSmemFixed, &launch_tile<PY, PX, NT, TD, false>, \
+    TD, PY, PX, NT, TileCfg<PY, PX, NT, TD>::kSmemTotal, &launch_tile<PY, PX, NT, TD, false>, \
         &launch_tile<PY, PX, NT, TD, true>, &set_smem_attr<PY, PX, NT, TD, false>,          \
         &set_smem_attr<PY, PX, NT, TD, true>                                                \
   }
@@ -282,6 +282,9 @@ struct fm_plan {
   int units = 1, wpx = 1, npx = 1, win_y = 1, win_x = 1, unit_step_x = 0;  // wpx: even plane stride
   std::vector<int2> taps;                 // clamp-bound taps of fm_range.cuh, best first
   int* range_part = nullptr;              // [ipc*units][8] split partials of fm_range.cuh
+  float2* enc_tab = nullptr;              // per ladder entry: exp(-2 pi i j / T), j < T, then 0
+  int* d_enc_off = nullptr;               // [L] offsets into enc_tab
+  std::vector<int> enc_off;
   int upl = 1;                            // units per launch (chat slots per image)
   int* d_ladder = nullptr;
   int64_t* d_spec_off = nullptr;
@@ -325,6 +328,8 @@ void free_plan(fm_plan* p) {
   cudaFree(p->d_ladder);
   cudaFree(p->d_spec_off);
   cudaFree(p->range_part);
+  cudaFree(p->enc_tab);
+  cudaFree(p->d_enc_off);
   cudaFree(p->unit_param);
   cudaFree(p->bucket_count);
   cudaFree(p->bucket_list);
@@ -688,6 +693,23 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     }
     cudaMemcpy(p->range_part, init.data(), sizeof(int) * 8 * np, cudaMemcpyHostToDevice);
   }
+  {
+    // encode tables, FP64-rounded: entry j = exp(-2 pi i j / T), entry T = 0
+    std::vector<float2> tab;
+    for (int li = 0; li < L; ++li) {
+      const int Tl = 2 * p->ladder[li];
+      p->enc_off.push_back((int)tab.size());
+      for (int j = 0; j < Tl; ++j) {
+        const double ang = -2.0 * kPi * j / Tl;
+        tab.push_back(make_float2((float)std::cos(ang), (float)std::sin(ang)));
+      }
+      tab.push_back(make_float2(0.f, 0.f));
+    }
+    if ((e = cudaMalloc(&p->enc_tab, sizeof(float2) * tab.size())) != cudaSuccess) return cfail(e, "table alloc");
+    if ((e = cudaMalloc(&p->d_enc_off, sizeof(int) * L)) != cudaSuccess) return cfail(e, "table alloc");
+    cudaMemcpy(p->enc_tab, tab.data(), sizeof(float2) * tab.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(p->d_enc_off, p->enc_off.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
+  }
   cudaMemcpy(p->d_ladder, p->ladder.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
   cudaMemcpy(p->d_spec_off, p->spec_off.data(), sizeof(int64_t) * L, cudaMemcpyHostToDevice);
   if ((e = cudaMalloc(&p->twN, sizeof(float2) * std::max(1, p->N))) != cudaSuccess) return cfail(e, "table alloc");
@@ -763,6 +785,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     a.spec = p->spec + p->spec_off[li];
     a.spec_out = p->spec + p->spec_off[li];
     a.spec_scale = (float)(1.0 / ((double)(p->two_d ? p->PY : 1) * p->PX * Tl));
+    a.enc_tab = p->enc_tab + p->enc_off[li];
     a.tiles_x = 1;
     a.tiles_total = 1;
     a.err = p->stats + 1;
@@ -935,6 +958,8 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     a.bucket_count = p->bucket_count;
     a.bucket_list = p->bucket_list;
     a.ladder = p->d_ladder;
+    a.enc_tab = p->enc_tab;
+    a.enc_off = p->d_enc_off;
     a.cap = (int)cap;
     a.L = L;
     // Few units (one small image): split every unit's planes into chunks so the

@@ -76,6 +76,8 @@ struct TileArgs {
   float4* spec_out;           // SPEC writes
   float spec_scale;           // SPEC: 1 / (PY_eff * PX * T)
   float2* chat;               // CONV: [imgs][units][K_max][wpx] (window-local pixels)
+  const float2* enc_tab;      // encode tables exp(-2 pi i j / T), j <= T (entry T = 0); SPEC: this T's
+  const int* enc_off;         // CONV: [ladder] offset of the ladder entry's table
   int* err;                   // value-range error flag
   // per-unit tonal length (CONV): a unit is one 2-D tile or one group of PY 1-D tiles
   const int4* unit_param;     // [imgs][units]: x = anchor (clamp level: v = f - anchor, or anchor - f for erosion), y = N_t, z = ladder index
@@ -130,6 +132,11 @@ struct TileCfg {
   static constexpr bool kTwxInPad = kTwxSlots <= PY;
   static constexpr int kTwxBytes = kTwxInPad ? 0 : kTwxSlots * 16;
   static constexpr int kSmemFixed = kBufBytes + kSpecBytes + kTvBytes + kTwxBytes;
+  // encode table w_T^{-j}, j <= T (entry T = 0 for "no pixel"), in what is left
+  // of the 227 KB (P = 128: T <= 95; beyond, the table is read from L1/L2)
+  static constexpr int kEncAvail = (227 * 1024 - kSmemFixed - 256) / 8;  // 256: static smem of the kernel
+  static constexpr int kEncSlots = kEncAvail < 0 ? 0 : (kEncAvail < 161 ? kEncAvail : 161);
+  static constexpr int kSmemTotal = kSmemFixed + kEncSlots * 8;
 };
 
 __device__ __forceinline__ int load_img(const void* img, int dtype, int64_t i) {
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   // uses the smallest ladder length that holds its own value range
   int T = a.T, K = a.K, enc_bias = a.enc_bias;
   uint32_t magicT = a.magicT;
-  float two_pi_over_T = a.two_pi_over_T;
+  int unit_li = 0;   // ladder entry of a CONV unit
   const float4* spec_base = a.spec;
   int unit = a.unit0 + blockIdx.x;   // absolute unit (tile, or group of 1-D tiles)
   int kchunk_idx = blockIdx.y;        // SPEC: grid y; CONV: from the job list
@@ -226,10 +233,17 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     if (kchunk_idx * a.k_chunk >= K) return;   // this k-chunk is beyond the unit's planes
     T = 2 * up.y;
     magicT = (uint32_t)(0x100000000ull / (uint64_t)T);
-    two_pi_over_T = 6.28318530717958647692f / (float)T;
+    unit_li = up.z;
     enc_bias = a.enc_sign > 0 ? -up.x : up.x;
     spec_base = a.spec + a.spec_off[up.z];
   }
+  // encode table of this unit's T: shared memory when it fits, else global (L1)
+  const float2* enc_g = SPEC ? a.enc_tab : a.enc_tab + a.enc_off[unit_li];
+  float2* enc_s = reinterpret_cast<float2*>(smem_raw + C::kSmemFixed);
+  const bool enc_in_smem = T + 1 <= C::kEncSlots;
+  if (enc_in_smem)
+    for (int j = tid; j <= T; j += NT) enc_s[j] = enc_g[j];
+  const float2* encT = enc_in_smem ? enc_s : enc_g;
 
   // ---- stage the tile's tonal indices v(x) (kSent = no entry)
   {
@@ -309,19 +323,14 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
 #pragma unroll
       for (int g = 0; g < C::NBUF; ++g) spec_fetch(k, g);
     }
-    // encode helper: w_T^{k v} = exp(-2 pi i ((k v) mod T) / T).  The index is
-    // reduced exactly in integers to r' in [-T/2, T/2], so the MUFU sin/cos
-    // argument stays in [-pi, pi] (abs. error < 4e-7, far inside the 0.5 budget).
-    // Branch-free: the sentinel's (meaningless) angle is computed and then masked.
+    // encode helper: w_T^{k v} = exp(-2 pi i ((k v) mod T) / T) from the table;
+    // the index is reduced exactly in integers, the sentinel reads entry T = 0
     auto enc = [&](uint32_t t) -> float2 {
       const uint32_t n = (uint32_t)k * t;
       uint32_t r = n - __umulhi(n, magicT) * (uint32_t)T;
       r = (r >= (uint32_t)T) ? r - (uint32_t)T : r;
-      const int rr = (2 * r > (uint32_t)T) ? (int)r - T : (int)r;
-      float sn, cs;
-      __sincosf((float)rr * two_pi_over_T, &sn, &cs);
-      const bool live = t != kSent;
-      return make_float2(live ? cs : 0.f, live ? -sn : 0.f);
+      r = (t == kSent) ? (uint32_t)T : r;
+      return encT[r];
     };
 
     if constexpr (TWO_D) {
