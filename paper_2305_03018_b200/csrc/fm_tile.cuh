@@ -31,6 +31,7 @@
 //    chunks ahead, so its L2 latency overlaps the FFT passes instead of
 //    stalling the spectral product.
 #pragma once
+#include <type_traits>
 #include "fm_dft.cuh"
 
 namespace fm {
@@ -240,10 +241,19 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   // encode table of this unit's T: shared memory when it fits, else global (L1)
   const float2* enc_g = SPEC ? a.enc_tab : a.enc_tab + a.enc_off[unit_li];
   float2* enc_s = reinterpret_cast<float2*>(smem_raw + C::kSmemFixed);
-  const bool enc_in_smem = T + 1 <= C::kEncSlots;
+  // 2-D with room for two tables: per-plane tables M_k[t] = w_T^{(k t) mod T}
+  // (double-buffered, M_k[T] = 0 for "no pixel"), so the encode is one LDS;
+  // else the base table w_T^j with the index (k t) mod T reduced per element
+  const bool mtab = TWO_D && 2 * (T + 1) <= C::kEncSlots;
+  const bool enc_in_smem = !mtab && T + 1 <= C::kEncSlots;
   if (enc_in_smem)
     for (int j = tid; j <= T; j += NT) enc_s[j] = enc_g[j];
   const float2* encT = enc_in_smem ? enc_s : enc_g;
+  auto build_mtab = [&](int kk) {
+    float2* M = enc_s + (kk & 1) * (T + 1);
+    for (int j = tid; j <= T; j += NT) M[j] = j < T ? enc_g[(kk * j) % T] : make_float2(0.f, 0.f);
+  };
+  const uint16_t sent = mtab ? (uint16_t)T : kSent;
 
   // ---- stage the tile's tonal indices v(x) (kSent = no entry)
   {
@@ -255,7 +265,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     int bad = 0;
     for (int p = tid; p < C::NPTS; p += NT) {
       const int py = p / PX, px = p - (p / PX) * PX;
-      uint16_t t = kSent;
+      uint16_t t = sent;
       if (SPEC) {
         const int sy = TWO_D ? py : 0;
         if (sy < a.my && px < a.mx) {
@@ -301,6 +311,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     const float2 w1 = c_tw[TwOff<PX>::v + ((n2 + 1) * k1) % PX];
     *twx_slot(j) = make_float4(w0.x, w0.y, w1.x, w1.y);
   }
+  if (mtab) build_mtab(kchunk_idx * a.k_chunk);
   __syncthreads();
   const int ty = (TWO_D && !SPEC) ? unit / a.tiles_x : 0;
   const int tx = (TWO_D && !SPEC) ? unit - ty * a.tiles_x : 0;
@@ -335,31 +346,44 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
 
     if constexpr (TWO_D) {
       // ---------------- forward y, pass A (with encode): item (xp, n2)
+      const float2* Mk = enc_s + (k & 1) * (T + 1);
+      auto y_pass_a = [&](auto use_m) {
 #pragma unroll
-      for (int g = 0; g < C::G_yA; ++g) {
-        const int i = tid + NT * g;
-        const int xp = i % C::XP, n2 = i / C::XP;
-        float2 wa[C::R1y], wb[C::R1y];
+        for (int g = 0; g < C::G_yA; ++g) {
+          const int i = tid + NT * g;
+          const int xp = i % C::XP, n2 = i / C::XP;
+          float2 wa[C::R1y], wb[C::R1y];
 #pragma unroll
-        for (int n1 = 0; n1 < C::R1y; ++n1) {
-          const uint32_t tt = tv32[((n2 + C::R2y * n1) * PX) / 2 + xp];
-          wa[n1] = enc(tt & 0xFFFFu);
-          wb[n1] = enc(tt >> 16);
-        }
-        dft<C::R1y, false>(wa);
-        dft<C::R1y, false>(wb);
-#pragma unroll
-        for (int k1 = 0; k1 < C::R1y; ++k1) {
-          float2 za = wa[k1], zb = wb[k1];
-          if (k1 != 0) {
-            const float2 w = c_tw[TwOff<PY>::v + n2 * k1];
-            za = cmul(za, w);
-            zb = cmul(zb, w);
+          for (int n1 = 0; n1 < C::R1y; ++n1) {
+            const uint32_t tt = tv32[((n2 + C::R2y * n1) * PX) / 2 + xp];
+            if constexpr (decltype(use_m)::value) {
+              wa[n1] = Mk[tt & 0xFFFFu];
+              wb[n1] = Mk[tt >> 16];
+            } else {
+              wa[n1] = enc(tt & 0xFFFFu);
+              wb[n1] = enc(tt >> 16);
+            }
           }
-          st2(n2 + C::R2y * k1, 2 * xp, za, zb);
+          dft<C::R1y, false>(wa);
+          dft<C::R1y, false>(wb);
+#pragma unroll
+          for (int k1 = 0; k1 < C::R1y; ++k1) {
+            float2 za = wa[k1], zb = wb[k1];
+            if (k1 != 0) {
+              const float2 w = c_tw[TwOff<PY>::v + n2 * k1];
+              za = cmul(za, w);
+              zb = cmul(zb, w);
+            }
+            st2(n2 + C::R2y * k1, 2 * xp, za, zb);
+          }
         }
-      }
+      };
+      if (mtab) y_pass_a(std::true_type{});
+      else y_pass_a(std::false_type{});
       __syncthreads();
+      // next plane's table into the other buffer (its last reader, plane k-1's
+      // y pass A, finished before this plane's first barrier)
+      if (mtab && k + 1 < k_end) build_mtab(k + 1);
       // ---------------- forward y, pass B: item (xp, k1)
 #pragma unroll
       for (int g = 0; g < C::G_yB; ++g) {
