@@ -572,13 +572,18 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
         const int ox = tx * a.QX + x - (a.mx - 1);
         const bool va = x >= a.mx - 1 && ox < a.OW;
         const bool vb = x + 1 >= a.mx - 1 && ox + 1 < a.OW;
+        // rows y = n2 + R2y*n1 in [my-1, y_end) are stored; hoisted out of the n1 loop
+        const int y_end = min(PY, a.OH - ty * a.QY + (a.my - 1));
+        float2* col = dst + (ptrdiff_t)n2 * a.QX + x;
+        const ptrdiff_t step = (ptrdiff_t)C::R2y * a.QX;
+        // 16-byte stores when both columns are valid and every row start is aligned
+        const bool pair = va && vb && (a.QX % 2 == 0) && ((reinterpret_cast<uintptr_t>(col) & 15) == 0);
 #pragma unroll
         for (int n1 = 0; n1 < C::R1y; ++n1) {
           const int y = n2 + C::R2y * n1;
-          const int oy = ty * a.QY + y - (a.my - 1);
-          if (y >= a.my - 1 && oy < a.OH) {
-            float2* row = dst + (size_t)y * a.QX + x;
-            if (va && vb && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+          if (y >= a.my - 1 && y < y_end) {
+            float2* row = col + n1 * step;
+            if (pair) {
               *reinterpret_cast<float4*>(row) = make_float4(wa[n1].x, wa[n1].y, wb[n1].x, wb[n1].y);
             } else {
               if (va) row[0] = wa[n1];
