@@ -9,7 +9,9 @@
  *                 Minkowski-range result into f's domain (_paste, morphology.py:51-62)
  *   erode_naive   morphology.py:88-113 — acc = min of f(x+y)-b(y); no pair -> neutral
  * Row-parallel over pthreads; the inner loop is a contiguous max/min over one
- * image row, so it auto-vectorises.
+ * image row, so it auto-vectorises.  Arithmetic is int32 with +-2^30
+ * sentinels (the reference uses int64 and +-2^40, morphology.py:27): valid for
+ * |f| + |b| < 2^29, which every test input respects.
  *
  * Build: make -C oracle   ->   oracle/_build/libmorph_oracle.so
  */
