@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FM_ABI_VERSION 2
+#define FM_ABI_VERSION 3
 
 typedef enum fm_status {
   FM_OK = 0,
@@ -71,7 +71,19 @@ typedef struct fm_plan_desc {
   int32_t tile;          /* 0 = auto, else forced FFT tile edge (16..256) */
   int32_t tonal_len;     /* 0 = auto, else forced tonal length T (even, > l_R) */
   int32_t out_dtype;     /* fm_out_dtype of the output values (0 = int32) */
+  int32_t flags;         /* FM_FLAG_* */
 } fm_plan_desc;
+
+/* fm_plan_desc.flags */
+enum {
+  /* Count-volume mode (dilation only): fm_execute writes, instead of the dilation,
+   * the count volume of umbra(f) (*) umbra(b) over the full Minkowski range
+   * (crop must be 0) as int32 [batch][OH][OW][count_len], count_len = l_r + 1,
+   * degree index d <-> degree d + img_min + se_min; replaces
+   * conv_full_fft_with_stats(build_umbra(f), build_umbra(b)) (fft_conv.py:128-150,
+   * umbra.py:177-186).  `valid` still receives "any count". */
+  FM_FLAG_COUNTS = 1
+};
 
 /* Read-only facts about a plan (for stats / bench / tests). */
 typedef struct fm_plan_info {
@@ -88,6 +100,7 @@ typedef struct fm_plan_info {
   int64_t scratch_bytes;
   int32_t se_min, se_max;  /* over defined SE entries (after reflection for erosion) */
   int32_t se_count;        /* defined SE entries */
+  int32_t count_len;       /* FM_FLAG_COUNTS: degrees per output pixel (l_r + 1), else 0 */
 } fm_plan_info;
 
 typedef struct fm_stats {
@@ -163,6 +176,12 @@ int fm_naive(const fm_plan_desc* desc, const int32_t* se_values, const uint8_t* 
 int64_t fm_kernel_launches(void);
 
 const char* fm_last_error(void);
+
+/* Exact full-mode N-D (ndim 1..3) integer convolution on the device:
+ * out[k] = sum_i a[i] b[k-i], shapes sa + sb - 1 (direct_full, fft_conv.py:94-106;
+ * conv_full_direct, fft_conv.py:109-111).  int64 device buffers, row-major. */
+int fm_conv_full_direct(int ndim, const int64_t* a_shape, const int64_t* a, const int64_t* b_shape,
+                        const int64_t* b, int64_t* out, void* stream);
 int fm_abi_version(void);
 
 #ifdef __cplusplus

@@ -10,11 +10,15 @@ from .morphology import (MorphMethod, beucher_gradient, closing, dilate, dilate_
                          dilate_naive, erode, erode_fft, erode_naive, negate, opening,
                          reflect)
 from ._lib import PrecisionBudgetError
+from .fft_conv import (ConvPlan, FftStats, OffsetArray, conv_full_direct, conv_full_fft,
+                       conv_full_fft_with_stats, next_fast_size, set_fft_workers)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "GridFunction", "MorphMethod", "PrecisionBudgetError", "beucher_gradient", "closing",
+    "ConvPlan", "FftStats", "GridFunction", "MorphMethod", "OffsetArray", "PrecisionBudgetError",
+    "beucher_gradient", "closing", "conv_full_direct", "conv_full_fft", "conv_full_fft_with_stats",
+    "next_fast_size", "set_fft_workers",
     "dilate", "dilate_fft", "dilate_naive", "erode", "erode_fft", "erode_naive",
     "full_output_range", "intersect_ranges", "negate", "opening", "reflect",
 ]

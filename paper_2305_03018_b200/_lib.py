@@ -24,8 +24,9 @@ FM_OUT_I32, FM_OUT_U8, FM_OUT_U16, FM_OUT_I16 = 0, 1, 2, 3
 EXPORTED = (
     "fm_plan_create", "fm_execute", "fm_execute_host", "fm_read_stats", "fm_reset_stats",
     "fm_plan_query", "fm_plan_destroy", "fm_naive", "fm_kernel_launches", "fm_last_error",
-    "fm_abi_version", "fm_set_timing", "fm_get_timing",
+    "fm_abi_version", "fm_set_timing", "fm_get_timing", "fm_conv_full_direct",
 )
+FM_FLAG_COUNTS = 1
 
 
 class PlanDesc(ctypes.Structure):
@@ -46,6 +47,7 @@ class PlanDesc(ctypes.Structure):
         ("tile", ctypes.c_int32),
         ("tonal_len", ctypes.c_int32),
         ("out_dtype", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
     ]
 
 
@@ -68,6 +70,7 @@ class PlanInfo(ctypes.Structure):
         ("se_min", ctypes.c_int32),
         ("se_max", ctypes.c_int32),
         ("se_count", ctypes.c_int32),
+        ("count_len", ctypes.c_int32),
     ]
 
 
@@ -129,6 +132,8 @@ def load() -> ctypes.CDLL:
         L.fm_get_timing.restype = ctypes.c_int
         L.fm_abi_version.argtypes = []
         L.fm_abi_version.restype = i32
+        L.fm_conv_full_direct.argtypes = [ctypes.c_int, vp, vp, vp, vp, vp, vp]
+        L.fm_conv_full_direct.restype = ctypes.c_int
         _lib = L
         return L
 

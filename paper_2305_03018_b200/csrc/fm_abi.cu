@@ -20,6 +20,7 @@
 
 #include "fftmorph_b200.h"
 #include "fm_bigtile.cuh"
+#include "fm_direct.cuh"
 #include "fm_naive.cuh"
 #include "fm_range.cuh"
 #include "fm_tile.cuh"
@@ -282,6 +283,7 @@ struct fm_plan {
   int units = 1, wpx = 1, npx = 1, win_y = 1, win_x = 1, unit_step_x = 0;  // wpx: even plane stride
   std::vector<int2> taps;                 // clamp-bound taps of fm_range.cuh, best first
   int* range_part = nullptr;              // [ipc*units][8] split partials of fm_range.cuh
+  bool counts = false;                    // FM_FLAG_COUNTS: count-volume output
   float2* enc_tab = nullptr;              // per ladder entry: exp(-2 pi i j / T), j < T, then 0
   int* d_enc_off = nullptr;               // [L] offsets into enc_tab
   std::vector<int> enc_off;
@@ -400,8 +402,12 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   const fm_plan_desc& d = *desc;
   if (d.img_min > d.img_max) return fail(FM_EINVAL, "img_min > img_max");
 
+  if (d.flags & ~FM_FLAG_COUNTS) return fail(FM_EINVAL, "unknown flags");
+  if ((d.flags & FM_FLAG_COUNTS) && (d.mode != FM_DILATE || d.crop))
+    return fail(FM_EINVAL, "count volumes need mode=dilate and crop=0");
   fm_plan* p = new fm_plan();
   p->d = d;
+  p->counts = (d.flags & FM_FLAG_COUNTS) != 0;
   p->device = d.device;
   p->two_d = d.ndim == 2;
   p->batch = d.batch;
@@ -565,7 +571,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
 
   // tonal ladder: each conv unit uses the smallest N_t of the ladder with
   // 2 N_t > its own l_R (fm_range.cuh); a forced tonal_len pins a single entry
-  if (d.tonal_len > 0) {
+  if (d.tonal_len > 0 || p->counts) {
     p->ladder = {p->N};
   } else {
     for (int i = 0; i < kTonalCount; ++i)
@@ -609,7 +615,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     if (const char* env = std::getenv("FM_RANGE_TAPS")) cap_taps = std::max(0, std::min(kMaxBoundTaps, std::atoi(env)));
     const size_t wsm = (size_t)p->win_y * p->win_x * sizeof(int16_t);
     const bool fits = p->vmax <= 32767 && (p->se_max - p->se_min) < 32768 && wsm <= kRangeSmemMax;
-    if (fits && cap_taps > 0) {
+    if (fits && cap_taps > 0 && !p->counts) {
       std::vector<std::pair<int64_t, int2>> cand;
       for (int py = 0; py < p->my; ++py)
         for (int px = 0; px < p->mx; ++px) {
@@ -821,6 +827,7 @@ int fm_plan_query(const fm_plan* p, fm_plan_info* info) {
   info->se_min = p->se_min;
   info->se_max = p->se_max;
   info->se_count = p->se_count;
+  info->count_len = p->counts ? p->lr + 1 : 0;
   return FM_OK;
 }
 
@@ -1070,6 +1077,11 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     t.se_min = p->se_min;
     t.fill = p->d.fill;
     t.dev_max = reinterpret_cast<float*>(p->stats);
+    if (p->counts) {
+      t.counts = reinterpret_cast<int32_t*>(out) + (size_t)c0 * npix * (size_t)(p->lr + 1);
+      t.count_len = p->lr + 1;
+      t.count_base = p->d.img_min;
+    }
     int e1 = -1;
     if (p->timing) { e1 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
     double planes = 0, tonal_b = 0;
@@ -1092,7 +1104,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       t.N = N;
       t.T = 2 * N;
       t.list = p->bucket_list + (size_t)li * cap;
-      const TonalVariant* tv = p->ladder_var[li];
+      const TonalVariant* tv = p->counts ? nullptr : p->ladder_var[li];
       const int occ = tv ? g_tonal_pipe_occ[tv - kTonal] : 0;
       if (tv && occ > 0 && !g_tonal_nopipe && N <= g_tonal_pipe_max) {
         t.njobs = cnt;
@@ -1139,6 +1151,9 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, void* ou
                void* stream) {
   if (!p || !img || !out) return fail(FM_EINVAL, "null argument");
   DeviceGuard dg(p->device);
+  if (p->counts)
+    FM_CUDA(cudaMemsetAsync(out, 0, (size_t)p->batch * p->OH * p->OW * (size_t)(p->lr + 1) * sizeof(int32_t),
+                            (cudaStream_t)stream));
   return run_images(p, img, img_defined, out, valid, (cudaStream_t)stream, 0, p->batch);
 }
 
@@ -1204,6 +1219,7 @@ int fm_read_stats(fm_plan* p, fm_stats* st) {
 int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, void* out_host_v,
                     uint8_t* valid_host, void* stream) {
   if (!p || !img_host || !out_host_v) return fail(FM_EINVAL, "null argument");
+  if (p->counts) return fail(FM_EUNSUPPORTED, "count-volume plans run on device buffers (fm_execute)");
   DeviceGuard dg(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   const size_t in_n = (size_t)p->batch * p->H * p->W;
@@ -1261,6 +1277,31 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, v
 }
 
 void fm_plan_destroy(fm_plan* p) { free_plan(p); }
+
+int fm_conv_full_direct(int ndim, const int64_t* a_shape, const int64_t* a, const int64_t* b_shape,
+                        const int64_t* b, int64_t* out, void* stream) {
+  if (ndim < 1 || ndim > 3) return fail(FM_EINVAL, "ndim must be 1..3");
+  if (!a_shape || !b_shape || !a || !b || !out) return fail(FM_EINVAL, "null argument");
+  DirectArgs d{};
+  d.nout = 1;
+  for (int i = 0; i < 3; ++i) {
+    const int j = i - (3 - ndim);
+    d.as[i] = j >= 0 ? a_shape[j] : 1;
+    d.bs[i] = j >= 0 ? b_shape[j] : 1;
+    if (d.as[i] < 1 || d.bs[i] < 1) return fail(FM_EINVAL, "empty array");
+    d.os[i] = d.as[i] + d.bs[i] - 1;
+    d.nout *= d.os[i];
+  }
+  d.a = a;
+  d.b = b;
+  d.out = out;
+  const int64_t blocks = (d.nout + 255) / 256;
+  if (blocks > (1ll << 31) - 1) return fail(FM_EUNSUPPORTED, "output too large");
+  conv_direct_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d);
+  g_launches++;
+  FM_CUDA(cudaGetLastError());
+  return FM_OK;
+}
 
 int fm_naive(const fm_plan_desc* desc, const int32_t* se_values, const uint8_t* se_defined, const void* img,
              const uint8_t* img_defined, int32_t* out, uint8_t* valid, void* stream) {

@@ -39,6 +39,9 @@ struct TonalArgs {
   int out_sign, se_min, fill;
   int stride;             // generic kernel: per-pixel smem stride (float2), odd
   float* dev_max;         // max |c - rint c| (float bits, atomicMax as int)
+  // count-volume mode (generic kernel): counts[pixel][d], d = t + (anchor - count_base)
+  int32_t* counts;
+  int count_len, count_base;
 };
 
 __device__ __forceinline__ void store_out(const TonalArgs& a, size_t i, int v) {
@@ -427,14 +430,21 @@ __global__ void __launch_bounds__(128) tonal_kernel(const TonalArgs a) {
       outb = t;
     }
     int top = -1;
+    int32_t* crow = a.counts ? a.counts + pp.dst * (size_t)a.count_len : nullptr;
+    const int shift = pp.anchor - a.count_base;
     for (int n = 0; n < N; ++n) {
       const float2 z = in[n];
       dev = fmaxf(dev, fabsf(z.x - rintf(z.x)));
       dev = fmaxf(dev, fabsf(z.y - rintf(z.y)));
       if (z.x > 0.5f) top = 2 * n;
       if (z.y > 0.5f) top = 2 * n + 1;
+      if (crow) {
+        const int d0 = 2 * n + shift;
+        if (d0 >= 0 && d0 < a.count_len) crow[d0] = (int32_t)rintf(z.x);
+        if (d0 + 1 >= 0 && d0 + 1 < a.count_len) crow[d0 + 1] = (int32_t)rintf(z.y);
+      }
     }
-    store_out(a, pp.dst, top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill);
+    if (!crow) store_out(a, pp.dst, top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill);
     if (a.valid) a.valid[pp.dst] = top >= 0 ? 1 : 0;
   }
 #pragma unroll

@@ -50,7 +50,8 @@ class MorphPlan:
 
     def __init__(self, *, shape, se_values, se_lo, se_defined=None, mode="dilate",
                  crop=True, img_dtype=torch.uint8, img_min=0, img_max=255, fill=0,
-                 batch=1, device=None, scratch_bytes=0, tile=0, tonal_len=0, out_dtype=torch.int32):
+                 batch=1, device=None, scratch_bytes=0, tile=0, tonal_len=0, out_dtype=torch.int32,
+                 counts=False):
         L = _lib.load()
         shape = tuple(int(s) for s in shape)
         se_values = np.ascontiguousarray(np.asarray(se_values, dtype=np.int64))
@@ -83,6 +84,8 @@ class MorphPlan:
         d.tile = int(tile)
         d.tonal_len = int(tonal_len)
         d.out_dtype = _OUT_CODES[out_dtype]
+        d.flags = _lib.FM_FLAG_COUNTS if counts else 0
+        self.counts = bool(counts)
         self.out_dtype = out_dtype
         self.desc = d
         self.shape = shape
@@ -121,7 +124,10 @@ class MorphPlan:
             defined = defined.to(device=self.device, dtype=torch.uint8).reshape(exp).contiguous()
         oshape = (self.batch, *self.out_shape)
         if out is None:
-            out = torch.empty(oshape, dtype=self.out_dtype, device=self.device)
+            if self.counts:   # count volume [batch, *out_shape, count_len] int32
+                out = torch.empty((*oshape, self.info["count_len"]), dtype=torch.int32, device=self.device)
+            else:
+                out = torch.empty(oshape, dtype=self.out_dtype, device=self.device)
         if valid is None and want_valid:
             valid = torch.empty(oshape, dtype=torch.uint8, device=self.device)
         rc = L.fm_execute(self._h, ctypes.c_void_p(img.data_ptr()),

@@ -35,7 +35,7 @@ def test_header_and_binding_agree():
 def test_library_exports_every_symbol(lib):
     for name in _declared_functions():
         assert hasattr(lib, name), name
-    assert lib.fm_abi_version() == 2
+    assert lib.fm_abi_version() == 3
 
 
 def test_dynamic_symbol_table():
@@ -60,9 +60,10 @@ def test_struct_layouts_match_header(tmp_path):
         #include <stddef.h>
         #include "fftmorph_b200.h"
         int main(void) {
-          printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(fm_plan_desc), sizeof(fm_plan_info), sizeof(fm_stats),
-                 offsetof(fm_plan_desc, img_min), offsetof(fm_plan_desc, scratch_bytes),
-                 offsetof(fm_plan_info, se_count));
+          printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(fm_plan_desc), sizeof(fm_plan_info),
+                 sizeof(fm_stats), offsetof(fm_plan_desc, img_min), offsetof(fm_plan_desc, scratch_bytes),
+                 offsetof(fm_plan_info, se_count), offsetof(fm_plan_desc, flags), offsetof(fm_plan_info, count_len),
+                 sizeof(fm_timing), offsetof(fm_timing, range_launches));
           return 0;
         }
     """))
@@ -70,7 +71,9 @@ def test_struct_layouts_match_header(tmp_path):
     subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     want = [ctypes.sizeof(_lib.PlanDesc), ctypes.sizeof(_lib.PlanInfo), ctypes.sizeof(_lib.Stats),
-            _lib.PlanDesc.img_min.offset, _lib.PlanDesc.scratch_bytes.offset, _lib.PlanInfo.se_count.offset]
+            _lib.PlanDesc.img_min.offset, _lib.PlanDesc.scratch_bytes.offset, _lib.PlanInfo.se_count.offset,
+            _lib.PlanDesc.flags.offset, _lib.PlanInfo.count_len.offset, ctypes.sizeof(_lib.Timing),
+            _lib.Timing.range_launches.offset]
     assert got == want
 
 
