@@ -191,6 +191,7 @@ constexpr int kAuxStreams = 3;
 int g_tonal_pipe_occ[kTonalCount];   // CTAs per SM of each pipelined variant (0: not pipelined)
 int g_num_sms = 148;
 const bool g_tonal_nopipe = std::getenv("FM_TONAL_NOPIPE") != nullptr;  // A/B switch for measurements
+const bool g_no_skip0 = std::getenv("FM_NO_SKIP0") != nullptr;         // A/B: always compute plane 0
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
 const int g_tonal_pipe_max = std::getenv("FM_TONAL_PIPE_MAX") ? std::atoi(std::getenv("FM_TONAL_PIPE_MAX")) : 40;
@@ -892,6 +893,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       S = (int)std::min<int64_t>(std::min(max_s, 32), std::max<int64_t>(1, (4 * 148 + ctas - 1) / ctas));
     }
     r.splits = S;
+    r.skip0 = (p->big || g_no_skip0) ? 0 : 1;
     size_t rsm = 0;
     if (r.ntaps > 0) {
       rsm = p->two_d ? (size_t)((p->QY + S - 1) / S + p->my - 1) * p->win_x * 2
@@ -1103,6 +1105,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       cudaStream_t ts = si == 0 ? s : p->aux[si - 1];
       t.N = N;
       t.T = 2 * N;
+      t.x0_full = (float)((double)p->se_count / (2.0 * N));
       t.list = p->bucket_list + (size_t)li * cap;
       const TonalVariant* tv = p->counts ? nullptr : p->ladder_var[li];
       const int occ = tv ? g_tonal_pipe_occ[tv - kTonal] : 0;

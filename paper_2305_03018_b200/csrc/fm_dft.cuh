@@ -10,6 +10,10 @@
 
 namespace fm {
 
+// work-list entry flag (int2.y of the per-ladder unit lists): the unit is
+// "full" — its plane 0 is a known constant, not computed or stored
+constexpr int kJobFull = 1 << 30;
+
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }

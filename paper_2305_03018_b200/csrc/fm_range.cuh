@@ -29,6 +29,7 @@
 #include <stdint.h>
 #include <cuda_runtime.h>
 #include <type_traits>
+#include "fm_dft.cuh"
 
 namespace fm {
 
@@ -56,6 +57,7 @@ struct RangeArgs {
   int lr_se;              // se_max - se_min
   int cy, cx;             // SE centre, for the seed pixels
   int splits;             // CTAs per unit (output rows, or columns in 1-D, split between them)
+  int skip0;              // the conv path may skip plane 0 of "full" units
   int ntaps;              // 0: no clamp; else a multiple of 8 (padded with kTapPadB taps)
   const int* ladder;      // ascending N values
   int L;
@@ -91,9 +93,22 @@ __device__ __forceinline__ void unit_finish(const RangeArgs& a, int img, int uni
     }
   // anchor in image units: v = f - anchor (dilation) / anchor - f (erosion)
   const int anchor = a.enc_sign * (c - a.enc_bias);
-  a.unit_param[(size_t)img * a.units + unit] = make_int4(anchor, a.ladder[li], li, any ? 1 : 0);
+  // "full": the whole input window lies in the image and has no gaps, so every
+  // valid output pairs with every defined SE entry and plane 0 is a constant
+  bool full = false;
+  if (a.skip0 && a.img_def == nullptr) {
+    if (a.two_d) {
+      const int ty = unit / a.tiles_x, tx = unit - ty * a.tiles_x;
+      const int y0 = ty * a.QY + a.DY, x0 = tx * a.QX + a.DX;
+      full = y0 >= 0 && y0 + a.win_y <= a.H && x0 >= 0 && x0 + a.win_x <= a.W;
+    } else {
+      const int x0 = unit * a.unit_step_x + a.DX;
+      full = x0 >= 0 && x0 + a.win_x <= a.W;
+    }
+  }
+  a.unit_param[(size_t)img * a.units + unit] = make_int4(anchor, a.ladder[li], li, (any ? 1 : 0) | (full ? 2 : 0));
   const int slot = atomicAdd(&a.bucket_count[li], 1);
-  a.bucket_list[(size_t)li * a.cap + slot] = make_int2(img, unit);
+  a.bucket_list[(size_t)li * a.cap + slot] = make_int2(img, unit | (full ? kJobFull : 0));
 }
 
 // grid (units_in_launch * splits, images); split s of a unit handles output

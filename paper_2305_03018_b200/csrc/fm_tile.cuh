@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   int T = a.T, K = a.K, enc_bias = a.enc_bias;
   uint32_t magicT = a.magicT;
   int unit_li = 0;   // ladder entry of a CONV unit
+  bool skip0 = false; // CONV unit whose plane 0 is a known constant (fm_range.cuh "full")
   const float4* spec_base = a.spec;
   int unit = a.unit0 + blockIdx.x;   // absolute unit (tile, or group of 1-D tiles)
   int kchunk_idx = blockIdx.y;        // SPEC: grid y; CONV: from the job list
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
           const int u = rem / fch;
           const int2 job = a.bucket_list[(size_t)found * a.cap + u];
           s_job[0] = job.x;
-          s_job[1] = job.y;
+          s_job[1] = job.y & ~kJobFull;
           s_job[2] = rem - u * fch;   // plane chunk of the unit
         }
       }
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     T = 2 * up.y;
     magicT = (uint32_t)(0x100000000ull / (uint64_t)T);
     unit_li = up.z;
+    skip0 = (up.w & 2) != 0;
     enc_bias = a.enc_sign > 0 ? -up.x : up.x;
     spec_base = a.spec + a.spec_off[up.z];
   }
@@ -311,7 +313,10 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     const float2 w1 = c_tw[TwOff<PX>::v + ((n2 + 1) * k1) % PX];
     *twx_slot(j) = make_float4(w0.x, w0.y, w1.x, w1.y);
   }
-  if (mtab) build_mtab(kchunk_idx * a.k_chunk);
+  {
+    const int k_first = kchunk_idx * a.k_chunk + ((skip0 && kchunk_idx == 0) ? 1 : 0);
+    if (mtab) build_mtab(k_first);
+  }
   __syncthreads();
   const int ty = (TWO_D && !SPEC) ? unit / a.tiles_x : 0;
   const int tx = (TWO_D && !SPEC) ? unit - ty * a.tiles_x : 0;
@@ -330,6 +335,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   };
 
   for (int k = k_begin; k < k_end; ++k) {
+    if (k == 0 && skip0) continue;   // plane 0 of a full unit: the tonal pass knows it
     if constexpr (!SPEC) {
 #pragma unroll
       for (int g = 0; g < C::NBUF; ++g) spec_fetch(k, g);

@@ -42,6 +42,9 @@ struct TonalArgs {
   // count-volume mode (generic kernel): counts[pixel][d], d = t + (anchor - count_base)
   int32_t* counts;
   int count_len, count_base;
+  // units flagged "full" (unit_param.w bit 1: window inside the image, no gaps)
+  // have plane 0 = (defined SE entries) / T everywhere; the conv kernel skips it
+  float x0_full;
 };
 
 __device__ __forceinline__ void store_out(const TonalArgs& a, size_t i, int v) {
@@ -55,12 +58,12 @@ __device__ __forceinline__ void store_out(const TonalArgs& a, size_t i, int v) {
 
 // Pixel p of the work unit list[blockIdx.y]: chat offset, output offset, anchor.
 struct TonalPix {
-  bool live;
+  bool live, full;
   size_t src, dst;
   int anchor;
 };
 __device__ __forceinline__ TonalPix tonal_pixel_job(const TonalArgs& a, int2 job, int p) {
-  const int img = job.x, unit = job.y;
+  const int img = job.x, unit = job.y & ~kJobFull;
   TonalPix r;
   int oy, ox;
   if (a.two_d) {
@@ -76,7 +79,9 @@ __device__ __forceinline__ TonalPix tonal_pixel_job(const TonalArgs& a, int2 job
   r.live = p < a.npx && oy < a.OH && ox < a.OW;
   r.src = ((size_t)img * a.upl + (unit - a.unit0)) * a.K_max * (size_t)a.wpx + p;
   r.dst = ((size_t)img * a.OH + oy) * a.OW + ox;
-  r.anchor = r.live ? a.unit_param[(size_t)img * a.units + unit].x : 0;
+  const int4 up = a.unit_param[(size_t)img * a.units + unit];
+  r.anchor = r.live ? up.x : 0;
+  r.full = (up.w & 2) != 0;
   return r;
 }
 __device__ __forceinline__ TonalPix tonal_pixel(const TonalArgs& a, int p) {
@@ -225,7 +230,7 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
     if constexpr (!SM) {
       float2 X[N + 1];
 #pragma unroll
-      for (int k = 0; k <= N; ++k) X[k] = __ldcs(src + (size_t)k * plane);
+      for (int k = 0; k <= N; ++k) X[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : __ldcs(src + (size_t)k * plane);
       float2 A[N], B[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
@@ -240,7 +245,7 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
       SmemArr<NT> A{tsm_t + threadIdx.x}, B{tsm_t + (size_t)N * NT + threadIdx.x};
       // X[0..N-1] -> B, X[N] stays in a register
 #pragma unroll 8
-      for (int k = 0; k < N; ++k) B[k] = __ldcs(src + (size_t)k * plane);
+      for (int k = 0; k < N; ++k) B[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : __ldcs(src + (size_t)k * plane);
       const float2 xN = __ldcs(src + (size_t)N * plane);
 #pragma unroll 4
       for (int k = 0; k < N; ++k) {
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a) 
   constexpr int NCW = NT / 32;
   extern __shared__ __align__(128) float2 tstg[];   // [ST][K][NT]
   __shared__ __align__(8) uint64_t full[ST], empty[ST];
+  __shared__ int stage_k0[ST];   // 1: the stage's unit has a known plane 0 (not copied)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int bpj = (a.npx + NT - 1) / NT;
   const int items = a.njobs * bpj;
@@ -337,13 +343,15 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a) 
         if (i >= ST) mbar_wait(&empty[st], (uint32_t)(((i / ST) - 1) & 1));
         const int j = item / bpj, blk = item - j * bpj;
         const int2 job = a.list[j];
-        const float2* src = a.chat + ((size_t)job.x * a.upl + (job.y - a.unit0)) * a.K_max * (size_t)a.wpx +
+        const float2* src = a.chat + ((size_t)job.x * a.upl + ((job.y & ~kJobFull) - a.unit0)) * a.K_max * (size_t)a.wpx +
                             (size_t)blk * NT;
         const uint32_t bytes = (uint32_t)min(NT, a.wpx - blk * NT) * 8u;
-        mbar_expect_tx(&full[st], bytes * K);
+        const int k0 = (job.y & kJobFull) ? 1 : 0;   // plane 0 known (not copied)
+        stage_k0[st] = k0;   // published to the consumers by the arrive below
+        mbar_expect_tx(&full[st], bytes * (K - k0));
         float2* dst = tstg + (size_t)st * K * NT;
 #pragma unroll 1
-        for (int k = 0; k < K; ++k) bulk_g2s(dst + k * NT, src + (size_t)k * a.wpx, bytes, &full[st], pol);
+        for (int k = k0; k < K; ++k) bulk_g2s(dst + k * NT, src + (size_t)k * a.wpx, bytes, &full[st], pol);
       }
     }
     return;
@@ -360,7 +368,8 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a) 
     float2 A[N], B[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      const float2 xk = xs[k * NT], xc = conjf2(xs[(N - k) * NT]);
+      const float2 xk = (k == 0 && stage_k0[st]) ? make_float2(a.x0_full, 0.f) : xs[k * NT];
+      const float2 xc = conjf2(xs[(N - k) * NT]);
       A[k] = cadd(cadd(xk, xc), mul_pi(cmul(c_ttw[off + k], csub(xk, xc))));
     }
     __syncwarp();
@@ -402,7 +411,7 @@ __global__ void __launch_bounds__(128) tonal_kernel(const TonalArgs a) {
     const float2* src = a.chat + pp.src;
     float2* A = bufA + (size_t)threadIdx.x * a.stride;
     float2* B = bufB + (size_t)threadIdx.x * a.stride;
-    for (int k = 0; k <= N; ++k) A[k] = __ldcs(src + (size_t)k * plane);
+    for (int k = 0; k <= N; ++k) A[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : __ldcs(src + (size_t)k * plane);
     // c2r packing: Z[k] = (X[k] + X[N-k]^*) + i w_T^{-k}... so that the
     // unnormalised length-N inverse DFT of Z gives z[n] = c(2n) + i c(2n+1).
     for (int k = 0; k < N; ++k) {
