@@ -265,39 +265,64 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
       tx = unit - ty * a.tiles_x;
     }
     int bad = 0;
-    for (int p = tid; p < C::NPTS; p += NT) {
-      const int py = p / PX, px = p - (p / PX) * PX;
-      uint16_t t = sent;
-      if (SPEC) {
+    if constexpr (SPEC) {
+      for (int p = tid; p < C::NPTS; p += NT) {
+        const int py = p / PX, px = p - (p / PX) * PX;
+        uint16_t t = sent;
         const int sy = TWO_D ? py : 0;
         if (sy < a.my && px < a.mx) {
           const int si = sy * a.mx + px;
           if (a.se_def == nullptr || a.se_def[si]) t = (uint16_t)(a.se_vals[si] + a.enc_bias);
         }
-      } else {
-        int iy, ix;
-        bool rowok;
-        if (TWO_D) {
-          iy = ty * a.QY + a.DY + py;
-          ix = tx * a.QX + a.DX + px;
-          rowok = true;
-        } else {
-          const int tile = unit * PY + py;
-          iy = 0;
-          ix = tile * a.QX + a.DX + px;
-          rowok = tile < a.tiles_total;
+        tv[p] = t;
+      }
+    } else {
+      // batches of GB independent (predicated) loads per thread, then the
+      // conversions: the image reads overlap instead of paying one global
+      // latency per pixel
+      constexpr int IT = C::NPTS / NT;
+      static_assert(IT * NT == C::NPTS, "staging split");
+      constexpr int GB = IT < 16 ? IT : 16;
+#pragma unroll 1
+      for (int g0 = 0; g0 < IT; g0 += GB) {
+        int raw[GB];
+        bool ok[GB];
+#pragma unroll
+        for (int u = 0; u < GB; ++u) {
+          const int p = tid + (g0 + u) * NT;
+          const int py = p / PX, px = p - (p / PX) * PX;
+          int iy, ix;
+          bool rowok;
+          if (TWO_D) {
+            iy = ty * a.QY + a.DY + py;
+            ix = tx * a.QX + a.DX + px;
+            rowok = true;
+          } else {
+            const int tile = unit * PY + py;
+            iy = 0;
+            ix = tile * a.QX + a.DX + px;
+            rowok = tile < a.tiles_total;
+          }
+          ok[u] = rowok && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+          raw[u] = 0;
+          if (ok[u]) {
+            const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
+            raw[u] = load_img(a.img, a.img_dtype, gi);
+            if (a.img_def != nullptr) ok[u] = a.img_def[gi] != 0;
+          }
         }
-        if (rowok && iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
-          const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
-          if (a.img_def == nullptr || a.img_def[gi]) {
+#pragma unroll
+        for (int u = 0; u < GB; ++u) {
+          uint16_t t = sent;
+          if (ok[u]) {
             // values below the unit's clamp level encode as the clamp (fm_range.cuh)
-            const int v = max(a.enc_sign * load_img(a.img, a.img_dtype, gi) + enc_bias, 0);
+            const int v = max(a.enc_sign * raw[u] + enc_bias, 0);
             if (v >= T) bad = 1;
             else t = (uint16_t)v;
           }
+          tv[tid + (g0 + u) * NT] = t;
         }
       }
-      tv[p] = t;
     }
     if (!SPEC && bad) atomicOr(a.err, 1);
   }
