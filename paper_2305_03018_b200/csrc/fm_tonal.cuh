@@ -280,11 +280,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps until the phase
+// completes (or the hint expires) instead of spinning on issue slots
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAIT_%=;\n}" ::"r"(
           smem_addr(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)
       : "memory");
 }
 __device__ __forceinline__ uint64_t evict_first_policy() {
@@ -301,9 +303,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <int N>
-constexpr int tonal_pipe_nt() { return (N + 1) * 128 * 8 * 3 > 96 * 1024 ? 64 : 128; }
+constexpr int tonal_pipe_nt() { return (N + 1) * 128 * 8 * 2 > 96 * 1024 ? 64 : 128; }
 template <int N>
-constexpr int tonal_pipe_st() { return (N + 1) * tonal_pipe_nt<N>() * 8 * 3 > 96 * 1024 ? 2 : 3; }
+constexpr int tonal_pipe_st() { return 2; }   // two stages: more CTAs per SM beat a deeper ring (measured)
 template <int N>
 constexpr int tonal_pipe_smem() { return (N + 1) * tonal_pipe_nt<N>() * 8 * tonal_pipe_st<N>(); }
 
@@ -338,11 +340,16 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a) 
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
       int i = 0;
+      // the next item's work-list entry is loaded one iteration ahead, so its
+      // latency overlaps the wait for a free stage
+      int2 job_next = blockIdx.x < items ? a.list[blockIdx.x / bpj] : make_int2(0, 0);
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++i) {
         const int st = i % ST;
+        const int2 job = job_next;
+        const int item_next = item + gridDim.x;
+        if (item_next < items) job_next = a.list[item_next / bpj];
         if (i >= ST) mbar_wait(&empty[st], (uint32_t)(((i / ST) - 1) & 1));
         const int j = item / bpj, blk = item - j * bpj;
-        const int2 job = a.list[j];
         const float2* src = a.chat + ((size_t)job.x * a.upl + ((job.y & ~kJobFull) - a.unit0)) * a.K_max * (size_t)a.wpx +
                             (size_t)blk * NT;
         const uint32_t bytes = (uint32_t)min(NT, a.wpx - blk * NT) * 8u;
