@@ -192,6 +192,7 @@ int g_tonal_pipe_occ[kTonalCount];   // CTAs per SM of each pipelined variant (0
 int g_num_sms = 148;
 const bool g_tonal_nopipe = std::getenv("FM_TONAL_NOPIPE") != nullptr;  // A/B switch for measurements
 const bool g_no_skip0 = std::getenv("FM_NO_SKIP0") != nullptr;         // A/B: always compute plane 0
+const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
 const int g_tonal_pipe_max = std::getenv("FM_TONAL_PIPE_MAX") ? std::atoi(std::getenv("FM_TONAL_PIPE_MAX")) : 40;
@@ -894,6 +895,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     }
     r.splits = S;
     r.skip0 = (p->big || g_no_skip0) ? 0 : 1;
+    r.warp_sync = g_range_sync;
     size_t rsm = 0;
     if (r.ntaps > 0) {
       rsm = p->two_d ? (size_t)((p->QY + S - 1) / S + p->my - 1) * p->win_x * 2

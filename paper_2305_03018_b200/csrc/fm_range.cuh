@@ -58,6 +58,7 @@ struct RangeArgs {
   int cy, cx;             // SE centre, for the seed pixels
   int splits;             // CTAs per unit (output rows, or columns in 1-D, split between them)
   int skip0;              // the conv path may skip plane 0 of "full" units
+  int warp_sync;          // bound taps walked warp-synchronously (else per-lane pixel queues)
   int ntaps;              // 0: no clamp; else a multiple of 8 (padded with kTapPadB taps)
   const int* ladder;      // ascending N values
   int L;
@@ -314,35 +315,78 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
     // A pixel may stop as soon as g reaches the breakpoint level below the
     // running minimum: only the interval between ladder breakpoints that D
     // falls into changes the unit's tonal length.
-    int q = tid;
-    if (q < npx) {
-      int base = base_of(q), t = 0, g = INT32_MIN, seen = INT32_MIN, lvl = INT32_MIN;
-      while (true) {
-        const int bnd = *vb;
-        if (bnd != seen) {
-          seen = bnd;
-          lvl = level_of(bnd);
+    if (a.warp_sync) {
+      // warps take 32 consecutive pixels and walk the taps together (same tap,
+      // neighbouring pixels: conflict-free shared-memory reads); finished lanes idle
+      for (int qb = warp * 32; qb < npx; qb += kRangeNT) {
+        const int q = qb + lane;
+        const bool act = q < npx;
+        const int base = act ? base_of(q) : 0;
+        int g = INT32_MIN, t = 0, seen = INT32_MIN, lvl = INT32_MIN;
+        bool done = !act, stop_all = false;
+        while (true) {
+          const int bnd = __shfl_sync(0xffffffffu, *vb, 0);
+          if (bnd != seen) {
+            seen = bnd;
+            lvl = level_of(bnd);
+          }
+          if (lvl <= floor_d) {
+            stop_all = true;
+            break;
+          }
+          if (!done && g >= lvl) done = true;
+          if (!done && t >= a.ntaps) {
+            if (g < bnd) atomicMin(&s_bound, g);
+            done = true;
+          }
+          if (__all_sync(0xffffffffu, done)) break;
+          if (!done) {
+            const int4 o0 = *reinterpret_cast<const int4*>(s_toff + t), o1 = *reinterpret_cast<const int4*>(s_toff + t + 4);
+            const int4 b0 = *reinterpret_cast<const int4*>(s_tb + t), b1 = *reinterpret_cast<const int4*>(s_tb + t + 4);
+            g = max(g, (int)swin[base + o0.x] + b0.x);
+            g = max(g, (int)swin[base + o0.y] + b0.y);
+            g = max(g, (int)swin[base + o0.z] + b0.z);
+            g = max(g, (int)swin[base + o0.w] + b0.w);
+            g = max(g, (int)swin[base + o1.x] + b1.x);
+            g = max(g, (int)swin[base + o1.y] + b1.y);
+            g = max(g, (int)swin[base + o1.z] + b1.z);
+            g = max(g, (int)swin[base + o1.w] + b1.w);
+          }
+          t += 8;
         }
-        if (lvl <= floor_d) break;  // no clamp possible: stop
-        if (t >= a.ntaps || g >= lvl) {
-          if (t >= a.ntaps && g < bnd) atomicMin(&s_bound, g);
-          q += kRangeNT;
-          if (q >= npx) break;
-          base = base_of(q);
-          t = 0;
-          g = INT32_MIN;
+        if (stop_all) break;
+      }
+    } else {
+      int q = tid;
+      if (q < npx) {
+        int base = base_of(q), t = 0, g = INT32_MIN, seen = INT32_MIN, lvl = INT32_MIN;
+        while (true) {
+          const int bnd = *vb;
+          if (bnd != seen) {
+            seen = bnd;
+            lvl = level_of(bnd);
+          }
+          if (lvl <= floor_d) break;  // no clamp possible: stop
+          if (t >= a.ntaps || g >= lvl) {
+            if (t >= a.ntaps && g < bnd) atomicMin(&s_bound, g);
+            q += kRangeNT;
+            if (q >= npx) break;
+            base = base_of(q);
+            t = 0;
+            g = INT32_MIN;
+          }
+          const int4 o0 = *reinterpret_cast<const int4*>(s_toff + t), o1 = *reinterpret_cast<const int4*>(s_toff + t + 4);
+          const int4 b0 = *reinterpret_cast<const int4*>(s_tb + t), b1 = *reinterpret_cast<const int4*>(s_tb + t + 4);
+          g = max(g, (int)swin[base + o0.x] + b0.x);
+          g = max(g, (int)swin[base + o0.y] + b0.y);
+          g = max(g, (int)swin[base + o0.z] + b0.z);
+          g = max(g, (int)swin[base + o0.w] + b0.w);
+          g = max(g, (int)swin[base + o1.x] + b1.x);
+          g = max(g, (int)swin[base + o1.y] + b1.y);
+          g = max(g, (int)swin[base + o1.z] + b1.z);
+          g = max(g, (int)swin[base + o1.w] + b1.w);
+          t += 8;
         }
-        const int4 o0 = *reinterpret_cast<const int4*>(s_toff + t), o1 = *reinterpret_cast<const int4*>(s_toff + t + 4);
-        const int4 b0 = *reinterpret_cast<const int4*>(s_tb + t), b1 = *reinterpret_cast<const int4*>(s_tb + t + 4);
-        g = max(g, (int)swin[base + o0.x] + b0.x);
-        g = max(g, (int)swin[base + o0.y] + b0.y);
-        g = max(g, (int)swin[base + o0.z] + b0.z);
-        g = max(g, (int)swin[base + o0.w] + b0.w);
-        g = max(g, (int)swin[base + o1.x] + b1.x);
-        g = max(g, (int)swin[base + o1.y] + b1.y);
-        g = max(g, (int)swin[base + o1.z] + b1.z);
-        g = max(g, (int)swin[base + o1.w] + b1.w);
-        t += 8;
       }
     }
     __syncthreads();
