@@ -284,6 +284,7 @@ struct fm_plan {
   std::vector<const TonalVariant*> ladder_var;
   int units = 1, wpx = 1, npx = 1, win_y = 1, win_x = 1, unit_step_x = 0;  // wpx: even plane stride
   std::vector<int2> taps;                 // clamp-bound taps of fm_range.cuh, best first
+  std::vector<int> full_prefix;           // prefix count of "full" units (window inside the image)
   int* range_part = nullptr;              // [ipc*units][8] split partials of fm_range.cuh
   bool counts = false;                    // FM_FLAG_COUNTS: count-volume output
   float2* enc_tab = nullptr;              // per ladder entry: exp(-2 pi i j / T), j < T, then 0
@@ -607,6 +608,20 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   }
 
   p->wpx = (p->npx + 1) & ~1;  // even plane stride: 16-byte aligned bulk copies of pixel blocks
+  // units whose input window lies inside the image (the "full" test of fm_range.cuh)
+  p->full_prefix.assign(p->units + 1, 0);
+  for (int u = 0; u < p->units; ++u) {
+    bool full;
+    if (p->two_d) {
+      const int ty = u / p->tiles_x, tx = u - ty * p->tiles_x;
+      const int64_t y0 = (int64_t)ty * p->QY + p->DY, x0 = (int64_t)tx * p->QX + p->DX;
+      full = y0 >= 0 && y0 + p->win_y <= p->H && x0 >= 0 && x0 + p->win_x <= p->W;
+    } else {
+      const int64_t x0 = (int64_t)u * p->unit_step_x + p->DX;
+      full = x0 >= 0 && x0 + p->win_x <= p->W;
+    }
+    p->full_prefix[u + 1] = p->full_prefix[u] + (full ? 1 : 0);
+  }
 
   // clamp-bound taps (fm_range.cuh): the highest SE entries, ties spread over
   // the SE by a multiplicative hash; offsets index the staged input window;
@@ -1137,6 +1152,12 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     for (int i = 0; i < nstreams - 1; ++i) {
       FM_CUDA(cudaEventRecord(p->ev_join[i], p->aux[i]));
       FM_CUDA(cudaStreamWaitEvent(s, p->ev_join[i], 0));
+    }
+    // full units (fm_range.cuh) skip plane 0: fewer planes computed, stored and read
+    if (!p->big && !g_no_skip0 && img_defined == nullptr) {
+      const double skipped = (double)n * (double)(p->full_prefix[u0 + nu] - p->full_prefix[u0]);
+      planes -= skipped;
+      tonal_b -= skipped * (double)p->npx * 8.0;
     }
     p->planes_done += (int64_t)planes;
     p->units_done += (int64_t)n * nu;
