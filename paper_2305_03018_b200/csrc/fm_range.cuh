@@ -307,9 +307,10 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
     const int rows = jy_end - oy0, cols = jx_end - jx_beg;
     const int npx = rows * cols;
     const int xoff = a.two_d ? 0 : jx_beg - wx0;
-    const float inv_cols = 1.0f / (float)cols;
+    // q -> (jy, jx) with a high multiply by ceil(2^32/cols): exact for q < 2^16
+    const uint32_t cmagic = cols > 1 ? (uint32_t)((0x100000000ull + cols - 1) / (uint64_t)cols) : 0u;
     auto base_of = [&](int q) {
-      const int jy = (int)(((float)q + 0.5f) * inv_cols);  // exact for q < 2^22
+      const int jy = cmagic ? (int)__umulhi((uint32_t)q, cmagic) : q;
       return jy * wx + (q - jy * cols) + xoff;
     };
     // A pixel may stop as soon as g reaches the breakpoint level below the
