@@ -254,9 +254,8 @@ struct fm_plan {
   int64_t ipc = 1;  // images per launch
   size_t conv_smem = 0, tonal_smem = 0;
   int tonal_threads = 128, tonal_stride = 1;
-  const TonalVariant* tonal_var = nullptr;
   int enc_sign = 1, enc_bias = 0, vmax = 0;
-  int out_sign = 1, out_bias = 0;
+  int out_sign = 1;
   // device buffers
   float4* spec = nullptr;
   float2* twN = nullptr;
@@ -464,12 +463,10 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     p->enc_sign = 1;
     p->enc_bias = -d.img_min;
     p->out_sign = 1;
-    p->out_bias = d.img_min + smin;
   } else {
     p->enc_sign = -1;
     p->enc_bias = d.img_max;
     p->out_sign = -1;
-    p->out_bias = d.img_max - smin;
   }
   p->vmax = d.img_max - d.img_min;
   {
@@ -803,8 +800,6 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     a.k_chunk = 1;
     a.enc_sign = 1;
     a.enc_bias = -smin;
-    a.vmax = 1 << 30;
-    a.two_pi_over_T = (float)(2.0 * kPi / Tl);
     a.spec = p->spec + p->spec_off[li];
     a.spec_out = p->spec + p->spec_off[li];
     a.spec_scale = (float)(1.0 / ((double)(p->two_d ? p->PY : 1) * p->PX * Tl));
@@ -969,8 +964,6 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     a.k_chunk = p->k_chunk;
     a.enc_sign = p->enc_sign;
     a.enc_bias = p->enc_bias;
-    a.vmax = p->vmax;
-    a.two_pi_over_T = (float)(2.0 * kPi / p->T);
     a.spec = p->spec;
     a.chat = p->chat;
     a.err = p->stats + 1;

@@ -71,8 +71,6 @@ struct TileArgs {
   uint32_t magicT;            // floor(2^32 / T)
   int k_chunk;
   int enc_sign, enc_bias;     // v = enc_sign * f + enc_bias (CONV) / v = b - se_min (SPEC)
-  int vmax;                   // largest legal v
-  float two_pi_over_T;        // 2 pi / T
   const float4* spec;         // [K][thread order] SE spectrum, pairs (CONV reads)
   float4* spec_out;           // SPEC writes
   float spec_scale;           // SPEC: 1 / (PY_eff * PX * T)
