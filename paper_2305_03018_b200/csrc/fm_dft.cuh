@@ -14,23 +14,23 @@ namespace fm {
 // "full" — its plane 0 is a known constant, not computed or stored
 constexpr int kJobFull = 1 << 30;
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 // a * b
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+__host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
 // a * conj(b)
-__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+__host__ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
-__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }  // a * (-i)
-__device__ __forceinline__ float2 mul_pi(float2 a) { return make_float2(-a.y, a.x); }  // a * (+i)
-__device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+__host__ __device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }  // a * (-i)
+__host__ __device__ __forceinline__ float2 mul_pi(float2 a) { return make_float2(-a.y, a.x); }  // a * (+i)
+__host__ __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
 
 // cos(2*pi*j/16); j is a compile-time constant after unrolling so the switch folds.
-__device__ __forceinline__ float cos16(int j) {
+__host__ __device__ __forceinline__ float cos16(int j) {
   switch (j & 15) {
     case 0: return 1.0f;
     case 1: return 0.923879532511286756f;
@@ -50,11 +50,11 @@ __device__ __forceinline__ float cos16(int j) {
     default: return 0.923879532511286756f;
   }
 }
-__device__ __forceinline__ float sin16(int j) { return cos16(j - 4); }
+__host__ __device__ __forceinline__ float sin16(int j) { return cos16(j - 4); }
 
 // v * W_R^e (forward) or v * conj(W_R^e) (inverse), for R | 16, e compile-time.
 template <int R, bool INV>
-__device__ __forceinline__ float2 twc(float2 v, int e) {
+__host__ __device__ __forceinline__ float2 twc(float2 v, int e) {
   const int j = (e * (16 / R)) & 15;
   if (j == 0) return v;
   if (j == 4) return INV ? mul_pi(v) : mul_mi(v);
@@ -66,17 +66,17 @@ __device__ __forceinline__ float2 twc(float2 v, int e) {
 }
 
 template <int R, bool INV>
-__device__ __forceinline__ void dft(float2 (&x)[R]);
+__host__ __device__ __forceinline__ void dft(float2 (&x)[R]);
 
 template <bool INV>
-__device__ __forceinline__ void dft2_(float2 (&x)[2]) {
+__host__ __device__ __forceinline__ void dft2_(float2 (&x)[2]) {
   const float2 a = x[0], b = x[1];
   x[0] = cadd(a, b);
   x[1] = csub(a, b);
 }
 
 template <bool INV>
-__device__ __forceinline__ void dft4_(float2 (&x)[4]) {
+__host__ __device__ __forceinline__ void dft4_(float2 (&x)[4]) {
   const float2 t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]);
   const float2 t2 = cadd(x[1], x[3]), t3 = csub(x[1], x[3]);
   const float2 r = INV ? mul_pi(t3) : mul_mi(t3);
@@ -89,7 +89,7 @@ __device__ __forceinline__ void dft4_(float2 (&x)[4]) {
 // R = A*B four-step in registers, natural input and output order:
 // X[k1 + A*k2] = sum_{n2<B} W_B^{n2 k2} W_R^{n2 k1} sum_{n1<A} x[n2 + B*n1] W_A^{n1 k1}
 template <int A, int B, bool INV>
-__device__ __forceinline__ void dft_ab(float2 (&x)[A * B]) {
+__host__ __device__ __forceinline__ void dft_ab(float2 (&x)[A * B]) {
   constexpr int R = A * B;
   float2 t[R];
 #pragma unroll
@@ -113,7 +113,7 @@ __device__ __forceinline__ void dft_ab(float2 (&x)[A * B]) {
 }
 
 template <bool INV>
-__device__ __forceinline__ void dft3_(float2 (&x)[3]) {
+__host__ __device__ __forceinline__ void dft3_(float2 (&x)[3]) {
   const float s3 = 0.866025403784438647f;  // sin(2*pi/3)
   const float2 t1 = cadd(x[1], x[2]);
   const float2 t2 = make_float2(fmaf(-0.5f, t1.x, x[0].x), fmaf(-0.5f, t1.y, x[0].y));
@@ -126,7 +126,7 @@ __device__ __forceinline__ void dft3_(float2 (&x)[3]) {
 }
 
 template <bool INV>
-__device__ __forceinline__ void dft5_(float2 (&x)[5]) {
+__host__ __device__ __forceinline__ void dft5_(float2 (&x)[5]) {
   const float c1 = 0.309016994374947424f;   // cos(2pi/5)
   const float c2 = -0.809016994374947424f;  // cos(4pi/5)
   const float s1 = 0.951056516295153572f;   // sin(2pi/5)
@@ -147,8 +147,113 @@ __device__ __forceinline__ void dft5_(float2 (&x)[5]) {
   x[3] = csub(a2, r2);
 }
 
+// ---------------------------------------------------------------------------
+// FMA-shaped radix-8 / radix-16 codelets.  Four-step (A x 4) in registers like
+// dft_ab, but the second-stage twiddles are folded into the radix-4
+// butterflies: a W8-type twiddle h(1 -/+ i) becomes two adds whose scale h
+// rides in the butterfly FMAs, and a general twiddle c(1 -/+ i tan) becomes two
+// FMAs with the cosine again carried by the butterfly FMAs
+// (DFT16: 144 instead of 160 FP instructions, DFT8: 52 instead of 56).
+// sigma = -1 forward (W = exp(-2 pi i/16)), +1 inverse.
+
+// Radix-4 stage over b_n = W^{n e} a_n for the W8-type row (e = 2 in units of
+// W16): outputs X_{k2} = sum_n W4^{n k2} b_n, k2 = 0..3.
+template <bool INV>
+__host__ __device__ __forceinline__ void bfly4_w8(float2 a0, float2 a1, float2 a2, float2 a3, float2& X0, float2& X1,
+                                                  float2& X2, float2& X3) {
+  constexpr float h = 0.707106781186547524f;
+  constexpr float sg = INV ? 1.0f : -1.0f;
+  // b2 = sigma*i*a2: S = a0 + b2, D = a0 - b2
+  const float2 S = make_float2(a0.x - sg * a2.y, a0.y + sg * a2.x);
+  const float2 D = make_float2(a0.x + sg * a2.y, a0.y - sg * a2.x);
+  // b1 + b3 = h P', b1 - b3 = h Q'  (b1 = W^2 a1, b3 = W^6 a3)
+  const float2 d = csub(a1, a3), e = cadd(a1, a3);
+  const float2 P = make_float2(d.x - sg * e.y, d.y + sg * e.x);
+  const float2 Q = make_float2(e.x - sg * d.y, e.y + sg * d.x);
+  X0 = make_float2(fmaf(h, P.x, S.x), fmaf(h, P.y, S.y));
+  X2 = make_float2(fmaf(-h, P.x, S.x), fmaf(-h, P.y, S.y));
+  X1 = make_float2(fmaf(-sg * h, Q.y, D.x), fmaf(sg * h, Q.x, D.y));
+  X3 = make_float2(fmaf(sg * h, Q.y, D.x), fmaf(-sg * h, Q.x, D.y));
+}
+
+template <bool INV>
+__host__ __device__ __forceinline__ void dft8_(float2 (&x)[8]) {
+  float2 a[4][2];
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) {
+    a[n2][0] = cadd(x[n2], x[n2 + 4]);
+    a[n2][1] = csub(x[n2], x[n2 + 4]);
+  }
+  float2 b[4] = {a[0][0], a[1][0], a[2][0], a[3][0]};
+  dft4_<INV>(b);
+  x[0] = b[0];
+  x[2] = b[1];
+  x[4] = b[2];
+  x[6] = b[3];
+  bfly4_w8<INV>(a[0][1], a[1][1], a[2][1], a[3][1], x[1], x[3], x[5], x[7]);
+}
+
+template <bool INV>
+__host__ __device__ __forceinline__ void dft16_(float2 (&x)[16]) {
+  constexpr float h = 0.707106781186547524f;
+  constexpr float c1 = 0.923879532511286756f;  // cos(pi/8)
+  constexpr float t1 = 0.414213562373095049f;  // tan(pi/8)
+  constexpr float sg = INV ? 1.0f : -1.0f;
+  float2 a[4][4];
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) {
+    float2 v[4] = {x[n2], x[n2 + 4], x[n2 + 8], x[n2 + 12]};
+    dft4_<INV>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) a[n2][k1] = v[k1];
+  }
+  // k1 = 0: plain radix-4
+  {
+    float2 b[4] = {a[0][0], a[1][0], a[2][0], a[3][0]};
+    dft4_<INV>(b);
+    x[0] = b[0];
+    x[4] = b[1];
+    x[8] = b[2];
+    x[12] = b[3];
+  }
+  // k1 = 2: twiddles W^0, W^2, W^4, W^6
+  bfly4_w8<INV>(a[0][2], a[1][2], a[2][2], a[3][2], x[2], x[6], x[10], x[14]);
+  // k1 = 1: twiddles W^0, W^1, W^2, W^3
+  {
+    const float2 a0 = a[0][1], a1 = a[1][1], a2 = a[2][1], a3 = a[3][1];
+    // b2 = W^2 a2 = h (a2.x - s a2.y, a2.y + s a2.x)
+    const float2 A2 = make_float2(a2.x - sg * a2.y, a2.y + sg * a2.x);
+    const float2 S = make_float2(fmaf(h, A2.x, a0.x), fmaf(h, A2.y, a0.y));
+    const float2 D = make_float2(fmaf(-h, A2.x, a0.x), fmaf(-h, A2.y, a0.y));
+    // b1 = W^1 a1 = c1 u, b3 = W^3 a3 = c1 v
+    const float2 u = make_float2(fmaf(-sg * t1, a1.y, a1.x), fmaf(sg * t1, a1.x, a1.y));
+    const float2 v = make_float2(fmaf(t1, a3.x, -sg * a3.y), fmaf(t1, a3.y, sg * a3.x));
+    const float2 p = cadd(u, v), q = csub(u, v);
+    x[1] = make_float2(fmaf(c1, p.x, S.x), fmaf(c1, p.y, S.y));
+    x[9] = make_float2(fmaf(-c1, p.x, S.x), fmaf(-c1, p.y, S.y));
+    x[5] = make_float2(fmaf(-sg * c1, q.y, D.x), fmaf(sg * c1, q.x, D.y));
+    x[13] = make_float2(fmaf(sg * c1, q.y, D.x), fmaf(-sg * c1, q.x, D.y));
+  }
+  // k1 = 3: twiddles W^0, W^3, W^6, W^9 (= -W^1)
+  {
+    const float2 a0 = a[0][3], a1 = a[1][3], a2 = a[2][3], a3 = a[3][3];
+    // b2 = W^6 a2 = h (-a2.x - s a2.y, -a2.y + s a2.x)
+    const float2 A2 = make_float2(-a2.x - sg * a2.y, -a2.y + sg * a2.x);
+    const float2 S = make_float2(fmaf(h, A2.x, a0.x), fmaf(h, A2.y, a0.y));
+    const float2 D = make_float2(fmaf(-h, A2.x, a0.x), fmaf(-h, A2.y, a0.y));
+    // b1 = W^3 a1 = c1 v1, b3 = W^9 a3 = -c1 u3
+    const float2 v1 = make_float2(fmaf(t1, a1.x, -sg * a1.y), fmaf(t1, a1.y, sg * a1.x));
+    const float2 u3 = make_float2(fmaf(-sg * t1, a3.y, a3.x), fmaf(sg * t1, a3.x, a3.y));
+    const float2 p = csub(v1, u3), q = cadd(v1, u3);
+    x[3] = make_float2(fmaf(c1, p.x, S.x), fmaf(c1, p.y, S.y));
+    x[11] = make_float2(fmaf(-c1, p.x, S.x), fmaf(-c1, p.y, S.y));
+    x[7] = make_float2(fmaf(-sg * c1, q.y, D.x), fmaf(sg * c1, q.x, D.y));
+    x[15] = make_float2(fmaf(sg * c1, q.y, D.x), fmaf(-sg * c1, q.x, D.y));
+  }
+}
+
 template <int R, bool INV>
-__device__ __forceinline__ void dft(float2 (&x)[R]) {
+__host__ __device__ __forceinline__ void dft(float2 (&x)[R]) {
   if constexpr (R == 1) {
   } else if constexpr (R == 2) {
     dft2_<INV>(x);
@@ -159,9 +264,9 @@ __device__ __forceinline__ void dft(float2 (&x)[R]) {
   } else if constexpr (R == 5) {
     dft5_<INV>(x);
   } else if constexpr (R == 8) {
-    dft_ab<2, 4, INV>(x);
+    dft8_<INV>(x);
   } else if constexpr (R == 16) {
-    dft_ab<4, 4, INV>(x);
+    dft16_<INV>(x);
   } else {
     static_assert(R == 1, "unsupported radix");
   }

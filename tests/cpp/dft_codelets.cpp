@@ -1,0 +1,26 @@
+// Host-side check of the register DFT codelets of fm_dft.cuh (compiled by
+// tests/test_dft_codelets.py with g++): every radix against an FP64 DFT.
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cmath>
+#include <complex>
+#include "fm_dft.cuh"
+using namespace fm;
+template <int R, bool INV> double check() {
+  double worst = 0;
+  for (int trial = 0; trial < 50; ++trial) {
+    float2 x[R]; std::complex<double> xd[R];
+    for (int i = 0; i < R; ++i) { float re = std::sin(1.3*i + trial), im = std::cos(0.7*i*i + 2*trial); x[i] = make_float2(re, im); xd[i] = {re, im}; }
+    dft<R, INV>(x);
+    for (int k = 0; k < R; ++k) {
+      std::complex<double> acc = 0;
+      for (int n = 0; n < R; ++n) acc += xd[n] * std::polar(1.0, (INV ? 2 : -2) * M_PI * n * k / R);
+      worst = std::max(worst, std::abs(acc - std::complex<double>(x[k].x, x[k].y)));
+    }
+  }
+  return worst;
+}
+int main() {
+  printf("%g %g %g %g %g %g %g %g %g %g\n", check<2, false>(), check<3, false>(), check<4, false>(), check<5, false>(),
+         check<8, false>(), check<16, false>(), check<3, true>(), check<5, true>(), check<8, true>(), check<16, true>());
+}

@@ -1,0 +1,21 @@
+"""CPU: the register DFT codelets (fm_dft.cuh, host-compilable) against an FP64 DFT."""
+
+import shutil
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_codelets_match_fp64_dft(tmp_path):
+    if shutil.which("g++") is None:
+        pytest.skip("g++ unavailable")
+    exe = tmp_path / "dft"
+    cuda_inc = "/usr/local/cuda/include"
+    subprocess.run(["g++", "-std=c++17", "-O1", f"-I{cuda_inc}", f"-I{ROOT / 'paper_2305_03018_b200' / 'csrc'}",
+                    str(ROOT / "tests" / "cpp" / "dft_codelets.cpp"), "-o", str(exe)], check=True)
+    errs = [float(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert len(errs) == 10
+    assert max(errs) < 2e-6, errs
