@@ -1268,17 +1268,39 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, v
   FM_CUDA(cudaEventRecord(p->ev_in, s));          // order after prior work on s
   FM_CUDA(cudaStreamWaitEvent(hs, p->ev_in, 0));
   FM_CUDA(cudaStreamWaitEvent(ds, p->ev_in, 0));
-  int64_t ci = 0;
-  for (int64_t c0 = 0; c0 < p->batch; c0 += p->ipc, ++ci) {
-    const int64_t n = std::min<int64_t>(p->ipc, p->batch - c0);
+  // chunk plan: a one-image chunk first and last, so the pipeline fills after
+  // one image's upload and drains after one image's download
+  std::vector<std::pair<int64_t, int64_t>> chunks;   // (first image, images)
+  {
+    int64_t c0 = 0, left = p->batch;
+    if (left > 2 && p->ipc > 1) {
+      chunks.push_back({0, 1});
+      c0 = 1;
+      left -= 1;
+    }
+    while (left > 0) {
+      int64_t n = std::min<int64_t>(p->ipc, left);
+      if (n == left && n > 1 && p->ipc > 1 && p->batch > 2) n -= 1;   // keep the last image on its own
+      chunks.push_back({c0, n});
+      c0 += n;
+      left -= n;
+    }
+  }
+  if (p->ev_chunks.size() < 2 * chunks.size()) {
+    const size_t old = p->ev_chunks.size();
+    p->ev_chunks.resize(2 * chunks.size());
+    for (size_t i = old; i < p->ev_chunks.size(); ++i)
+      FM_CUDA(cudaEventCreateWithFlags(&p->ev_chunks[i], cudaEventDisableTiming));
+  }
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+    const int64_t c0 = chunks[ci].first, n = chunks[ci].second;
     FM_CUDA(cudaMemcpyAsync(din + c0 * img_e * dsz, hin + c0 * img_e * dsz, n * img_e * dsz, cudaMemcpyHostToDevice, hs));
     if (def_host)
       FM_CUDA(cudaMemcpyAsync(p->h_def + c0 * img_e, def_host + c0 * img_e, n * img_e, cudaMemcpyHostToDevice, hs));
     FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci], hs));
   }
-  ci = 0;
-  for (int64_t c0 = 0; c0 < p->batch; c0 += p->ipc, ++ci) {
-    const int64_t n = std::min<int64_t>(p->ipc, p->batch - c0);
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+    const int64_t c0 = chunks[ci].first, n = chunks[ci].second;
     FM_CUDA(cudaStreamWaitEvent(s, p->ev_chunks[2 * ci], 0));
     int rc = run_images(p, p->h_img, def_host ? p->h_def : nullptr, p->h_out, valid_host ? p->h_valid : nullptr, s,
                         c0, c0 + n);

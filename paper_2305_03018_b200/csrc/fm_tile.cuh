@@ -344,7 +344,12 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   const int ty = (TWO_D && !SPEC) ? unit / a.tiles_x : 0;
   const int tx = (TWO_D && !SPEC) ? unit - ty * a.tiles_x : 0;
   const int k_begin = kchunk_idx * a.k_chunk;
-  const int k_end = min(K, k_begin + a.k_chunk);
+  // the plane loop bound lives in shared memory: under the kernel's register
+  // pressure a register copy gets spilled and reloaded from local memory
+  __shared__ int s_kend;
+  if (tid == 0) s_kend = min(K, k_begin + a.k_chunk);
+  __syncthreads();
+  const volatile int* kend_s = &s_kend;
   // window-local output planes of this unit (slot = launch-local unit index)
   float2* chat_unit = SPEC ? nullptr : a.chat + ((size_t)img * a.upl + (unit - a.unit0)) * a.K_max * (size_t)a.wpx;
 
@@ -357,7 +362,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     cp_async_commit();
   };
 
-  for (int k = k_begin; k < k_end; ++k) {
+  for (int k = k_begin; k < *kend_s; ++k) {
     if (k == 0 && skip0) continue;   // plane 0 of a full unit: the tonal pass knows it
     if constexpr (!SPEC) {
 #pragma unroll
@@ -412,7 +417,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
       __syncthreads();
       // next plane's table into the other buffer (its last reader, plane k-1's
       // y pass A, finished before this plane's first barrier)
-      if (mtab && k + 1 < k_end) build_mtab(k + 1);
+      if (mtab && k + 1 < *kend_s) build_mtab(k + 1);
       // ---------------- forward y, pass B: item (xp, k1)
 #pragma unroll
       for (int g = 0; g < C::G_yB; ++g) {
