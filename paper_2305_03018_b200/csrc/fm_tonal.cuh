@@ -373,11 +373,25 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a) 
     const TonalPix pp = tonal_pixel_job(a, a.list[j], blk * NT + tid);
     const float2* xs = tstg + (size_t)st * K * NT + tid;
     float2 A[N], B[N];
+    // c2r packing Z[k] = s_k + i w_k d_k, s_k = X[k] + X[N-k]^*, d_k = X[k] - X[N-k]^*,
+    // w_k = exp(+2 pi i k / T); the partner N-k reuses s, d and m = w_k d_k:
+    // Z[N-k] = s^* + i m^*  (w_{N-k} = -w_k^*, d_{N-k} = -d_k^*)
+    {
+      const float2 x0 = stage_k0[st] ? make_float2(a.x0_full, 0.f) : xs[0];
+      const float2 xc = conjf2(xs[N * NT]);
+      A[0] = cadd(cadd(x0, xc), mul_pi(csub(x0, xc)));
+    }
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      const float2 xk = (k == 0 && stage_k0[st]) ? make_float2(a.x0_full, 0.f) : xs[k * NT];
-      const float2 xc = conjf2(xs[(N - k) * NT]);
-      A[k] = cadd(cadd(xk, xc), mul_pi(cmul(c_ttw[off + k], csub(xk, xc))));
+    for (int k = 1; 2 * k < N; ++k) {
+      const float2 xk = xs[k * NT], xm = conjf2(xs[(N - k) * NT]);
+      const float2 sk = cadd(xk, xm), dk = csub(xk, xm);
+      const float2 m = cmul(c_ttw[off + k], dk);
+      A[k] = make_float2(sk.x - m.y, sk.y + m.x);
+      A[N - k] = make_float2(sk.x + m.y, m.x - sk.y);
+    }
+    if constexpr (N % 2 == 0 && N > 0) {
+      const float2 xh = xs[(N / 2) * NT];
+      A[N / 2] = make_float2(2.f * xh.x, -2.f * xh.y);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);   // stage read into registers
