@@ -192,6 +192,9 @@ int g_tonal_pipe_occ[kTonalCount];   // CTAs per SM of each pipelined variant (0
 int g_num_sms = 148;
 const bool g_tonal_nopipe = std::getenv("FM_TONAL_NOPIPE") != nullptr;  // A/B switch for measurements
 const bool g_no_skip0 = std::getenv("FM_NO_SKIP0") != nullptr;         // A/B: always compute plane 0
+// pipelined tonal CTAs per SM (persistent grid); below the occupancy limit it
+// leaves room for the next chunk's range CTAs
+const int g_tonal_occ_cap = std::getenv("FM_TONAL_OCC") ? std::atoi(std::getenv("FM_TONAL_OCC")) : 64;
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
@@ -284,7 +287,10 @@ struct fm_plan {
   int units = 1, wpx = 1, npx = 1, win_y = 1, win_x = 1, unit_step_x = 0;  // wpx: even plane stride
   std::vector<int2> taps;                 // clamp-bound taps of fm_range.cuh, best first
   std::vector<int> full_prefix;           // prefix count of "full" units (window inside the image)
-  int* range_part = nullptr;              // [ipc*units][8] split partials of fm_range.cuh
+  // range outputs are double-buffered so the range kernel of the next launch
+  // chunk runs on its own low-priority stream while this chunk's conv / tonal
+  // kernels still read the current set
+  int* range_part[2] = {};                // [ipc*units][8] split partials of fm_range.cuh
   bool counts = false;                    // FM_FLAG_COUNTS: count-volume output
   float2* enc_tab = nullptr;              // per ladder entry: exp(-2 pi i j / T), j < T, then 0
   int* d_enc_off = nullptr;               // [L] offsets into enc_tab
@@ -292,12 +298,15 @@ struct fm_plan {
   int upl = 1;                            // units per launch (chat slots per image)
   int* d_ladder = nullptr;
   int64_t* d_spec_off = nullptr;
-  int4* unit_param = nullptr;             // [ipc][units]
-  int* bucket_count = nullptr;            // [L]
-  int2* bucket_list = nullptr;            // [L][ipc*units]
-  int* h_counts = nullptr;                // mapped pinned [L], written by publish_counts
-  int* h_counts_dev = nullptr;            // its device alias
-  cudaEvent_t count_ev = nullptr;
+  int4* unit_param[2] = {};               // [ipc][units]
+  int* bucket_count[2] = {};              // [L]
+  int2* bucket_list[2] = {};              // [L][ipc*units]
+  int* h_counts[2] = {};                  // mapped pinned [L], written by publish_counts
+  int* h_counts_dev[2] = {};              // their device aliases
+  cudaEvent_t count_ev[2] = {};           // range + counts of a buffer set done (on range_stream)
+  cudaEvent_t free_ev[2] = {};            // conv + tonal done with a buffer set (on the caller's stream)
+  cudaEvent_t entry_ev = nullptr;
+  cudaStream_t range_stream = nullptr;
   cudaStream_t aux[kAuxStreams] = {};     // tonal launches side by side
   cudaEvent_t ev_fork = nullptr, ev_join[kAuxStreams] = {};
   int64_t planes_done = 0, units_done = 0; // for the plan's mean planes per unit
@@ -331,20 +340,25 @@ void free_plan(fm_plan* p) {
   for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
   cudaFree(p->d_ladder);
   cudaFree(p->d_spec_off);
-  cudaFree(p->range_part);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(p->range_part[b]);
+    cudaFree(p->unit_param[b]);
+    cudaFree(p->bucket_count[b]);
+    cudaFree(p->bucket_list[b]);
+    if (p->h_counts[b]) cudaFreeHost(p->h_counts[b]);
+    if (p->count_ev[b]) cudaEventDestroy(p->count_ev[b]);
+    if (p->free_ev[b]) cudaEventDestroy(p->free_ev[b]);
+  }
+  if (p->entry_ev) cudaEventDestroy(p->entry_ev);
+  if (p->range_stream) cudaStreamDestroy(p->range_stream);
   cudaFree(p->enc_tab);
   cudaFree(p->d_enc_off);
-  cudaFree(p->unit_param);
-  cudaFree(p->bucket_count);
-  cudaFree(p->bucket_list);
   cudaFree(p->S);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
   for (cudaEvent_t e : p->ev_chunks) cudaEventDestroy(e);
   if (p->ev_in) cudaEventDestroy(p->ev_in);
   if (p->ev_done) cudaEventDestroy(p->ev_done);
-  if (p->h_counts) cudaFreeHost(p->h_counts);
-  if (p->count_ev) cudaEventDestroy(p->count_ev);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   for (int i = 0; i < kAuxStreams; ++i) {
     if (p->aux[i]) cudaStreamDestroy(p->aux[i]);
@@ -691,12 +705,22 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   if ((e = cudaMalloc(&p->spec, sizeof(float4) * spec_f4)) != cudaSuccess) return cfail(e, "spec alloc");
   if ((e = cudaMalloc(&p->d_ladder, sizeof(int) * L)) != cudaSuccess) return cfail(e, "ladder alloc");
   if ((e = cudaMalloc(&p->d_spec_off, sizeof(int64_t) * L)) != cudaSuccess) return cfail(e, "ladder alloc");
-  if ((e = cudaMalloc(&p->unit_param, sizeof(int4) * p->ipc * p->units)) != cudaSuccess) return cfail(e, "unit alloc");
-  if ((e = cudaMalloc(&p->bucket_count, sizeof(int) * L)) != cudaSuccess) return cfail(e, "bucket alloc");
-  if ((e = cudaMalloc(&p->bucket_list, sizeof(int2) * cap * L)) != cudaSuccess) return cfail(e, "bucket alloc");
-  if ((e = cudaHostAlloc(&p->h_counts, sizeof(int) * L, cudaHostAllocMapped)) != cudaSuccess) return cfail(e, "pinned alloc");
-  if ((e = cudaHostGetDevicePointer(&p->h_counts_dev, p->h_counts, 0)) != cudaSuccess) return cfail(e, "pinned map");
-  if ((e = cudaEventCreateWithFlags(&p->count_ev, cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+  for (int b = 0; b < 2; ++b) {
+    if ((e = cudaMalloc(&p->unit_param[b], sizeof(int4) * p->ipc * p->units)) != cudaSuccess) return cfail(e, "unit alloc");
+    if ((e = cudaMalloc(&p->bucket_count[b], sizeof(int) * L)) != cudaSuccess) return cfail(e, "bucket alloc");
+    if ((e = cudaMalloc(&p->bucket_list[b], sizeof(int2) * cap * L)) != cudaSuccess) return cfail(e, "bucket alloc");
+    if ((e = cudaHostAlloc(&p->h_counts[b], sizeof(int) * L, cudaHostAllocMapped)) != cudaSuccess) return cfail(e, "pinned alloc");
+    if ((e = cudaHostGetDevicePointer(&p->h_counts_dev[b], p->h_counts[b], 0)) != cudaSuccess) return cfail(e, "pinned map");
+    if ((e = cudaEventCreateWithFlags(&p->count_ev[b], cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+    if ((e = cudaEventCreateWithFlags(&p->free_ev[b], cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+  }
+  if ((e = cudaEventCreateWithFlags(&p->entry_ev, cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+  {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if ((e = cudaStreamCreateWithPriority(&p->range_stream, cudaStreamNonBlocking, least)) != cudaSuccess)
+      return cfail(e, "stream");
+  }
   if ((e = cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
   for (int i = 0; i < kAuxStreams; ++i) {
     if ((e = cudaStreamCreateWithFlags(&p->aux[i], cudaStreamNonBlocking)) != cudaSuccess) return cfail(e, "stream");
@@ -704,14 +728,15 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   }
   {
     const size_t np = (size_t)p->ipc * p->units;
-    if ((e = cudaMalloc(&p->range_part, sizeof(int) * 8 * np)) != cudaSuccess) return cfail(e, "range alloc");
+    for (int b = 0; b < 2; ++b)
+      if ((e = cudaMalloc(&p->range_part[b], sizeof(int) * 8 * np)) != cudaSuccess) return cfail(e, "range alloc");
     std::vector<int> init(8 * np, 0);
     for (size_t i = 0; i < np; ++i) {
       init[8 * i + 0] = INT32_MAX;
       init[8 * i + 1] = INT32_MIN;
       init[8 * i + 2] = INT32_MAX;
     }
-    cudaMemcpy(p->range_part, init.data(), sizeof(int) * 8 * np, cudaMemcpyHostToDevice);
+    for (int b = 0; b < 2; ++b) cudaMemcpy(p->range_part[b], init.data(), sizeof(int) * 8 * np, cudaMemcpyHostToDevice);
   }
   {
     // encode tables, FP64-rounded: entry j = exp(-2 pi i j / T), entry T = 0
@@ -862,12 +887,28 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
   const int dsz = dtype_size(p->d.img_dtype);
   const int L = (int)p->ladder.size();
   const int64_t cap = p->ipc * p->upl;
+  // launch steps: (image chunk, unit chunk)
+  struct Step {
+    int64_t c0;
+    int n, u0, nu;
+  };
+  std::vector<Step> steps;
   for (int64_t c0 = cbeg; c0 < cend; c0 += p->ipc) {
-   const int n = (int)std::min<int64_t>(p->ipc, cend - c0);
-   for (int u0 = 0; u0 < p->units; u0 += p->upl) {
-    const int nu = std::min(p->upl, p->units - u0);
+    const int n = (int)std::min<int64_t>(p->ipc, cend - c0);
+    for (int u0 = 0; u0 < p->units; u0 += p->upl) steps.push_back({c0, n, u0, std::min(p->upl, p->units - u0)});
+  }
+  if (steps.empty()) return FM_OK;
+  // range kernels run one step ahead on a low-priority stream (double-buffered
+  // outputs): they fill the conv tail and overlap the tonal kernels
+  cudaStream_t rs = p->range_stream;
+  FM_CUDA(cudaEventRecord(p->entry_ev, s));          // inputs / prior work on s
+  FM_CUDA(cudaStreamWaitEvent(rs, p->entry_ev, 0));
+  auto launch_range = [&](const Step& st, int buf) -> int {
+    const int64_t c0 = st.c0;
+    const int n = st.n, u0 = st.u0, nu = st.nu;
+    FM_CUDA(cudaStreamWaitEvent(rs, p->free_ev[buf], 0));   // the previous user of this buffer set
     // ---- per-unit tonal range -> ladder entry + work lists (fm_range.cuh)
-    FM_CUDA(cudaMemsetAsync(p->bucket_count, 0, sizeof(int) * L, s));
+    FM_CUDA(cudaMemsetAsync(p->bucket_count[buf], 0, sizeof(int) * L, rs));
     RangeArgs r{};
     r.img = reinterpret_cast<const char*>(img) + (size_t)c0 * img_elems * dsz;
     r.img_def = img_defined ? img_defined + (size_t)c0 * img_elems : nullptr;
@@ -912,36 +953,51 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
                      : (size_t)((p->unit_step_x + S - 1) / S + p->mx - 1) * 2;
       rsm = (rsm + 15) & ~(size_t)15;
     }
-    r.part = p->range_part;
+    r.part = p->range_part[buf];
     r.ladder = p->d_ladder;
     r.L = L;
-    r.unit_param = p->unit_param;
-    r.bucket_count = p->bucket_count;
-    r.bucket_list = p->bucket_list;
+    r.unit_param = p->unit_param[buf];
+    r.bucket_count = p->bucket_count[buf];
+    r.bucket_list = p->bucket_list[buf];
     r.cap = (int)cap;
     r.err = p->stats + 1;
     int er = -1;
-    if (p->timing) { er = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
+    if (p->timing) { er = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), rs)); }
     {
       const dim3 rg((unsigned)(nu * S), n);
-      if (p->d.img_dtype == FM_U8) range_kernel<0><<<rg, kRangeNT, rsm, s>>>(r);
-      else if (p->d.img_dtype == FM_U16) range_kernel<1><<<rg, kRangeNT, rsm, s>>>(r);
-      else range_kernel<2><<<rg, kRangeNT, rsm, s>>>(r);
+      if (p->d.img_dtype == FM_U8) range_kernel<0><<<rg, kRangeNT, rsm, rs>>>(r);
+      else if (p->d.img_dtype == FM_U16) range_kernel<1><<<rg, kRangeNT, rsm, rs>>>(r);
+      else range_kernel<2><<<rg, kRangeNT, rsm, rs>>>(r);
     }
     g_launches++;
     FM_CUDA(cudaGetLastError());
     if (p->timing) {
-      FM_CUDA(cudaEventRecord(next_event(p), s));
+      FM_CUDA(cudaEventRecord(next_event(p), rs));
       p->pending_range.push_back({er, er + 1});
     }
     // the counts reach the host through a kernel store to mapped memory, not a
     // copy-engine D2H: a D2H copy would queue behind any large D2H transfer in
     // flight on the device (e.g. the previous chunk's outputs)
-    publish_counts<<<1, 64, 0, s>>>(p->bucket_count, p->h_counts_dev, L);
+    publish_counts<<<1, 64, 0, rs>>>(p->bucket_count[buf], p->h_counts_dev[buf], L);
     g_launches++;
     FM_CUDA(cudaGetLastError());
-    FM_CUDA(cudaEventRecord(p->count_ev, s));
+    FM_CUDA(cudaEventRecord(p->count_ev[buf], rs));
 
+    return FM_OK;
+  };
+  {
+    int rc = launch_range(steps[0], 0);
+    if (rc) return rc;
+  }
+  for (size_t si = 0; si < steps.size(); ++si) {
+    const int buf = (int)(si & 1);
+    if (si + 1 < steps.size()) {
+      int rc = launch_range(steps[si + 1], buf ^ 1);
+      if (rc) return rc;
+    }
+    const int64_t c0 = steps[si].c0;
+    const int n = steps[si].n, u0 = steps[si].u0, nu = steps[si].nu;
+    FM_CUDA(cudaStreamWaitEvent(s, p->count_ev[buf], 0));
     TileArgs a{};
     a.img = reinterpret_cast<const char*>(img) + (size_t)c0 * img_elems * dsz;
     a.img_def = img_defined ? img_defined + (size_t)c0 * img_elems : nullptr;
@@ -967,15 +1023,15 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     a.spec = p->spec;
     a.chat = p->chat;
     a.err = p->stats + 1;
-    a.unit_param = p->unit_param;
+    a.unit_param = p->unit_param[buf];
     a.spec_off = p->d_spec_off;
     a.units = p->units;
     a.unit0 = u0;
     a.upl = p->upl;
     a.K_max = p->K;
     a.wpx = p->wpx;
-    a.bucket_count = p->bucket_count;
-    a.bucket_list = p->bucket_list;
+    a.bucket_count = p->bucket_count[buf];
+    a.bucket_list = p->bucket_list[buf];
     a.ladder = p->d_ladder;
     a.enc_tab = p->enc_tab;
     a.enc_off = p->d_enc_off;
@@ -1016,7 +1072,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       b.mx = a.mx;
       b.tiles_x = a.tiles_x;
       b.enc_sign = a.enc_sign;
-      b.unit_param = p->unit_param;
+      b.unit_param = p->unit_param[buf];
       b.units = p->units;
       b.unit0 = u0;
       b.upl = p->upl;
@@ -1049,15 +1105,15 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
 
     // ---- the tonal kernels need the per-ladder unit counts (ready long before
     // the conv kernel finishes; the host waits only for the small copy)
-    FM_CUDA(cudaEventSynchronize(p->count_ev));
+    FM_CUDA(cudaEventSynchronize(p->count_ev[buf]));
     if (dyn) {
       int64_t planes_tot = 0;
       for (int li = 0; li < L; ++li)
-        planes_tot += (int64_t)reinterpret_cast<volatile int*>(p->h_counts)[li] * (p->ladder[li] + 1);
+        planes_tot += (int64_t)reinterpret_cast<volatile int*>(p->h_counts[buf])[li] * (p->ladder[li] + 1);
       const int kc = (int)std::max<int64_t>(1, (planes_tot + conv_target - 1) / conv_target);
       int64_t jobs = 0;
       for (int li = 0; li < L; ++li)
-        jobs += (int64_t)reinterpret_cast<volatile int*>(p->h_counts)[li] * ((p->ladder[li] + kc) / kc);
+        jobs += (int64_t)reinterpret_cast<volatile int*>(p->h_counts[buf])[li] * ((p->ladder[li] + kc) / kc);
       a.k_chunk = kc;
       if (jobs > 0) {
         int rc = launch_conv((unsigned)jobs);
@@ -1067,7 +1123,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     TonalArgs t{};
     t.chat = p->chat;
     t.K_max = p->K;
-    t.unit_param = p->unit_param;
+    t.unit_param = p->unit_param[buf];
     t.units = p->units;
     t.unit0 = u0;
     t.upl = p->upl;
@@ -1100,7 +1156,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     // one launch per ladder entry in use, spread over the aux streams so the
     // small ones (few units each) run side by side; joined back into s
     int nlaunch = 0;
-    for (int li = 0; li < L; ++li) nlaunch += reinterpret_cast<volatile int*>(p->h_counts)[li] > 0;
+    for (int li = 0; li < L; ++li) nlaunch += reinterpret_cast<volatile int*>(p->h_counts[buf])[li] > 0;
     const int nstreams = std::min(nlaunch, 1 + kAuxStreams);
     if (nstreams > 1) {
       FM_CUDA(cudaEventRecord(p->ev_fork, s));
@@ -1108,7 +1164,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     }
     int launch_i = 0;
     for (int li = L - 1; li >= 0; --li) {
-      const int cnt = reinterpret_cast<volatile int*>(p->h_counts)[li];
+      const int cnt = reinterpret_cast<volatile int*>(p->h_counts[buf])[li];
       if (cnt <= 0) continue;
       const int N = p->ladder[li];
       const int si = launch_i++ % nstreams;
@@ -1116,13 +1172,13 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       t.N = N;
       t.T = 2 * N;
       t.x0_full = (float)((double)p->se_count / (2.0 * N));
-      t.list = p->bucket_list + (size_t)li * cap;
+      t.list = p->bucket_list[buf] + (size_t)li * cap;
       const TonalVariant* tv = p->counts ? nullptr : p->ladder_var[li];
       const int occ = tv ? g_tonal_pipe_occ[tv - kTonal] : 0;
       if (tv && occ > 0 && !g_tonal_nopipe && N <= g_tonal_pipe_max) {
         t.njobs = cnt;
         const int64_t items = (int64_t)cnt * ((p->npx + tv->pipe_nt - 1) / tv->pipe_nt);
-        const int grid = (int)std::min<int64_t>(items, (int64_t)g_num_sms * occ);
+        const int grid = (int)std::min<int64_t>(items, (int64_t)g_num_sms * std::min(occ, g_tonal_occ_cap));
         tv->pipe_fn(dim3((unsigned)grid), tv->pipe_nt, tv->pipe_smem, ts, t);
       } else if (tv) {
         const int nt = tv->nt;
@@ -1161,7 +1217,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       p->acc.conv_flops += planes * p->conv_flops_per_plane;
       p->acc.tonal_bytes += tonal_b;
     }
-   }
+    FM_CUDA(cudaEventRecord(p->free_ev[buf], s));
   }
   return FM_OK;
 }
