@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "fftmorph_b200.h"
@@ -879,8 +880,12 @@ int fm_reset_stats(fm_plan* p, void* stream) {
 // launch chunks of ipc images and upl units.
 static int out_size(int od) { return od == FM_OUT_U8 ? 1 : (od == FM_OUT_U16 || od == FM_OUT_I16) ? 2 : 4; }
 
+// in_ready (optional): one event per image chunk of ipc images, recorded when
+// that chunk's input is in place; after_chunk (optional): called once a chunk's
+// last kernels are enqueued on s (the host-buffer path queues its D2H there).
 static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, void* out, uint8_t* valid,
-                      cudaStream_t s, int64_t cbeg, int64_t cend) {
+                      cudaStream_t s, int64_t cbeg, int64_t cend, const cudaEvent_t* in_ready = nullptr,
+                      const std::function<int(int64_t, int)>& after_chunk = nullptr) {
   p->last_stream = s;
   const int64_t npix = p->OH * p->OW;
   const int64_t img_elems = p->H * p->W;
@@ -907,6 +912,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     const int64_t c0 = st.c0;
     const int n = st.n, u0 = st.u0, nu = st.nu;
     FM_CUDA(cudaStreamWaitEvent(rs, p->free_ev[buf], 0));   // the previous user of this buffer set
+    if (in_ready) FM_CUDA(cudaStreamWaitEvent(rs, in_ready[(c0 - cbeg) / p->ipc], 0));
     // ---- per-unit tonal range -> ladder entry + work lists (fm_range.cuh)
     FM_CUDA(cudaMemsetAsync(p->bucket_count[buf], 0, sizeof(int) * L, rs));
     RangeArgs r{};
@@ -1218,6 +1224,10 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       p->acc.tonal_bytes += tonal_b;
     }
     FM_CUDA(cudaEventRecord(p->free_ev[buf], s));
+    if (after_chunk && u0 + nu >= p->units) {
+      int rc = after_chunk(c0, n);
+      if (rc) return rc;
+    }
   }
   return FM_OK;
 }
@@ -1324,49 +1334,40 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, v
   FM_CUDA(cudaEventRecord(p->ev_in, s));          // order after prior work on s
   FM_CUDA(cudaStreamWaitEvent(hs, p->ev_in, 0));
   FM_CUDA(cudaStreamWaitEvent(ds, p->ev_in, 0));
-  // chunk plan: a one-image chunk first and last, so the pipeline fills after
-  // one image's upload and drains after one image's download
-  std::vector<std::pair<int64_t, int64_t>> chunks;   // (first image, images)
-  {
-    int64_t c0 = 0, left = p->batch;
-    if (left > 2 && p->ipc > 1) {
-      chunks.push_back({0, 1});
-      c0 = 1;
-      left -= 1;
-    }
-    while (left > 0) {
-      int64_t n = std::min<int64_t>(p->ipc, left);
-      if (n == left && n > 1 && p->ipc > 1 && p->batch > 2) n -= 1;   // keep the last image on its own
-      chunks.push_back({c0, n});
-      c0 += n;
-      left -= n;
-    }
-  }
-  if (p->ev_chunks.size() < 2 * chunks.size()) {
+  // every H2D is queued up front on hs (one event per chunk of ipc images);
+  // one run_images call then pipelines the whole batch (the range kernels run
+  // a step ahead as in fm_execute) and each chunk's D2H is queued on ds as soon
+  // as its tonal kernels are
+  const int64_t nchunks = (p->batch + p->ipc - 1) / p->ipc;
+  if ((int64_t)p->ev_chunks.size() < 2 * nchunks) {
     const size_t old = p->ev_chunks.size();
-    p->ev_chunks.resize(2 * chunks.size());
+    p->ev_chunks.resize(2 * nchunks);
     for (size_t i = old; i < p->ev_chunks.size(); ++i)
       FM_CUDA(cudaEventCreateWithFlags(&p->ev_chunks[i], cudaEventDisableTiming));
   }
-  for (size_t ci = 0; ci < chunks.size(); ++ci) {
-    const int64_t c0 = chunks[ci].first, n = chunks[ci].second;
+  std::vector<cudaEvent_t> in_ev(nchunks);
+  for (int64_t ci = 0; ci < nchunks; ++ci) {
+    const int64_t c0 = ci * p->ipc, n = std::min<int64_t>(p->ipc, p->batch - c0);
     FM_CUDA(cudaMemcpyAsync(din + c0 * img_e * dsz, hin + c0 * img_e * dsz, n * img_e * dsz, cudaMemcpyHostToDevice, hs));
     if (def_host)
       FM_CUDA(cudaMemcpyAsync(p->h_def + c0 * img_e, def_host + c0 * img_e, n * img_e, cudaMemcpyHostToDevice, hs));
     FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci], hs));
+    in_ev[ci] = p->ev_chunks[2 * ci];
   }
-  for (size_t ci = 0; ci < chunks.size(); ++ci) {
-    const int64_t c0 = chunks[ci].first, n = chunks[ci].second;
-    FM_CUDA(cudaStreamWaitEvent(s, p->ev_chunks[2 * ci], 0));
-    int rc = run_images(p, p->h_img, def_host ? p->h_def : nullptr, p->h_out, valid_host ? p->h_valid : nullptr, s,
-                        c0, c0 + n);
-    if (rc) return rc;
+  auto after = [&](int64_t c0, int n) -> int {
+    const int64_t ci = c0 / p->ipc;
     FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci + 1], s));
     FM_CUDA(cudaStreamWaitEvent(ds, p->ev_chunks[2 * ci + 1], 0));
     FM_CUDA(cudaMemcpyAsync(out_host + c0 * out_e * osz, reinterpret_cast<char*>(p->h_out) + c0 * out_e * osz,
                             n * out_e * osz, cudaMemcpyDeviceToHost, ds));
     if (valid_host)
       FM_CUDA(cudaMemcpyAsync(valid_host + c0 * out_e, p->h_valid + c0 * out_e, n * out_e, cudaMemcpyDeviceToHost, ds));
+    return FM_OK;
+  };
+  {
+    int rc = run_images(p, p->h_img, def_host ? p->h_def : nullptr, p->h_out, valid_host ? p->h_valid : nullptr, s, 0,
+                        p->batch, in_ev.data(), after);
+    if (rc) return rc;
   }
   FM_CUDA(cudaStreamSynchronize(ds));
   FM_CUDA(cudaStreamSynchronize(s));
