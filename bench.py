@@ -93,6 +93,18 @@ class Clocks:
         except Exception:
             self.proc = None
 
+    def wait_first(self, timeout=10.0):
+        """Block until nvidia-smi has written its first sample (its start-up takes longer
+        than a short timed region)."""
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < timeout:
+            try:
+                if self.path.stat().st_size > 0:
+                    return
+            except FileNotFoundError:
+                pass
+            time.sleep(0.05)
+
     def stop(self):
         if self.proc is None:
             return None
@@ -200,6 +212,10 @@ def run_ours(args, rank, world, local_rank):
     def step():
         plan.execute(x, out=out, valid=valid, stream=stream)
 
+    # the clock sampler runs from before the warm-up (all of it under load) to the end
+    # of the timed region
+    clocks = Clocks(local_rank)
+    clocks.wait_first()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -207,7 +223,6 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = Clocks(local_rank)
     plan.get_timing(reset=True)
     plan.set_timing(True)
     l0 = _lib.kernel_launches()
@@ -323,7 +338,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--images", type=int, default=N_IMAGES)
-    ap.add_argument("--scratch-gib", type=int, default=4)
+    ap.add_argument("--scratch-gib", type=int, default=16)
     ap.add_argument("--out-dtype", choices=["u8", "i16", "i32"], default="u8",
                     help="output value type (the c5 dilation range 0..78 fits u8)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")

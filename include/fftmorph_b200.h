@@ -67,7 +67,7 @@ typedef struct fm_plan_desc {
                             [img_min, img_max] make fm_execute fail with FM_EINVAL */
   int32_t fill;          /* output value at pixels with no (image, SE) pair */
   int32_t device;        /* CUDA device ordinal */
-  int64_t scratch_bytes; /* spectral scratch budget (0 = default 4 GiB) */
+  int64_t scratch_bytes; /* spectral scratch budget (0 = default 16 GiB) */
   int32_t tile;          /* 0 = auto, else forced FFT tile edge (16..256) */
   int32_t tonal_len;     /* 0 = auto, else forced tonal length T (even, > l_R) */
   int32_t out_dtype;     /* fm_out_dtype of the output values (0 = int32) */

@@ -665,7 +665,8 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   // scratch per unit: its K_max spectral planes (+ the 256^2 tile slab on the big path).
   // Whole images per launch when they fit the budget, else chunks of units of one image.
   const int64_t per_unit = (int64_t)p->K * p->wpx * 8 + (p->big ? (int64_t)p->K * kBig * kBig * 8 : 0);
-  const int64_t budget = d.scratch_bytes > 0 ? d.scratch_bytes : (int64_t)4 << 30;
+  // default budget 16 GiB: large launches keep the per-launch tail small (B200: 180 GB HBM)
+  const int64_t budget = d.scratch_bytes > 0 ? d.scratch_bytes : (int64_t)16 << 30;
   p->upl = (int)std::max<int64_t>(1, std::min<int64_t>(p->units, budget / std::max<int64_t>(per_unit, 1)));
   if (p->upl < p->units) {
     p->ipc = 1;
@@ -880,12 +881,15 @@ int fm_reset_stats(fm_plan* p, void* stream) {
 // launch chunks of ipc images and upl units.
 static int out_size(int od) { return od == FM_OUT_U8 ? 1 : (od == FM_OUT_U16 || od == FM_OUT_I16) ? 2 : 4; }
 
-// in_ready (optional): one event per image chunk of ipc images, recorded when
-// that chunk's input is in place; after_chunk (optional): called once a chunk's
-// last kernels are enqueued on s (the host-buffer path queues its D2H there).
+// chunks (optional): explicit image chunks (first image, images <= ipc), else
+// chunks of ipc images; in_ready (optional): one event per chunk, recorded when
+// that chunk's input is in place; after_chunk (optional): called with the chunk
+// index once its last kernels are enqueued on s (the host-buffer path queues
+// its D2H there).
 static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, void* out, uint8_t* valid,
-                      cudaStream_t s, int64_t cbeg, int64_t cend, const cudaEvent_t* in_ready = nullptr,
-                      const std::function<int(int64_t, int)>& after_chunk = nullptr) {
+                      cudaStream_t s, int64_t cbeg, int64_t cend,
+                      const std::vector<std::pair<int64_t, int>>* chunks = nullptr, const cudaEvent_t* in_ready = nullptr,
+                      const std::function<int(size_t, int64_t, int)>& after_chunk = nullptr) {
   p->last_stream = s;
   const int64_t npix = p->OH * p->OW;
   const int64_t img_elems = p->H * p->W;
@@ -896,12 +900,18 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
   struct Step {
     int64_t c0;
     int n, u0, nu;
+    size_t chunk;
   };
   std::vector<Step> steps;
-  for (int64_t c0 = cbeg; c0 < cend; c0 += p->ipc) {
-    const int n = (int)std::min<int64_t>(p->ipc, cend - c0);
-    for (int u0 = 0; u0 < p->units; u0 += p->upl) steps.push_back({c0, n, u0, std::min(p->upl, p->units - u0)});
+  std::vector<std::pair<int64_t, int>> plan_chunks;
+  if (chunks) {
+    plan_chunks = *chunks;
+  } else {
+    for (int64_t c0 = cbeg; c0 < cend; c0 += p->ipc) plan_chunks.push_back({c0, (int)std::min<int64_t>(p->ipc, cend - c0)});
   }
+  for (size_t ci = 0; ci < plan_chunks.size(); ++ci)
+    for (int u0 = 0; u0 < p->units; u0 += p->upl)
+      steps.push_back({plan_chunks[ci].first, plan_chunks[ci].second, u0, std::min(p->upl, p->units - u0), ci});
   if (steps.empty()) return FM_OK;
   // range kernels run one step ahead on a low-priority stream (double-buffered
   // outputs): they fill the conv tail and overlap the tonal kernels
@@ -912,7 +922,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     const int64_t c0 = st.c0;
     const int n = st.n, u0 = st.u0, nu = st.nu;
     FM_CUDA(cudaStreamWaitEvent(rs, p->free_ev[buf], 0));   // the previous user of this buffer set
-    if (in_ready) FM_CUDA(cudaStreamWaitEvent(rs, in_ready[(c0 - cbeg) / p->ipc], 0));
+    if (in_ready) FM_CUDA(cudaStreamWaitEvent(rs, in_ready[st.chunk], 0));
     // ---- per-unit tonal range -> ladder entry + work lists (fm_range.cuh)
     FM_CUDA(cudaMemsetAsync(p->bucket_count[buf], 0, sizeof(int) * L, rs));
     RangeArgs r{};
@@ -1225,7 +1235,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     }
     FM_CUDA(cudaEventRecord(p->free_ev[buf], s));
     if (after_chunk && u0 + nu >= p->units) {
-      int rc = after_chunk(c0, n);
+      int rc = after_chunk(steps[si].chunk, c0, n);
       if (rc) return rc;
     }
   }
@@ -1338,7 +1348,25 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, v
   // one run_images call then pipelines the whole batch (the range kernels run
   // a step ahead as in fm_execute) and each chunk's D2H is queued on ds as soon
   // as its tonal kernels are
-  const int64_t nchunks = (p->batch + p->ipc - 1) / p->ipc;
+  // chunk plan: one-image chunks first and last, so the pipeline fills after one
+  // image's upload and drains after one image's download
+  std::vector<std::pair<int64_t, int>> chunks;
+  {
+    int64_t c0 = 0, left = p->batch;
+    if (left > 2 && p->ipc > 1) {
+      chunks.push_back({0, 1});
+      c0 = 1;
+      left -= 1;
+    }
+    while (left > 0) {
+      int64_t n = std::min<int64_t>(p->ipc, left);
+      if (n == left && n > 1 && p->ipc > 1 && p->batch > 2) n -= 1;
+      chunks.push_back({c0, (int)n});
+      c0 += n;
+      left -= n;
+    }
+  }
+  const int64_t nchunks = (int64_t)chunks.size();
   if ((int64_t)p->ev_chunks.size() < 2 * nchunks) {
     const size_t old = p->ev_chunks.size();
     p->ev_chunks.resize(2 * nchunks);
@@ -1347,15 +1375,14 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, v
   }
   std::vector<cudaEvent_t> in_ev(nchunks);
   for (int64_t ci = 0; ci < nchunks; ++ci) {
-    const int64_t c0 = ci * p->ipc, n = std::min<int64_t>(p->ipc, p->batch - c0);
+    const int64_t c0 = chunks[ci].first, n = chunks[ci].second;
     FM_CUDA(cudaMemcpyAsync(din + c0 * img_e * dsz, hin + c0 * img_e * dsz, n * img_e * dsz, cudaMemcpyHostToDevice, hs));
     if (def_host)
       FM_CUDA(cudaMemcpyAsync(p->h_def + c0 * img_e, def_host + c0 * img_e, n * img_e, cudaMemcpyHostToDevice, hs));
     FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci], hs));
     in_ev[ci] = p->ev_chunks[2 * ci];
   }
-  auto after = [&](int64_t c0, int n) -> int {
-    const int64_t ci = c0 / p->ipc;
+  auto after = [&](size_t ci, int64_t c0, int n) -> int {
     FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci + 1], s));
     FM_CUDA(cudaStreamWaitEvent(ds, p->ev_chunks[2 * ci + 1], 0));
     FM_CUDA(cudaMemcpyAsync(out_host + c0 * out_e * osz, reinterpret_cast<char*>(p->h_out) + c0 * out_e * osz,
@@ -1366,7 +1393,7 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, v
   };
   {
     int rc = run_images(p, p->h_img, def_host ? p->h_def : nullptr, p->h_out, valid_host ? p->h_valid : nullptr, s, 0,
-                        p->batch, in_ev.data(), after);
+                        p->batch, &chunks, in_ev.data(), after);
     if (rc) return rc;
   }
   FM_CUDA(cudaStreamSynchronize(ds));
