@@ -9,11 +9,14 @@ every operator raises — there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "_build" / "libfftmorph_b200.so"
+if os.environ.get("FM_LIB"):   # A/B builds for measurements (must still be an in-tree build)
+    LIB_PATH = Path(os.environ["FM_LIB"]).resolve()
 
 FM_OK, FM_EINVAL, FM_EPRECISION, FM_EDEVIATION, FM_ECUDA, FM_EUNSUPPORTED, FM_ENOMEM = range(7)
 FM_DILATE, FM_ERODE = 0, 1

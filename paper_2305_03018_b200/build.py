@@ -42,6 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3",
+           *os.environ.get("FM_NVCC_EXTRA", "").split(),
            "-I", str(ROOT / "include"), "-I", str(CSRC),
            *[str(s) for s in SOURCES], "-o", str(tmp), "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
