@@ -184,7 +184,16 @@ __device__ __forceinline__ void stock_stage(A& in, B& out) {
     for (int r = 0; r < R; ++r) v[r] = in[j + r * M];
     if (Ns > 1) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], c_ttw[off + 2 * ((jm * r * tstep) % N)]);
+      for (int r = 1; r < R; ++r) {
+        // exp(+2 pi i e / N); e is a constant after unrolling, so the trivial
+        // twiddles (1, -1, +-i) fold away
+        const int e = (jm * r * tstep) % N;
+        if (e == 0) continue;
+        if (4 * e == 2 * N) v[r] = make_float2(-v[r].x, -v[r].y);
+        else if (4 * e == N) v[r] = mul_pi(v[r]);
+        else if (4 * e == 3 * N) v[r] = mul_mi(v[r]);
+        else v[r] = cmul(v[r], c_ttw[off + 2 * e]);
+      }
     }
     dft<R, true>(v);
     const int idxD = (j / Ns) * Ns * R + jm;
