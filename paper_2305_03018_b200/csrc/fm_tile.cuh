@@ -117,6 +117,8 @@ struct TileCfg {
   static constexpr int NW = NT / 32;
   static constexpr int RPW = PY / NW;
   static_assert(RPW * NW == PY && RPW * (R2x / 2) == 32 && G_xA == 1, "x pass A: one item per lane");
+  // y pass B by warp-owned k1 groups (see the kernel): needs one 8-row group per warp
+  static constexpr bool kWarpY = TWO_D && R1y == NW && R2y == RPW && XP % 32 == 0 && G_yB * 32 == XP;
   static constexpr int kBufBytes = PY * RS * 8;
   static constexpr int kSpecPairs = NPTS / 2;           // float4 per tonal plane
   static constexpr int SQ = R2x / 2;                    // float4 per x-pass-B item
@@ -419,10 +421,14 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
       // y pass A, finished before this plane's first barrier)
       if (mtab && k + 1 < *kend_s) build_mtab(k + 1);
       // ---------------- forward y, pass B: item (xp, k1)
+      // With one warp per k1 group (R1y == warps, R2y == rows per warp) the
+      // group is exactly the warp's x-pass rows: y pass B, the x passes and
+      // inverse y pass B then run warp-locally between two CTA barriers.
 #pragma unroll
       for (int g = 0; g < C::G_yB; ++g) {
         const int i = tid + NT * g;
-        const int xp = i % C::XP, k1 = i / C::XP;
+        const int xp = C::kWarpY ? lane + 32 * g : i % C::XP;
+        const int k1 = C::kWarpY ? warp : i / C::XP;
         float2 wa[C::R2y], wb[C::R2y];
 #pragma unroll
         for (int n2 = 0; n2 < C::R2y; ++n2) {
@@ -435,7 +441,8 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
 #pragma unroll
         for (int k2 = 0; k2 < C::R2y; ++k2) st2(k2 + C::R2y * k1, 2 * xp, wa[k2], wb[k2]);
       }
-      __syncthreads();
+      if constexpr (C::kWarpY) __syncwarp();
+      else __syncthreads();
     }
 
     // ---------------- forward x, pass A: item (y, n2 pair); 1-D: with encode
@@ -558,14 +565,16 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
       }
     }
     if constexpr (TWO_D) {
-      __syncthreads();
+      if constexpr (C::kWarpY) __syncwarp();
+      else __syncthreads();
       // column pairs entirely left of the valid window are not needed any more
       const int xp_min = (a.mx - 1) / 2;
       // ---------------- inverse y, pass B: item (xp, k1)
 #pragma unroll
       for (int g = 0; g < C::G_yB; ++g) {
         const int i = tid + NT * g;
-        const int xp = i % C::XP, k1 = i / C::XP;
+        const int xp = C::kWarpY ? lane + 32 * g : i % C::XP;
+        const int k1 = C::kWarpY ? warp : i / C::XP;
         if (xp < xp_min) continue;
         float2 wa[C::R2y], wb[C::R2y];
 #pragma unroll
