@@ -32,6 +32,7 @@
 //    stalling the spectral product.
 #pragma once
 #include <type_traits>
+#include "fm_async.cuh"
 #include "fm_dft.cuh"
 
 namespace fm {
@@ -125,6 +126,12 @@ struct TileCfg {
   static constexpr int kChunkF4 = SQ * NT;              // float4 per spectrum chunk (one item per thread)
   static constexpr int NBUF = G_xB >= 2 ? 2 : 1;
   static constexpr int kSpecBytes = NBUF * kChunkF4 * 16;
+  // CONV: a plane's first two spectrum chunks arrive by bulk async copies
+  // (1-D TMA) issued a whole plane ahead, by the last warp to release the
+  // buffer; the later chunks by per-thread cp.async into the thread's own
+  // slots right after it consumed them (no cross-warp coupling mid-plane)
+  static constexpr bool kBulkSpec = NBUF == 2 && G_xB >= 2;
+  static constexpr uint32_t kChunkBytes = kChunkF4 * 16;
   static constexpr int kTvBytes = ((NPTS * 2 + 15) / 16) * 16;
   // x pass A twiddle pairs (W^{n2 k1}, W^{(n2+1) k1}) for the R2x/2 pair columns:
   // 16-byte slots, stride R1x+1 (conflict-free for the 4..8 distinct n2 of a
@@ -338,9 +345,28 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     const float2 w1 = c_tw[TwOff<PX>::v + ((n2 + 1) * k1) % PX];
     *twx_slot(j) = make_float4(w0.x, w0.y, w1.x, w1.y);
   }
+  __shared__ __align__(8) uint64_t s_full[2];   // spectrum ring (C::kBulkSpec)
+  __shared__ int s_rel[2];                       // warps that released the buffer's chunk
   {
     const int k_first = kchunk_idx * a.k_chunk + ((skip0 && kchunk_idx == 0) ? 1 : 0);
     if (mtab) build_mtab(k_first);
+    if constexpr (!SPEC && C::kBulkSpec) {
+      if (tid == 0) {
+        mbar_init(&s_full[0], 1);
+        mbar_init(&s_full[1], 1);
+        s_rel[0] = 0;
+        s_rel[1] = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (k_first < min(K, kchunk_idx * a.k_chunk + a.k_chunk)) {
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            mbar_expect_tx(&s_full[g], C::kChunkBytes);
+            bulk_g2s_nohint(sbuf + g * C::kChunkF4, spec_base + (size_t)k_first * C::kSpecPairs + (size_t)g * C::kChunkF4,
+                            C::kChunkBytes, &s_full[g]);
+          }
+        }
+      }
+    }
   }
   __syncthreads();
   const int ty = (TWO_D && !SPEC) ? unit / a.tiles_x : 0;
@@ -364,9 +390,10 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
     cp_async_commit();
   };
 
+  int pord = 0;   // planes done (ring phase when chunks per plane is not a multiple of 4)
   for (int k = k_begin; k < *kend_s; ++k) {
     if (k == 0 && skip0) continue;   // plane 0 of a full unit: the tonal pass knows it
-    if constexpr (!SPEC) {
+    if constexpr (!SPEC && !C::kBulkSpec) {
 #pragma unroll
       for (int g = 0; g < C::NBUF; ++g) spec_fetch(k, g);
     }
@@ -500,9 +527,17 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
             so[(g * C::SQ + q) * NT + tid] =
                 make_float4(w[2 * q].x * s, w[2 * q].y * s, w[2 * q + 1].x * s, w[2 * q + 1].y * s);
         } else {
-          // chunk g landed? (the newest NBUF-1 groups may still be in flight)
-          if (g + C::NBUF <= C::G_xB) cp_async_wait<C::NBUF - 1>();
-          else cp_async_wait<0>();
+          if (C::kBulkSpec && g < 2) {
+            mbar_wait(&s_full[g], (uint32_t)(pord & 1));
+          } else if (C::kBulkSpec) {
+            // per-thread chunks g >= 2 (committed after items g-2, g-1)
+            if (g + 1 < C::G_xB) cp_async_wait<1>();
+            else cp_async_wait<0>();
+          } else {
+            // chunk g landed? (the newest NBUF-1 groups may still be in flight)
+            if (g + C::NBUF <= C::G_xB) cp_async_wait<C::NBUF - 1>();
+            else cp_async_wait<0>();
+          }
           const float4* sp = sbuf + (g % C::NBUF) * C::kChunkF4 + tid;
           float4 s4[C::SQ];
 #pragma unroll
@@ -512,8 +547,27 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
             w[2 * q] = cmul(w[2 * q], make_float2(s4[q].x, s4[q].y));
             w[2 * q + 1] = cmul(w[2 * q + 1], make_float2(s4[q].z, s4[q].w));
           }
-          // refill this thread's own slots (their values are consumed above)
-          if (g + C::NBUF < C::G_xB) spec_fetch(k, g + C::NBUF);
+          if (C::kBulkSpec && g + 2 >= C::G_xB) {
+            // last chunks of the plane: release the buffer; the last warp to do so
+            // refills it with the next plane's chunk (a bulk copy a whole plane ahead)
+            __syncwarp();
+            if (lane == 0) {
+              __threadfence_block();
+              const int b = g & 1;
+              if (atomicAdd(&s_rel[b], 1) == C::NW - 1) {
+                s_rel[b] = 0;
+                if (k + 1 < *kend_s) {
+                  mbar_expect_tx(&s_full[b], C::kChunkBytes);
+                  bulk_g2s_nohint(sbuf + b * C::kChunkF4,
+                                  spec_base + (size_t)(k + 1) * C::kSpecPairs + (size_t)b * C::kChunkF4,
+                                  C::kChunkBytes, &s_full[b]);
+                }
+              }
+            }
+          } else if (g + C::NBUF < C::G_xB) {
+            // refill this thread's own slots (their values are consumed above)
+            spec_fetch(k, g + C::NBUF);
+          }
           dft<C::R2x, true>(w);
 #pragma unroll
           for (int q = 0; q < C::SQ; ++q) st2(y, 2 * q + C::R2x * k1, w[2 * q], w[2 * q + 1]);
@@ -638,6 +692,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
       // no barrier: the next plane's y pass A writes exactly the positions this
       // thread just read (same item partition), and no other thread reads them
     }
+    ++pord;
   }
 }
 
