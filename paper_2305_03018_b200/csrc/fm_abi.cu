@@ -25,6 +25,7 @@
 #include "fm_naive.cuh"
 #include "fm_range.cuh"
 #include "fm_tile.cuh"
+#include "fm_tile128.cuh"
 #include "fm_tonal.cuh"
 
 using namespace fm;
@@ -114,22 +115,40 @@ cudaError_t set_smem_attr(size_t smem) {
                               (int)(smem - fa.sharedSizeBytes));
 }
 
+template <bool SPEC>
+void launch_tile128(dim3 grid, size_t smem, cudaStream_t s, const TileArgs& a) {
+  tile128_kernel<SPEC><<<grid, T128::NT, smem, s>>>(a);
+}
+template <bool SPEC>
+cudaError_t set_smem_attr128(size_t smem) {
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, tile128_kernel<SPEC>);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(tile128_kernel<SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(smem - fa.sharedSizeBytes));
+}
+
 struct Variant {
   int two_d, py, px, nt;
   int smem_fixed;
   tile_launch_fn conv, spec;
   cudaError_t (*attr_conv)(size_t);
   cudaError_t (*attr_spec)(size_t);
+  int tmax;   // largest global tonal length the variant encodes (uint8 indices: 254)
 };
 
 #define FM_VARIANT(TD, PY, PX, NT)                                                        \
   Variant {                                                                               \
     TD, PY, PX, NT, TileCfg<PY, PX, NT, TD>::kSmemTotal, &launch_tile<PY, PX, NT, TD, false>, \
         &launch_tile<PY, PX, NT, TD, true>, &set_smem_attr<PY, PX, NT, TD, false>,          \
-        &set_smem_attr<PY, PX, NT, TD, true>                                                \
+        &set_smem_attr<PY, PX, NT, TD, true>, 1 << 30                                       \
   }
 
+// the three-pass 128x128 kernel (fm_tile128.cuh) comes first: at equal cost
+// the plan takes it whenever the tonal length fits its uint8 indices
 const Variant kVariants[] = {
+    Variant{true, 128, 128, T128::NT, T128::kSmemTotal, &launch_tile128<false>, &launch_tile128<true>,
+            &set_smem_attr128<false>, &set_smem_attr128<true>, T128::kTMax},
     FM_VARIANT(true, 16, 16, 32),   FM_VARIANT(true, 32, 32, 64),   FM_VARIANT(true, 64, 64, 256),
     FM_VARIANT(true, 128, 128, 512), FM_VARIANT(false, 32, 16, 64),  FM_VARIANT(false, 32, 32, 64),
     FM_VARIANT(false, 32, 64, 128),  FM_VARIANT(false, 32, 128, 128), FM_VARIANT(false, 32, 256, 256),
@@ -539,8 +558,12 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   // tile choice: minimise tiles * P^2 * (log2 P^2 + 2) over the built variants
   double best = 1e300;
   const Variant* bv = nullptr;
+  // FM_TILE3=0 disables the three-pass 128x128 kernel (A/B measurements)
+  const char* t3env = std::getenv("FM_TILE3");
+  const bool allow_t3 = !(t3env && t3env[0] == '0');
   for (const Variant& v : kVariants) {
     if ((bool)v.two_d != p->two_d) continue;
+    if (v.tmax < (1 << 30) && (!allow_t3 || p->T > v.tmax)) continue;
     const int P = v.px;
     if (d.tile > 0 && d.tile != P) continue;
     if (P < p->mx || (p->two_d && P < p->my)) continue;

@@ -252,6 +252,61 @@ __host__ __device__ __forceinline__ void dft16_(float2 (&x)[16]) {
   }
 }
 
+// v * W_32^j (forward) or v * conj(W_32^j), j in [0, 16) compile-time
+template <bool INV>
+__host__ __device__ __forceinline__ float2 tw32(float2 v, int j) {
+  if (j == 0) return v;
+  if (j == 8) return INV ? mul_pi(v) : mul_mi(v);
+  if ((j & 1) == 0) return twc<16, INV>(v, j / 2);
+  // cos(2 pi j / 32) for odd j
+  constexpr float c1 = 0.980785280403230449f, c3 = 0.831469612302545237f;
+  constexpr float c5 = 0.555570233019602225f, c7 = 0.195090322016128268f;
+  const int jj = j < 8 ? j : 16 - j;   // cos(2 pi (16 - j)/32) = -cos(2 pi j/32), sin equal
+  const float c0 = jj == 1 ? c1 : jj == 3 ? c3 : jj == 5 ? c5 : c7;
+  const float s0 = jj == 1 ? c7 : jj == 3 ? c5 : jj == 5 ? c3 : c1;   // sin(2 pi jj/32) = cos(2 pi (8-jj)/32)
+  const float c = j < 8 ? c0 : -c0;
+  return cmul(v, make_float2(c, INV ? s0 : -s0));
+}
+
+// 32-point DFT in registers, permuted frequency order (radix-2 DIF step, then two
+// DFT16s): forward takes x[n] natural and leaves X[2r] in x[r], X[2r+1] in
+// x[16+r]; the inverse variant takes that order and returns natural order.
+template <bool INV>
+__host__ __device__ __forceinline__ void dft32p_fwd(float2 (&x)[32]) {
+  float2 lo[16], hi[16];
+#pragma unroll
+  for (int n = 0; n < 16; ++n) {
+    lo[n] = cadd(x[n], x[n + 16]);
+    hi[n] = tw32<INV>(csub(x[n], x[n + 16]), n);
+  }
+  dft16_<INV>(lo);
+  dft16_<INV>(hi);
+#pragma unroll
+  for (int n = 0; n < 16; ++n) {
+    x[n] = lo[n];
+    x[n + 16] = hi[n];
+  }
+}
+template <bool INV>
+__host__ __device__ __forceinline__ void dft32p_inv(float2 (&x)[32]) {
+  float2 lo[16], hi[16];
+#pragma unroll
+  for (int n = 0; n < 16; ++n) {
+    lo[n] = x[n];
+    hi[n] = x[n + 16];
+  }
+  dft16_<INV>(lo);
+  dft16_<INV>(hi);
+#pragma unroll
+  for (int n = 0; n < 16; ++n) {
+    const float2 t = tw32<INV>(hi[n], n);
+    x[n] = cadd(lo[n], t);
+    x[n + 16] = csub(lo[n], t);
+  }
+}
+// frequency held by register r after dft32p_fwd
+__host__ __device__ constexpr int dft32p_freq(int r) { return r < 16 ? 2 * r : 2 * (r - 16) + 1; }
+
 template <int R, bool INV>
 __host__ __device__ __forceinline__ void dft(float2 (&x)[R]) {
   if constexpr (R == 1) {

@@ -166,39 +166,35 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int PY, int PX, int NT, bool TWO_D, bool SPEC>
-__global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
-  using C = TileCfg<PY, PX, NT, TWO_D>;
-  constexpr int RS = C::RS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* buf = reinterpret_cast<float2*>(smem_raw);
-  float4* sbuf = reinterpret_cast<float4*>(smem_raw + C::kBufBytes);
-  uint16_t* tv = reinterpret_cast<uint16_t*>(smem_raw + C::kBufBytes + C::kSpecBytes);
-  const uint32_t* tv32 = reinterpret_cast<const uint32_t*>(tv);
+// One CTA's job: SPEC launches are (unit 0, plane chunk blockIdx.y) of one
+// ladder entry; CONV launches map blockIdx.x to (img, unit, plane chunk) through
+// the range kernel's per-ladder work lists, walked from the longest tonal length
+// down (the longest units start first, so a launch ends without a tail of long
+// stragglers).  Every thread calls it (it contains a CTA barrier); false = no work.
+struct UnitJob {
+  int img, unit, kchunk;
+  int T, K, enc_bias, unit_li;
+  uint32_t magicT;
+  bool skip0;                 // CONV unit whose plane 0 is a known constant (fm_range.cuh "full")
+  const float4* spec_base;    // SE spectrum of the unit's ladder entry
+};
 
-  auto ld2 = [&](int y, int x) -> float4 { return *reinterpret_cast<const float4*>(buf + y * RS + x); };
-  auto st2 = [&](int y, int x, float2 p, float2 q) {
-    *reinterpret_cast<float4*>(buf + y * RS + x) = make_float4(p.x, p.y, q.x, q.y);
-  };
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  int img = 0;
-  // tonal length of this unit: the SPEC launch is per ladder entry; a CONV unit
-  // uses the smallest ladder length that holds its own value range
-  int T = a.T, K = a.K, enc_bias = a.enc_bias;
-  uint32_t magicT = a.magicT;
-  int unit_li = 0;   // ladder entry of a CONV unit
-  bool skip0 = false; // CONV unit whose plane 0 is a known constant (fm_range.cuh "full")
-  const float4* spec_base = a.spec;
-  int unit = a.unit0 + blockIdx.x;   // absolute unit (tile, or group of 1-D tiles)
-  int kchunk_idx = blockIdx.y;        // SPEC: grid y; CONV: from the job list
+template <bool SPEC>
+__device__ __forceinline__ bool decode_job(const TileArgs& a, UnitJob& j) {
+  j.img = 0;
+  j.unit = a.unit0 + blockIdx.x;
+  j.kchunk = blockIdx.y;
+  j.T = a.T;
+  j.K = a.K;
+  j.enc_bias = a.enc_bias;
+  j.magicT = a.magicT;
+  j.unit_li = 0;
+  j.skip0 = false;
+  j.spec_base = a.spec;
   if constexpr (!SPEC) {
-    // job J of this launch -> (img, unit) from the per-ladder work lists, walked
-    // from the longest tonal length down: the longest units start first, so
-    // the launch ends without a tail of long stragglers
+    const int lane = threadIdx.x & 31;
     __shared__ int s_job[3];
-    if (warp == 0) {
+    if (threadIdx.x < 32) {
       int rem = (int)blockIdx.x, found = -1, fch = 1;
       for (int top = a.L - 1; top >= 0 && found < 0; top -= 32) {
         const int li = top - lane;
@@ -233,20 +229,47 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
       }
     }
     __syncthreads();
-    if (s_job[0] < 0) return;
-    img = s_job[0];
-    unit = s_job[1];
-    kchunk_idx = s_job[2];
-    const int4 up = a.unit_param[(size_t)img * a.units + unit];
-    K = up.y + 1;
-    if (kchunk_idx * a.k_chunk >= K) return;   // this k-chunk is beyond the unit's planes
-    T = 2 * up.y;
-    magicT = (uint32_t)(0x100000000ull / (uint64_t)T);
-    unit_li = up.z;
-    skip0 = (up.w & 2) != 0;
-    enc_bias = a.enc_sign > 0 ? -up.x : up.x;
-    spec_base = a.spec + a.spec_off[up.z];
+    if (s_job[0] < 0) return false;
+    j.img = s_job[0];
+    j.unit = s_job[1];
+    j.kchunk = s_job[2];
+    const int4 up = a.unit_param[(size_t)j.img * a.units + j.unit];
+    j.K = up.y + 1;
+    if (j.kchunk * a.k_chunk >= j.K) return false;   // this k-chunk is beyond the unit's planes
+    j.T = 2 * up.y;
+    j.magicT = (uint32_t)(0x100000000ull / (uint64_t)j.T);
+    j.unit_li = up.z;
+    j.skip0 = (up.w & 2) != 0;
+    j.enc_bias = a.enc_sign > 0 ? -up.x : up.x;
+    j.spec_base = a.spec + a.spec_off[up.z];
   }
+  return true;
+}
+
+template <int PY, int PX, int NT, bool TWO_D, bool SPEC>
+__global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
+  using C = TileCfg<PY, PX, NT, TWO_D>;
+  constexpr int RS = C::RS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* buf = reinterpret_cast<float2*>(smem_raw);
+  float4* sbuf = reinterpret_cast<float4*>(smem_raw + C::kBufBytes);
+  uint16_t* tv = reinterpret_cast<uint16_t*>(smem_raw + C::kBufBytes + C::kSpecBytes);
+  const uint32_t* tv32 = reinterpret_cast<const uint32_t*>(tv);
+
+  auto ld2 = [&](int y, int x) -> float4 { return *reinterpret_cast<const float4*>(buf + y * RS + x); };
+  auto st2 = [&](int y, int x, float2 p, float2 q) {
+    *reinterpret_cast<float4*>(buf + y * RS + x) = make_float4(p.x, p.y, q.x, q.y);
+  };
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  UnitJob job;
+  if (!decode_job<SPEC>(a, job)) return;
+  const int img = job.img, unit = job.unit, kchunk_idx = job.kchunk;
+  const int T = job.T, K = job.K, enc_bias = job.enc_bias, unit_li = job.unit_li;
+  const uint32_t magicT = job.magicT;
+  const bool skip0 = job.skip0;
+  const float4* spec_base = job.spec_base;
   // encode table of this unit's T: shared memory when it fits, else global (L1)
   const float2* enc_g = SPEC ? a.enc_tab : a.enc_tab + a.enc_off[unit_li];
   float2* enc_s = reinterpret_cast<float2*>(smem_raw + C::kSmemFixed);

@@ -1,0 +1,351 @@
+// fm_tile128.cuh — three-pass 128x128 overlap-save tile convolution (2-D).
+//
+// Same job as tile_conv_kernel<128,128,512> (fm_tile.cuh: encode the tonal
+// twiddles w_T^{k v(x)} of one tile, forward 2-D FFT, product with the cached
+// SE spectrum, inverse 2-D FFT, store of the overlap-save window), but the
+// 2^14-point 2-D transform runs as THREE shared-memory passes per direction
+// instead of four, with every thread holding 32 points:
+//
+//   F1  y: 32-point DFT over n1 (y = n2 + 4 n1), twiddle W_128^{n2 k1}     thread (x, n2)
+//   F2  y: 4-point DFT over n2 -> k2;  x: 8-point DFT over m1 -> j1
+//       (x = m2 + 16 m1), twiddle W_128^{m2 j1}                             thread (k1, m2)
+//   F3  x: 16-point DFT over m2 -> j2; product; inverse 16-point DFT         thread (k1, k2, j1)
+//   I2  inverse of F2 (conjugate twiddle first)                            thread (k1, m2)
+//   I1  conjugate twiddle, inverse 32-point DFT, store of the window rows   thread (x, n2)
+//
+// so frequency (ky, kx) = (k1 + 32 k2, j1 + 8 j2).  F2 -> F3 -> I2 exchange
+// only data inside the warp's own shared-memory region (warp w owns k1 in
+// {2w, 2w+1}); F1 -> F2 and I2 -> I1 are the two CTA barriers per plane, and
+// I1 -> the next plane's F1 needs none (same thread partition and slots).
+//
+// Shared-memory layouts (float2 slots, per-warp regions of 1088):
+//   B1 (F1/I1 <-> F2/I2): (k1, n2, x) -> (k1>>1)*1088 + ((k1&1)*4 + n2)*128 + x
+//   B2 (F2/I2 <-> F3):    (k1, k2, j1, m2) -> (k1>>1)*1088 + ((k2*2 + (k1&1))*8 + j1)*17 + m2
+// Half-warps read/write 16 consecutive slots (or 16 slots with distinct
+// residues mod 16 through the 17-stride), so every 64-bit access is
+// conflict-free; all per-element offsets are compile-time immediates.
+//
+// Tonal indices are staged as uint8 (T <= kTMax, sentinel T reads the zero
+// entry of the per-plane encode table), which is what frees the room for the
+// padded B2 layout beside the two 32 KB SE-spectrum buffers.
+#pragma once
+#include "fm_tile.cuh"
+
+namespace fm {
+
+struct T128 {
+  static constexpr int P = 128, NT = 512, NW = NT / 32;
+  static constexpr int REG = 1088;                        // per-warp region (float2 slots)
+  static constexpr int kBufBytes = NW * REG * 8;          // 139264
+  static constexpr int kChunkF4 = 4 * NT;                 // 32 KB spectrum chunk: 4 float4 per thread
+  static constexpr uint32_t kChunkBytes = kChunkF4 * 16;
+  static constexpr int kSpecPairs = P * P / 2;            // float4 per tonal plane (4 chunks)
+  static constexpr int kSpecBytes = 2 * kChunkF4 * 16;    // two buffers
+  static constexpr int kTvBytes = P * P;                  // uint8 tonal indices
+  static constexpr int kTwBytes = 8 * 16 * 8;             // W_128^{m2 j1}, [j1][m2]
+  static constexpr int kSmemFixed = kBufBytes + kSpecBytes + kTvBytes + kTwBytes;
+  static constexpr int kEncSlots = (227 * 1024 - kSmemFixed - 256) / 8;   // two per-plane tables
+  static constexpr int kSmemTotal = kSmemFixed + kEncSlots * 8;
+  static constexpr int kTMax = 254;
+  static_assert(2 * (kTMax + 1) <= kEncSlots, "encode tables");
+};
+
+template <bool SPEC>
+__global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
+  using C = T128;
+  constexpr int P = C::P, NT = C::NT, REG = C::REG;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* buf = reinterpret_cast<float2*>(smem_raw);
+  float4* sbuf = reinterpret_cast<float4*>(smem_raw + C::kBufBytes);
+  uint8_t* tv = smem_raw + C::kBufBytes + C::kSpecBytes;
+  float2* twt = reinterpret_cast<float2*>(smem_raw + C::kBufBytes + C::kSpecBytes + C::kTvBytes);
+  float2* enc_s = twt + 128;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  UnitJob job;
+  if (!decode_job<SPEC>(a, job)) return;
+  const int img = job.img, unit = job.unit, kchunk_idx = job.kchunk;
+  const int T = job.T, K = job.K, enc_bias = job.enc_bias;
+  const bool skip0 = job.skip0;
+  const float4* spec_base = job.spec_base;
+  const float2* enc_g = SPEC ? a.enc_tab : a.enc_tab + a.enc_off[job.unit_li];
+  // per-plane encode tables M_k[t] = w_T^{(k t) mod T}, M_k[T] = 0 (double-buffered)
+  auto build_mtab = [&](int kk) {
+    float2* M = enc_s + (kk & 1) * (T + 1);
+    for (int j = tid; j <= T; j += NT) M[j] = j < T ? enc_g[(kk * j) % T] : make_float2(0.f, 0.f);
+  };
+
+  const int ty = SPEC ? 0 : unit / a.tiles_x;
+  const int tx = SPEC ? 0 : unit - ty * a.tiles_x;
+  // ---- stage the tile's tonal indices (sentinel T = no entry)
+  {
+    int bad = 0;
+    if constexpr (SPEC) {
+      for (int p = tid; p < P * P; p += NT) {
+        const int py = p / P, px = p - (p / P) * P;
+        int t = T;
+        if (py < a.my && px < a.mx) {
+          const int si = py * a.mx + px;
+          // ladder entries shorter than the SE's own range are never used by a
+          // unit; reduce so their (unused) spectra stay finite
+          if (a.se_def == nullptr || a.se_def[si]) t = (a.se_vals[si] + a.enc_bias) % T;
+        }
+        tv[p] = (uint8_t)t;
+      }
+    } else {
+      constexpr int IT = P * P / NT, GB = 16;
+#pragma unroll 1
+      for (int g0 = 0; g0 < IT; g0 += GB) {
+        int raw[GB];
+        bool ok[GB];
+#pragma unroll
+        for (int u = 0; u < GB; ++u) {
+          const int p = tid + (g0 + u) * NT;
+          const int py = p / P, px = p - (p / P) * P;
+          const int iy = ty * a.QY + a.DY + py, ix = tx * a.QX + a.DX + px;
+          ok[u] = iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+          raw[u] = 0;
+          if (ok[u]) {
+            const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
+            raw[u] = load_img(a.img, a.img_dtype, gi);
+            if (a.img_def != nullptr) ok[u] = a.img_def[gi] != 0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < GB; ++u) {
+          int t = T;
+          if (ok[u]) {
+            // values below the unit's clamp level encode as the clamp (fm_range.cuh)
+            const int v = max(a.enc_sign * raw[u] + enc_bias, 0);
+            if (v >= T) bad = 1;
+            else t = v;
+          }
+          tv[tid + (g0 + u) * NT] = (uint8_t)t;
+        }
+      }
+      if (bad) atomicOr(a.err, 1);
+    }
+  }
+  if (tid < 128) twt[tid] = c_tw[TwOff<128>::v + (tid & 15) * (tid >> 4)];
+  const int k_begin = kchunk_idx * a.k_chunk;
+  const int k_first = k_begin + ((skip0 && kchunk_idx == 0) ? 1 : 0);
+  build_mtab(k_first);
+  __shared__ __align__(8) uint64_t s_full[2];   // spectrum buffers: bulk-copy completion
+  __shared__ int s_rel[2];                       // warps that released the buffer
+  __shared__ int s_kend;
+  if (tid == 0) {
+    s_kend = min(K, k_begin + a.k_chunk);
+    if constexpr (!SPEC) {
+      mbar_init(&s_full[0], 1);
+      mbar_init(&s_full[1], 1);
+      s_rel[0] = 0;
+      s_rel[1] = 0;
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (k_first < min(K, k_begin + a.k_chunk)) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          mbar_expect_tx(&s_full[b], C::kChunkBytes);
+          bulk_g2s_nohint(sbuf + b * C::kChunkF4, spec_base + (size_t)k_first * C::kSpecPairs + (size_t)b * C::kChunkF4,
+                          C::kChunkBytes, &s_full[b]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // the plane loop bound lives in shared memory (a register copy would be spilled)
+  const volatile int* kend_s = &s_kend;
+  float2* chat_unit = SPEC ? nullptr : a.chat + ((size_t)img * a.upl + (unit - a.unit0)) * a.K_max * (size_t)a.wpx;
+
+  // thread roles
+  const int f_n2 = warp & 3, f_x = (warp >> 2) * 32 + lane;                // F1 / I1
+  const int hi = lane >> 4, m2 = lane & 15;                                  // F2 / I2 (k1 = 2 warp + hi)
+  float2* const b1_col = buf + f_n2 * P + f_x;                               // F1 / I1 slots
+  float2* const b1_row = buf + warp * REG + hi * 4 * P + m2;                 // F2 reads, I2 writes
+  float2* const b2_row = buf + warp * REG + hi * 8 * 17 + m2;                // F2 writes, I2 reads
+  float2* const b2_grp = buf + warp * REG + (lane & 15) * 17 + hi * 16 * 17; // F3 (+ 32*17 per slot)
+
+  int pord = 0;   // planes done: phase parity of the bulk-copied buffers
+  for (int k = k_begin; k < *kend_s; ++k) {
+    if (k == 0 && skip0) continue;   // plane 0 of a full unit: the tonal pass knows it
+    const float2* Mk = enc_s + (k & 1) * (T + 1);
+
+    // ---------------- F1: encode + y DFT32 + twiddle W^{n2 k1}
+    {
+      float2 v[32];
+#pragma unroll
+      for (int n1 = 0; n1 < 32; ++n1) v[n1] = Mk[tv[(f_n2 + 4 * n1) * P + f_x]];
+      dft32p_fwd<false>(v);
+      if (f_n2 != 0) {
+#pragma unroll
+        for (int r = 1; r < 32; ++r) v[r] = cmul(v[r], c_tw[TwOff<128>::v + f_n2 * dft32p_freq(r)]);
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int k1 = dft32p_freq(r);
+        b1_col[(k1 >> 1) * REG + (k1 & 1) * 4 * P] = v[r];
+      }
+    }
+    __syncthreads();
+    // next plane's table into the other buffer (its last reader, the previous
+    // plane's F1, finished before this barrier)
+    if (k + 1 < *kend_s) build_mtab(k + 1);
+
+    // ---------------- F2: y DFT4 over n2, x DFT8 over m1, twiddle W^{m2 j1}
+    {
+      float2 c[4][8];
+#pragma unroll
+      for (int n2 = 0; n2 < 4; ++n2)
+#pragma unroll
+        for (int m1 = 0; m1 < 8; ++m1) c[n2][m1] = b1_row[n2 * P + 16 * m1];
+      __syncwarp();   // the warp's region is rewritten in the B2 layout below
+#pragma unroll
+      for (int m1 = 0; m1 < 8; ++m1) {
+        float2 t[4] = {c[0][m1], c[1][m1], c[2][m1], c[3][m1]};
+        dft4_<false>(t);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) c[k2][m1] = t[k2];
+      }
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) {
+        dft8_<false>(c[k2]);
+#pragma unroll
+        for (int j1 = 1; j1 < 8; ++j1) c[k2][j1] = cmul(c[k2][j1], twt[j1 * 16 + m2]);
+      }
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2)
+#pragma unroll
+        for (int j1 = 0; j1 < 8; ++j1) b2_row[k2 * 2 * 8 * 17 + j1 * 17] = c[k2][j1];
+    }
+    __syncwarp();
+
+    // ---------------- F3: x DFT16 over m2 (+ product + inverse DFT16)
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      float2* g = b2_grp + s * 32 * 17;
+      float2 u[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) u[q] = g[q];
+      dft16_<false>(u);
+      if constexpr (SPEC) {
+        float4* so = a.spec_out + (size_t)k * C::kSpecPairs;
+        const float sc = a.spec_scale;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 p0 = u[8 * h + 2 * q], p1 = u[8 * h + 2 * q + 1];
+            so[(size_t)((2 * s + h) * 4 + q) * NT + tid] = make_float4(p0.x * sc, p0.y * sc, p1.x * sc, p1.y * sc);
+          }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int ch = 2 * s + h;   // chunk: slot s, frequencies j2 in [8h, 8h+8)
+          if (ch < 2) {
+            mbar_wait(&s_full[ch], (uint32_t)(pord & 1));
+          } else {
+            if (ch == 2) cp_async_wait<1>();
+            else cp_async_wait<0>();
+          }
+          const float4* sp = sbuf + (ch & 1) * C::kChunkF4 + tid;
+          float4 s4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) s4[q] = sp[q * NT];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            u[8 * h + 2 * q] = cmul(u[8 * h + 2 * q], make_float2(s4[q].x, s4[q].y));
+            u[8 * h + 2 * q + 1] = cmul(u[8 * h + 2 * q + 1], make_float2(s4[q].z, s4[q].w));
+          }
+          if (ch < 2) {
+            // this thread's slots of the buffer are free: its part of chunk ch+2
+            const float4* src = spec_base + (size_t)k * C::kSpecPairs + (size_t)(ch + 2) * C::kChunkF4 + tid;
+            float4* dst = sbuf + ch * C::kChunkF4 + tid;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cp_async16(dst + q * NT, src + q * NT);
+            cp_async_commit();
+          } else {
+            // the plane's last chunks: the last warp to release the buffer refills
+            // it with the next plane's chunk (a bulk copy a whole plane ahead)
+            __syncwarp();
+            if (lane == 0) {
+              __threadfence_block();
+              const int b = ch & 1;
+              if (atomicAdd(&s_rel[b], 1) == C::NW - 1) {
+                s_rel[b] = 0;
+                if (k + 1 < *kend_s) {
+                  mbar_expect_tx(&s_full[b], C::kChunkBytes);
+                  bulk_g2s_nohint(sbuf + b * C::kChunkF4,
+                                  spec_base + (size_t)(k + 1) * C::kSpecPairs + (size_t)b * C::kChunkF4,
+                                  C::kChunkBytes, &s_full[b]);
+                }
+              }
+            }
+          }
+        }
+        dft16_<true>(u);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) g[q] = u[q];
+      }
+    }
+    if constexpr (SPEC) continue;
+    __syncwarp();
+
+    // ---------------- I2: conjugate twiddle, inverse x DFT8 over j1, inverse y DFT4 over k2
+    {
+      float2 c[4][8];
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2)
+#pragma unroll
+        for (int j1 = 0; j1 < 8; ++j1) c[k2][j1] = b2_row[k2 * 2 * 8 * 17 + j1 * 17];
+      __syncwarp();   // the warp's region is rewritten in the B1 layout below
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) {
+#pragma unroll
+        for (int j1 = 1; j1 < 8; ++j1) c[k2][j1] = cmulc(c[k2][j1], twt[j1 * 16 + m2]);
+        dft8_<true>(c[k2]);
+      }
+#pragma unroll
+      for (int m1 = 0; m1 < 8; ++m1) {
+        float2 t[4] = {c[0][m1], c[1][m1], c[2][m1], c[3][m1]};
+        dft4_<true>(t);
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) c[n2][m1] = t[n2];
+      }
+#pragma unroll
+      for (int n2 = 0; n2 < 4; ++n2)
+#pragma unroll
+        for (int m1 = 0; m1 < 8; ++m1) b1_row[n2 * P + 16 * m1] = c[n2][m1];
+    }
+    __syncthreads();
+
+    // ---------------- I1: conjugate twiddle, inverse y DFT32, store of the window
+    {
+      float2 v[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int k1 = dft32p_freq(r);
+        v[r] = b1_col[(k1 >> 1) * REG + (k1 & 1) * 4 * P];
+      }
+      if (f_n2 != 0) {
+#pragma unroll
+        for (int r = 1; r < 32; ++r) v[r] = cmulc(v[r], c_tw[TwOff<128>::v + f_n2 * dft32p_freq(r)]);
+      }
+      dft32p_inv<true>(v);
+      // window pixel (y - (my-1)) * QX + (x - (mx-1)); rows y = n2 + 4 n1
+      const int ox = tx * a.QX + f_x - (a.mx - 1);
+      if (f_x >= a.mx - 1 && ox < a.OW) {
+        const int y_end = min(P, a.OH - ty * a.QY + (a.my - 1));
+        float2* dst = chat_unit + ((ptrdiff_t)k * a.wpx + (ptrdiff_t)(f_n2 - (a.my - 1)) * a.QX + (f_x - (a.mx - 1)));
+#pragma unroll
+        for (int n1 = 0; n1 < 32; ++n1) {
+          const int y = f_n2 + 4 * n1;
+          if (y >= a.my - 1 && y < y_end) dst[(ptrdiff_t)(4 * n1) * a.QX] = v[n1];
+        }
+      }
+      // no barrier: the next plane's F1 writes exactly the slots this thread read
+    }
+    ++pord;
+  }
+}
+
+}  // namespace fm

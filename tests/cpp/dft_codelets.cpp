@@ -20,7 +20,28 @@ template <int R, bool INV> double check() {
   }
   return worst;
 }
+// dft32p_fwd (permuted output order, dft32p_freq) and dft32p_inv (that order in, natural out)
+template <bool INV> double check32() {
+  double worst = 0;
+  for (int trial = 0; trial < 50; ++trial) {
+    float2 x[32], y[32]; std::complex<double> xd[32];
+    for (int i = 0; i < 32; ++i) { float re = std::sin(1.3*i + trial), im = std::cos(0.7*i*i + 2*trial); x[i] = make_float2(re, im); xd[i] = {re, im}; }
+    for (int r = 0; r < 32; ++r) y[r] = x[dft32p_freq(r)];   // input of the inverse in permuted order
+    dft32p_fwd<INV>(x);
+    dft32p_inv<INV>(y);
+    for (int k = 0; k < 32; ++k) {
+      std::complex<double> acc = 0;
+      for (int n = 0; n < 32; ++n) acc += xd[n] * std::polar(1.0, (INV ? 2 : -2) * M_PI * n * k / 32);
+      // forward: register r holds frequency dft32p_freq(r)
+      for (int r = 0; r < 32; ++r)
+        if (dft32p_freq(r) == k) worst = std::max(worst, std::abs(acc - std::complex<double>(x[r].x, x[r].y)));
+      worst = std::max(worst, std::abs(acc - std::complex<double>(y[k].x, y[k].y)));
+    }
+  }
+  return worst;
+}
 int main() {
-  printf("%g %g %g %g %g %g %g %g %g %g\n", check<2, false>(), check<3, false>(), check<4, false>(), check<5, false>(),
-         check<8, false>(), check<16, false>(), check<3, true>(), check<5, true>(), check<8, true>(), check<16, true>());
+  printf("%g %g %g %g %g %g %g %g %g %g %g %g\n", check<2, false>(), check<3, false>(), check<4, false>(), check<5, false>(),
+         check<8, false>(), check<16, false>(), check<3, true>(), check<5, true>(), check<8, true>(), check<16, true>(),
+         check32<false>(), check32<true>());
 }
