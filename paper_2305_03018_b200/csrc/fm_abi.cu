@@ -65,6 +65,13 @@ int ensure_twiddles(int device) {
       tw[offs[s] + j] = make_float2((float)std::cos(ang), (float)std::sin(ang));
     }
   FM_CUDA(cudaMemcpyToSymbol(c_tw, tw.data(), sizeof(float2) * kTwTotal));
+  std::vector<float2> twy(4 * 32);
+  for (int n2 = 0; n2 < 4; ++n2)
+    for (int k1 = 0; k1 < 32; ++k1) {
+      const double ang = -2.0 * kPi * (n2 * k1) / 128.0;
+      twy[n2 * 32 + k1] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+    }
+  FM_CUDA(cudaMemcpyToSymbol(c_twy, twy.data(), sizeof(float2) * twy.size()));
   std::vector<float2> tt(kTonalTabTotal);
   for (int i = 0; i < kTonalCount; ++i) {
     const int n = kTonalNs[i], off = tonal_off(n);

@@ -50,6 +50,10 @@ struct T128 {
   static_assert(2 * (kTMax + 1) <= kEncSlots, "encode tables");
 };
 
+// F1/I1 twiddles W_128^{n2 k1} laid out [n2][k1]: the warp-uniform n2 row plus
+// a compile-time k1 offset is one uniform constant load per element
+__constant__ float2 c_twy[4 * 32];
+
 template <bool SPEC>
 __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
   using C = T128;
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
       dft32p_fwd<false>(v);
       if (f_n2 != 0) {
 #pragma unroll
-        for (int r = 1; r < 32; ++r) v[r] = cmul(v[r], c_tw[TwOff<128>::v + f_n2 * dft32p_freq(r)]);
+        for (int r = 1; r < 32; ++r) v[r] = cmul(v[r], c_twy[f_n2 * 32 + dft32p_freq(r)]);
       }
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
@@ -328,18 +332,26 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
       }
       if (f_n2 != 0) {
 #pragma unroll
-        for (int r = 1; r < 32; ++r) v[r] = cmulc(v[r], c_tw[TwOff<128>::v + f_n2 * dft32p_freq(r)]);
+        for (int r = 1; r < 32; ++r) v[r] = cmulc(v[r], c_twy[f_n2 * 32 + dft32p_freq(r)]);
       }
       dft32p_inv<true>(v);
-      // window pixel (y - (my-1)) * QX + (x - (mx-1)); rows y = n2 + 4 n1
+      // window pixel (y - (my-1)) * QX + (x - (mx-1)); rows y = n2 + 4 n1 in
+      // [my-1, y_end) are stored: a per-thread row mask (bit n1) and a running
+      // pointer keep the unrolled store loop at one predicate test and one
+      // 64-bit add per row
       const int ox = tx * a.QX + f_x - (a.mx - 1);
       if (f_x >= a.mx - 1 && ox < a.OW) {
         const int y_end = min(P, a.OH - ty * a.QY + (a.my - 1));
+        const int lo = (max(0, a.my - 1 - f_n2) + 3) >> 2;
+        const int hi = min(32, (max(0, y_end - f_n2) + 3) >> 2);
+        const uint32_t below_hi = hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u);
+        const uint32_t rows = hi > lo ? below_hi & ~((1u << lo) - 1u) : 0u;
         float2* dst = chat_unit + ((ptrdiff_t)k * a.wpx + (ptrdiff_t)(f_n2 - (a.my - 1)) * a.QX + (f_x - (a.mx - 1)));
+        const int step = 4 * a.QX;
 #pragma unroll
         for (int n1 = 0; n1 < 32; ++n1) {
-          const int y = f_n2 + 4 * n1;
-          if (y >= a.my - 1 && y < y_end) dst[(ptrdiff_t)(4 * n1) * a.QX] = v[n1];
+          if ((rows >> n1) & 1u) *dst = v[n1];
+          dst += step;
         }
       }
       // no barrier: the next plane's F1 writes exactly the slots this thread read
