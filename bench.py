@@ -289,7 +289,8 @@ def run_ours(args, rank, world, local_rank):
     info = plan.info
     traffic, traffic_src = _ncu_traffic(info["images_per_launch"])
     fpp = 2.0 * 5.0 * 128 * 128 * math.log2(128 * 128) + 6.0 * 128 * 128
-    mean_planes = tim["conv_flops"] / fpp / (441 * args.images * args.steps) if tim["conv_flops"] else None
+    tiles = info["tiles_y"] * info["tiles_x"]
+    mean_planes = tim["conv_flops"] / fpp / (tiles * args.images * args.steps) if tim["conv_flops"] else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -298,11 +299,12 @@ def run_ours(args, rank, world, local_rank):
                                "[0,15], exact dilation, sharded by image",
                    "images": args.images, "images_per_gpu": nloc, "tonal_len": info["tonal_len"],
                    "planes_max": info["planes"], "mean_planes_per_tile": mean_planes,
-                   "tile": [info["tile_y"], info["tile_x"]],
+                   "tile": [info["tile_y"], info["tile_x"]], "tiles_per_image": tiles,
+                   "window": [info["valid_y"], info["valid_x"]],
                    "images_per_launch": info["images_per_launch"],
                    "l2": "no flush: inputs 256 MiB and the spectral volume (~0.7 GB/image at "
                          f"{(mean_planes or 0):.1f} planes/tile) exceed the 126 MB L2"},
-        "roofline": {"bound": "hbm", "kernel": "tile_conv_kernel (encode + 2-D FFT conv, fm_tile.cuh)",
+        "roofline": {"bound": "hbm", "kernel": "tile128_kernel (encode + three-pass 2-D FFT conv, fm_tile128.cuh)",
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_note,
                      "bytes_per_launch": conv_bytes, "ms_per_launch": conv_s * 1000.0,

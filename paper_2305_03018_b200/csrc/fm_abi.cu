@@ -604,6 +604,14 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   p->PY = p->big ? kBig : bv->py;
   p->PX = p->big ? kBig : bv->px;
   p->QX = p->PX - p->mx + 1;
+  // three-pass 128 kernel: its inverse y pass runs one warp per 32 window
+  // columns; a window a few columns past a multiple of 32 is trimmed to it
+  // (c5: 98 -> 96, 2% more tiles, a quarter of that pass saved)
+  {
+    const char* tq = std::getenv("FM_TRIM_QX");   // A/B switch: FM_TRIM_QX=0 keeps the full window
+    const bool trim = !(tq && tq[0] == '0');
+    if (trim && bv && bv->tmax < (1 << 30) && p->QX > 32 && p->QX % 32 != 0 && p->QX % 32 <= 4) p->QX -= p->QX % 32;
+  }
   p->QY = p->two_d ? p->PY - p->my + 1 : 1;
   p->tiles_x = (int)((p->OW + p->QX - 1) / p->QX);
   p->tiles_y = p->two_d ? (int)((p->OH + p->QY - 1) / p->QY) : 1;

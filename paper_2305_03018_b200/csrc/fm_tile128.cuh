@@ -162,7 +162,11 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
   float2* chat_unit = SPEC ? nullptr : a.chat + ((size_t)img * a.upl + (unit - a.unit0)) * a.K_max * (size_t)a.wpx;
 
   // thread roles
-  const int f_n2 = warp & 3, f_x = (warp >> 2) * 32 + lane;                // F1 / I1
+  // F1 / I1: column x = (c + mx - 1) mod 128 for c = 32 (warp>>2) + lane, so the
+  // window columns c < QX come first and a warp with 32 (warp>>2) >= QX has no
+  // output column (the plan trims QX to a multiple of 32 when that idles a warp)
+  const int f_n2 = warp & 3, f_c = (warp >> 2) * 32 + lane, f_x = (f_c + a.mx - 1) & (P - 1);
+  const bool i1_idle = (warp >> 2) * 32 >= a.QX;
   const int hi = lane >> 4, m2 = lane & 15;                                  // F2 / I2 (k1 = 2 warp + hi)
   float2* const b1_col = buf + f_n2 * P + f_x;                               // F1 / I1 slots
   float2* const b1_row = buf + warp * REG + hi * 4 * P + m2;                 // F2 reads, I2 writes
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
     __syncthreads();
 
     // ---------------- I1: conjugate twiddle, inverse y DFT32, store of the window
-    {
+    if (!i1_idle) {
       float2 v[32];
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
@@ -339,14 +343,14 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
       // [my-1, y_end) are stored: a per-thread row mask (bit n1) and a running
       // pointer keep the unrolled store loop at one predicate test and one
       // 64-bit add per row
-      const int ox = tx * a.QX + f_x - (a.mx - 1);
-      if (f_x >= a.mx - 1 && ox < a.OW) {
+      const int ox = tx * a.QX + f_c;
+      if (f_c < a.QX && ox < a.OW) {
         const int y_end = min(P, a.OH - ty * a.QY + (a.my - 1));
         const int lo = (max(0, a.my - 1 - f_n2) + 3) >> 2;
         const int hi = min(32, (max(0, y_end - f_n2) + 3) >> 2);
         const uint32_t below_hi = hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u);
         const uint32_t rows = hi > lo ? below_hi & ~((1u << lo) - 1u) : 0u;
-        float2* dst = chat_unit + ((ptrdiff_t)k * a.wpx + (ptrdiff_t)(f_n2 - (a.my - 1)) * a.QX + (f_x - (a.mx - 1)));
+        float2* dst = chat_unit + ((ptrdiff_t)k * a.wpx + (ptrdiff_t)(f_n2 - (a.my - 1)) * a.QX + f_c);
         const int step = 4 * a.QX;
 #pragma unroll
         for (int n1 = 0; n1 < 32; ++n1) {
