@@ -165,8 +165,12 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
   // F1 / I1: column x = (c + mx - 1) mod 128 for c = 32 (warp>>2) + lane, so the
   // window columns c < QX come first and a warp with 32 (warp>>2) >= QX has no
   // output column (the plan trims QX to a multiple of 32 when that idles a warp)
-  const int f_n2 = warp & 3, f_c = (warp >> 2) * 32 + lane, f_x = (f_c + a.mx - 1) & (P - 1);
-  const bool i1_idle = (warp >> 2) * 32 >= a.QX;
+  // Warps w = s + 4j share scheduler s: (n2, column block) = (j, (j + s) mod 4) is
+  // a Latin square, so every scheduler gets one warp of each n2 (n2 = 0 skips
+  // the twiddles) and one of each column block (the idle inverse-y block)
+  const int f_n2 = warp >> 2, f_xb = ((warp >> 2) + (warp & 3)) & 3;
+  const int f_c = f_xb * 32 + lane, f_x = (f_c + a.mx - 1) & (P - 1);
+  const bool i1_idle = f_xb * 32 >= a.QX;
   const int hi = lane >> 4, m2 = lane & 15;                                  // F2 / I2 (k1 = 2 warp + hi)
   float2* const b1_col = buf + f_n2 * P + f_x;                               // F1 / I1 slots
   float2* const b1_row = buf + warp * REG + hi * 4 * P + m2;                 // F2 reads, I2 writes
@@ -278,7 +282,9 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
             if (lane == 0) {
               __threadfence_block();
               const int b = ch & 1;
-              if (atomicAdd(&s_rel[b], 1) == C::NW - 1) {
+              int prev;
+              asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(prev) : "r"(smem_addr(&s_rel[b])) : "memory");
+              if (prev == C::NW - 1) {
                 s_rel[b] = 0;
                 if (k + 1 < *kend_s) {
                   mbar_expect_tx(&s_full[b], C::kChunkBytes);
