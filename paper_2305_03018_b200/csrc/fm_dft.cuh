@@ -14,33 +14,86 @@ namespace fm {
 // "full" — its plane 0 is a known constant, not computed or stored
 constexpr int kJobFull = 1 << 30;
 
+// Complex primitives.  On sm_100 every one of them is ONE packed f32x2
+// instruction (FADD2 / FMUL2 / FFMA2: same lane throughput as two scalar ops,
+// half the issue slots): a real scale rides as a broadcast operand and the
+// "times +-i" swizzle + sign as operand modifiers, so a complex multiply is
+// FMUL2 + FFMA2.  The host path (codelet tests) computes the same formulas.
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
-// sm_100: complex add/sub as one packed FADD2 (f32x2): half the issue slots
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long r) {
+  float a, b;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+  return make_float2(a, b);
+}
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) {
   unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<unsigned long long*>(&a)),
-      "l"(*reinterpret_cast<unsigned long long*>(&b)));
-  return *reinterpret_cast<float2*>(&r);
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return upk2(r);
 }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) {
   unsigned long long r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<unsigned long long*>(&a)),
-      "l"(*reinterpret_cast<unsigned long long*>(&b)));
-  return *reinterpret_cast<float2*>(&r);
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return upk2(r);
+}
+// a + i b,  a - i b
+__device__ __forceinline__ float2 cadd_i(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(-b.y, b.x)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 csub_i(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(b.y, -b.x)));
+  return upk2(r);
+}
+// s a
+__device__ __forceinline__ float2 cscale(float2 a, float s) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(s, s)));
+  return upk2(r);
+}
+// s a + c
+__device__ __forceinline__ float2 cfma(float s, float2 a, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a.x, a.y)), "l"(pk2(s, s)), "l"(pk2(c.x, c.y)));
+  return upk2(r);
+}
+// s (i a) + c,  s (-i a) + c
+__device__ __forceinline__ float2 cfma_i(float s, float2 a, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(-a.y, a.x)), "l"(pk2(s, s)), "l"(pk2(c.x, c.y)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 cfma_mi(float s, float2 a, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a.y, -a.x)), "l"(pk2(s, s)), "l"(pk2(c.x, c.y)));
+  return upk2(r);
 }
 #else
 __host__ __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __host__ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-#endif
+__host__ __device__ __forceinline__ float2 cadd_i(float2 a, float2 b) { return make_float2(a.x - b.y, a.y + b.x); }
+__host__ __device__ __forceinline__ float2 csub_i(float2 a, float2 b) { return make_float2(a.x + b.y, a.y - b.x); }
 __host__ __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
-// a * b
-__host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+__host__ __device__ __forceinline__ float2 cfma(float s, float2 a, float2 c) {
+  return make_float2(fmaf(s, a.x, c.x), fmaf(s, a.y, c.y));
 }
-// a * conj(b)
-__host__ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+__host__ __device__ __forceinline__ float2 cfma_i(float s, float2 a, float2 c) {
+  return make_float2(fmaf(s, -a.y, c.x), fmaf(s, a.x, c.y));
 }
+__host__ __device__ __forceinline__ float2 cfma_mi(float s, float2 a, float2 c) {
+  return make_float2(fmaf(s, a.y, c.x), fmaf(s, -a.x, c.y));
+}
+#endif
+// a * b = b.x a + b.y (i a)
+__host__ __device__ __forceinline__ float2 cmul(float2 a, float2 b) { return cfma_i(b.y, a, cscale(a, b.x)); }
+// a * conj(b) = b.x a + b.y (-i a)
+__host__ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) { return cfma_mi(b.y, a, cscale(a, b.x)); }
 __host__ __device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }  // a * (-i)
 __host__ __device__ __forceinline__ float2 mul_pi(float2 a) { return make_float2(-a.y, a.x); }  // a * (+i)
 __host__ __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
@@ -95,11 +148,10 @@ template <bool INV>
 __host__ __device__ __forceinline__ void dft4_(float2 (&x)[4]) {
   const float2 t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]);
   const float2 t2 = cadd(x[1], x[3]), t3 = csub(x[1], x[3]);
-  const float2 r = INV ? mul_pi(t3) : mul_mi(t3);
   x[0] = cadd(t0, t2);
   x[2] = csub(t0, t2);
-  x[1] = cadd(t1, r);
-  x[3] = csub(t1, r);
+  x[1] = INV ? cadd_i(t1, t3) : csub_i(t1, t3);
+  x[3] = INV ? csub_i(t1, t3) : cadd_i(t1, t3);
 }
 
 // R = A*B four-step in registers, natural input and output order:
@@ -132,13 +184,12 @@ template <bool INV>
 __host__ __device__ __forceinline__ void dft3_(float2 (&x)[3]) {
   const float s3 = 0.866025403784438647f;  // sin(2*pi/3)
   const float2 t1 = cadd(x[1], x[2]);
-  const float2 t2 = make_float2(fmaf(-0.5f, t1.x, x[0].x), fmaf(-0.5f, t1.y, x[0].y));
+  const float2 t2 = cfma(-0.5f, t1, x[0]);
   const float2 d = csub(x[1], x[2]);
-  const float2 t3 = make_float2(s3 * d.x, s3 * d.y);
-  const float2 r = INV ? mul_pi(t3) : mul_mi(t3);
   x[0] = cadd(x[0], t1);
-  x[1] = cadd(t2, r);
-  x[2] = csub(t2, r);
+  // t2 +- s3 (i d) (inverse), t2 -+ s3 (i d) (forward)
+  x[1] = INV ? cfma_i(s3, d, t2) : cfma_mi(s3, d, t2);
+  x[2] = INV ? cfma_mi(s3, d, t2) : cfma_i(s3, d, t2);
 }
 
 template <bool INV>
@@ -150,17 +201,16 @@ __host__ __device__ __forceinline__ void dft5_(float2 (&x)[5]) {
   const float2 t1 = cadd(x[1], x[4]), t2 = cadd(x[2], x[3]);
   const float2 t3 = csub(x[1], x[4]), t4 = csub(x[2], x[3]);
   const float2 x0 = x[0];
-  const float2 a1 = make_float2(x0.x + c1 * t1.x + c2 * t2.x, x0.y + c1 * t1.y + c2 * t2.y);
-  const float2 a2 = make_float2(x0.x + c2 * t1.x + c1 * t2.x, x0.y + c2 * t1.y + c1 * t2.y);
-  const float2 b1 = make_float2(s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y);
-  const float2 b2 = make_float2(s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y);
-  const float2 r1 = INV ? mul_pi(b1) : mul_mi(b1);
-  const float2 r2 = INV ? mul_pi(b2) : mul_mi(b2);
-  x[0] = make_float2(x0.x + t1.x + t2.x, x0.y + t1.y + t2.y);
-  x[1] = cadd(a1, r1);
-  x[4] = csub(a1, r1);
-  x[2] = cadd(a2, r2);
-  x[3] = csub(a2, r2);
+  const float2 a1 = cfma(c2, t2, cfma(c1, t1, x0));
+  const float2 a2 = cfma(c1, t2, cfma(c2, t1, x0));
+  const float2 b1 = cfma(s2, t4, cscale(t3, s1));
+  const float2 b2 = cfma(-s1, t4, cscale(t3, s2));
+  x[0] = cadd(x0, cadd(t1, t2));
+  // a +- i b (inverse), a -+ i b (forward)
+  x[1] = INV ? cadd_i(a1, b1) : csub_i(a1, b1);
+  x[4] = INV ? csub_i(a1, b1) : cadd_i(a1, b1);
+  x[2] = INV ? cadd_i(a2, b2) : csub_i(a2, b2);
+  x[3] = INV ? csub_i(a2, b2) : cadd_i(a2, b2);
 }
 
 // ---------------------------------------------------------------------------
@@ -180,16 +230,16 @@ __host__ __device__ __forceinline__ void bfly4_w8(float2 a0, float2 a1, float2 a
   constexpr float h = 0.707106781186547524f;
   constexpr float sg = INV ? 1.0f : -1.0f;
   // b2 = sigma*i*a2: S = a0 + b2, D = a0 - b2
-  const float2 S = make_float2(a0.x - sg * a2.y, a0.y + sg * a2.x);
-  const float2 D = make_float2(a0.x + sg * a2.y, a0.y - sg * a2.x);
+  const float2 S = INV ? cadd_i(a0, a2) : csub_i(a0, a2);
+  const float2 D = INV ? csub_i(a0, a2) : cadd_i(a0, a2);
   // b1 + b3 = h P', b1 - b3 = h Q'  (b1 = W^2 a1, b3 = W^6 a3)
   const float2 d = csub(a1, a3), e = cadd(a1, a3);
-  const float2 P = make_float2(d.x - sg * e.y, d.y + sg * e.x);
-  const float2 Q = make_float2(e.x - sg * d.y, e.y + sg * d.x);
-  X0 = make_float2(fmaf(h, P.x, S.x), fmaf(h, P.y, S.y));
-  X2 = make_float2(fmaf(-h, P.x, S.x), fmaf(-h, P.y, S.y));
-  X1 = make_float2(fmaf(-sg * h, Q.y, D.x), fmaf(sg * h, Q.x, D.y));
-  X3 = make_float2(fmaf(sg * h, Q.y, D.x), fmaf(-sg * h, Q.x, D.y));
+  const float2 P = INV ? cadd_i(d, e) : csub_i(d, e);
+  const float2 Q = INV ? cadd_i(e, d) : csub_i(e, d);
+  X0 = cfma(h, P, S);
+  X2 = cfma(-h, P, S);
+  X1 = cfma_i(sg * h, Q, D);
+  X3 = cfma_i(-sg * h, Q, D);
 }
 
 template <bool INV>
@@ -238,33 +288,33 @@ __host__ __device__ __forceinline__ void dft16_(float2 (&x)[16]) {
   {
     const float2 a0 = a[0][1], a1 = a[1][1], a2 = a[2][1], a3 = a[3][1];
     // b2 = W^2 a2 = h (a2.x - s a2.y, a2.y + s a2.x)
-    const float2 A2 = make_float2(a2.x - sg * a2.y, a2.y + sg * a2.x);
-    const float2 S = make_float2(fmaf(h, A2.x, a0.x), fmaf(h, A2.y, a0.y));
-    const float2 D = make_float2(fmaf(-h, A2.x, a0.x), fmaf(-h, A2.y, a0.y));
+    const float2 A2 = INV ? cadd_i(a2, a2) : csub_i(a2, a2);
+    const float2 S = cfma(h, A2, a0);
+    const float2 D = cfma(-h, A2, a0);
     // b1 = W^1 a1 = c1 u, b3 = W^3 a3 = c1 v
-    const float2 u = make_float2(fmaf(-sg * t1, a1.y, a1.x), fmaf(sg * t1, a1.x, a1.y));
-    const float2 v = make_float2(fmaf(t1, a3.x, -sg * a3.y), fmaf(t1, a3.y, sg * a3.x));
+    const float2 u = cfma_i(sg * t1, a1, a1);
+    const float2 v = cfma_i(sg, a3, cscale(a3, t1));
     const float2 p = cadd(u, v), q = csub(u, v);
-    x[1] = make_float2(fmaf(c1, p.x, S.x), fmaf(c1, p.y, S.y));
-    x[9] = make_float2(fmaf(-c1, p.x, S.x), fmaf(-c1, p.y, S.y));
-    x[5] = make_float2(fmaf(-sg * c1, q.y, D.x), fmaf(sg * c1, q.x, D.y));
-    x[13] = make_float2(fmaf(sg * c1, q.y, D.x), fmaf(-sg * c1, q.x, D.y));
+    x[1] = cfma(c1, p, S);
+    x[9] = cfma(-c1, p, S);
+    x[5] = cfma_i(sg * c1, q, D);
+    x[13] = cfma_i(-sg * c1, q, D);
   }
   // k1 = 3: twiddles W^0, W^3, W^6, W^9 (= -W^1)
   {
     const float2 a0 = a[0][3], a1 = a[1][3], a2 = a[2][3], a3 = a[3][3];
-    // b2 = W^6 a2 = h (-a2.x - s a2.y, -a2.y + s a2.x)
-    const float2 A2 = make_float2(-a2.x - sg * a2.y, -a2.y + sg * a2.x);
-    const float2 S = make_float2(fmaf(h, A2.x, a0.x), fmaf(h, A2.y, a0.y));
-    const float2 D = make_float2(fmaf(-h, A2.x, a0.x), fmaf(-h, A2.y, a0.y));
+    // b2 = W^6 a2 = -h (a2 - s i a2) = -h B2
+    const float2 B2 = INV ? csub_i(a2, a2) : cadd_i(a2, a2);
+    const float2 S = cfma(-h, B2, a0);
+    const float2 D = cfma(h, B2, a0);
     // b1 = W^3 a1 = c1 v1, b3 = W^9 a3 = -c1 u3
-    const float2 v1 = make_float2(fmaf(t1, a1.x, -sg * a1.y), fmaf(t1, a1.y, sg * a1.x));
-    const float2 u3 = make_float2(fmaf(-sg * t1, a3.y, a3.x), fmaf(sg * t1, a3.x, a3.y));
+    const float2 v1 = cfma_i(sg, a1, cscale(a1, t1));
+    const float2 u3 = cfma_i(sg * t1, a3, a3);
     const float2 p = csub(v1, u3), q = cadd(v1, u3);
-    x[3] = make_float2(fmaf(c1, p.x, S.x), fmaf(c1, p.y, S.y));
-    x[11] = make_float2(fmaf(-c1, p.x, S.x), fmaf(-c1, p.y, S.y));
-    x[7] = make_float2(fmaf(-sg * c1, q.y, D.x), fmaf(sg * c1, q.x, D.y));
-    x[15] = make_float2(fmaf(sg * c1, q.y, D.x), fmaf(-sg * c1, q.x, D.y));
+    x[3] = cfma(c1, p, S);
+    x[11] = cfma(-c1, p, S);
+    x[7] = cfma_i(sg * c1, q, D);
+    x[15] = cfma_i(-sg * c1, q, D);
   }
 }
 
