@@ -219,9 +219,11 @@ __device__ __forceinline__ int tonal_threshold(const A& res, float& dev) {
 #pragma unroll U
   for (int n = 0; n < N; ++n) {
     const float2 z = res[n];
-    // rint via the 1.5*2^23 magic (round-to-nearest-even, |c| < 2^22): FMA pipe, not XU
-    dev = fmaxf(dev, fabsf(z.x - ((z.x + 12582912.0f) - 12582912.0f)));
-    dev = fmaxf(dev, fabsf(z.y - ((z.y + 12582912.0f) - 12582912.0f)));
+    // rint via the 1.5*2^23 magic (round-to-nearest-even, |c| < 2^22): FMA pipe,
+    // not XU; both counts of the pair at once (packed f32x2 adds)
+    const float2 m = cadd(z, make_float2(12582912.0f, 12582912.0f));
+    const float2 d = csub(z, csub(m, make_float2(12582912.0f, 12582912.0f)));
+    dev = fmaxf(dev, fmaxf(fabsf(d.x), fabsf(d.y)));
     top = z.x > 0.5f ? 2 * n : top;
     top = z.y > 0.5f ? 2 * n + 1 : top;
   }
