@@ -334,6 +334,27 @@ __host__ __device__ __forceinline__ float2 tw32(float2 v, int j) {
   return cmul(v, make_float2(c, INV ? s0 : -s0));
 }
 
+// cos / sin (2 pi j / 128) for a compile-time j in [0, 128): quarter-wave table
+__host__ __device__ constexpr float cos128q(int i) {
+  constexpr float q[33] = {1.000000000000000000f, 0.998795456205172405f, 0.995184726672196929f, 0.989176509964781014f, 0.980785280403230431f, 0.970031253194543974f, 0.956940335732208824f, 0.941544065183020806f, 0.923879532511286738f, 0.903989293123443338f, 0.881921264348355050f, 0.857728610000272118f, 0.831469612302545236f, 0.803207531480644943f, 0.773010453362736993f, 0.740951125354959106f, 0.707106781186547573f, 0.671558954847018330f, 0.634393284163645488f, 0.595699304492433468f, 0.555570233019602289f, 0.514102744193221661f, 0.471396736825997809f, 0.427555093430282196f, 0.382683432365089837f, 0.336889853392220051f, 0.290284677254462331f, 0.242980179903263982f, 0.195090322016128331f, 0.146730474455361748f, 0.098017140329560770f, 0.049067674327418126f, 0.000000000000000061f};
+  return q[i];
+}
+__host__ __device__ constexpr float cos128(int j) {
+  return (j >> 5) == 0 ? cos128q(j & 31) : (j >> 5) == 1 ? -cos128q(32 - (j & 31))
+         : (j >> 5) == 2 ? -cos128q(j & 31) : cos128q(32 - (j & 31));
+}
+__host__ __device__ constexpr float sin128(int j) { return cos128((j + 96) & 127); }   // sin x = cos(x - pi/2)
+// v * W_128^j (forward) or v * conj(W_128^j), j compile-time
+template <bool INV>
+__host__ __device__ __forceinline__ float2 tw128(float2 v, int j) {
+  j &= 127;
+  if (j == 0) return v;
+  if (j == 32) return INV ? mul_pi(v) : mul_mi(v);
+  if (j == 64) return make_float2(-v.x, -v.y);
+  if (j == 96) return INV ? mul_mi(v) : mul_pi(v);
+  return cmul(v, make_float2(cos128(j), INV ? sin128(j) : -sin128(j)));
+}
+
 // 32-point DFT in registers, permuted frequency order (radix-2 DIF step, then two
 // DFT16s): forward takes x[n] natural and leaves X[2r] in x[r], X[2r+1] in
 // x[16+r]; the inverse variant takes that order and returns natural order.

@@ -40,8 +40,21 @@ template <bool INV> double check32() {
   }
   return worst;
 }
+// tw128: v * W_128^j (and conjugate) for every j
+double check_tw128() {
+  double worst = 0;
+  for (int j = 0; j < 128; ++j) {
+    const float2 v = make_float2(0.37f, -1.21f);
+    const std::complex<double> vd(0.37, -1.21);
+    const float2 f = tw128<false>(v, j), b = tw128<true>(v, j);
+    const std::complex<double> wf = vd * std::polar(1.0, -2 * M_PI * j / 128), wb = vd * std::polar(1.0, 2 * M_PI * j / 128);
+    worst = std::max(worst, std::abs(wf - std::complex<double>(f.x, f.y)));
+    worst = std::max(worst, std::abs(wb - std::complex<double>(b.x, b.y)));
+  }
+  return worst;
+}
 int main() {
-  printf("%g %g %g %g %g %g %g %g %g %g %g %g\n", check<2, false>(), check<3, false>(), check<4, false>(), check<5, false>(),
+  printf("%g %g %g %g %g %g %g %g %g %g %g %g %g\n", check<2, false>(), check<3, false>(), check<4, false>(), check<5, false>(),
          check<8, false>(), check<16, false>(), check<3, true>(), check<5, true>(), check<8, true>(), check<16, true>(),
-         check32<false>(), check32<true>());
+         check32<false>(), check32<true>(), check_tw128());
 }
