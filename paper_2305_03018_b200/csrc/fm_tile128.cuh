@@ -182,6 +182,14 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
     if (k == 0 && skip0) continue;   // plane 0 of a full unit: the tonal pass knows it
     const float2* Mk = enc_s + (k & 1) * (T + 1);
 
+    // slot 1's SE spectrum (chunks 2, 3: this thread's 8 float4), L2 -> registers,
+    // in flight through F1, F2 and slot 0 of F3
+    float4 sp1[8];
+    if constexpr (!SPEC) {
+      const float4* src = spec_base + (size_t)k * C::kSpecPairs + (size_t)2 * C::kChunkF4 + tid;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sp1[i] = __ldcg(src + (i >> 2) * C::kChunkF4 + (i & 3) * NT);
+    }
     // ---------------- F1: encode + y DFT32 + twiddle W^{n2 k1}
     {
       float2 v[32];
@@ -253,31 +261,25 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int ch = 2 * s + h;   // chunk: slot s, frequencies j2 in [8h, 8h+8)
+          float4 s4[4];
           if (ch < 2) {
             mbar_wait(&s_full[ch], (uint32_t)(pord & 1));
-          } else {
-            if (ch == 2) cp_async_wait<1>();
-            else cp_async_wait<0>();
-          }
-          const float4* sp = sbuf + (ch & 1) * C::kChunkF4 + tid;
-          float4 s4[4];
+            const float4* sp = sbuf + ch * C::kChunkF4 + tid;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) s4[q] = sp[q * NT];
+            for (int q = 0; q < 4; ++q) s4[q] = sp[q * NT];
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s4[q] = sp1[(ch - 2) * 4 + q];
+          }
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             u[8 * h + 2 * q] = cmul(u[8 * h + 2 * q], make_float2(s4[q].x, s4[q].y));
             u[8 * h + 2 * q + 1] = cmul(u[8 * h + 2 * q + 1], make_float2(s4[q].z, s4[q].w));
           }
           if (ch < 2) {
-            // this thread's slots of the buffer are free: its part of chunk ch+2
-            const float4* src = spec_base + (size_t)k * C::kSpecPairs + (size_t)(ch + 2) * C::kChunkF4 + tid;
-            float4* dst = sbuf + ch * C::kChunkF4 + tid;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) cp_async16(dst + q * NT, src + q * NT);
-            cp_async_commit();
-          } else {
-            // the plane's last chunks: the last warp to release the buffer refills
-            // it with the next plane's chunk (a bulk copy a whole plane ahead)
+            // slot 0's chunks: the last warp to release the buffer refills it with
+            // the next plane's chunk (a bulk copy a whole plane ahead); slot 1's
+            // chunks come straight from L2 into registers (loaded during F2)
             __syncwarp();
             if (lane == 0) {
               __threadfence_block();
