@@ -122,16 +122,16 @@ cudaError_t set_smem_attr(size_t smem) {
                               (int)(smem - fa.sharedSizeBytes));
 }
 
-template <bool SPEC>
+template <typename TV, bool SPEC>
 void launch_tile128(dim3 grid, size_t smem, cudaStream_t s, const TileArgs& a) {
-  tile128_kernel<SPEC><<<grid, T128::NT, smem, s>>>(a);
+  tile128_kernel<TV, SPEC><<<grid, T128<TV>::NT, smem, s>>>(a);
 }
-template <bool SPEC>
+template <typename TV, bool SPEC>
 cudaError_t set_smem_attr128(size_t smem) {
   cudaFuncAttributes fa{};
-  cudaError_t e = cudaFuncGetAttributes(&fa, tile128_kernel<SPEC>);
+  cudaError_t e = cudaFuncGetAttributes(&fa, tile128_kernel<TV, SPEC>);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(tile128_kernel<SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(tile128_kernel<TV, SPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(smem - fa.sharedSizeBytes));
 }
 
@@ -151,11 +151,17 @@ struct Variant {
         &set_smem_attr<PY, PX, NT, TD, true>, 1 << 30                                       \
   }
 
-// the three-pass 128x128 kernel (fm_tile128.cuh) comes first: at equal cost
-// the plan takes it whenever the tonal length fits its uint8 indices
+#define FM_VARIANT128(TV)                                                                              \
+  Variant {                                                                                            \
+    true, 128, 128, T128<TV>::NT, T128<TV>::kSmemTotal, &launch_tile128<TV, false>, &launch_tile128<TV, true>, \
+        &set_smem_attr128<TV, false>, &set_smem_attr128<TV, true>, T128<TV>::kTMax                      \
+  }
+
+// the three-pass 128x128 kernels (fm_tile128.cuh) come first: at equal cost the
+// plan takes the uint8-index one when the tonal length fits it, else the
+// uint16 one, else the four-pass kernel
 const Variant kVariants[] = {
-    Variant{true, 128, 128, T128::NT, T128::kSmemTotal, &launch_tile128<false>, &launch_tile128<true>,
-            &set_smem_attr128<false>, &set_smem_attr128<true>, T128::kTMax},
+    FM_VARIANT128(uint8_t), FM_VARIANT128(uint16_t),
     FM_VARIANT(true, 16, 16, 32),   FM_VARIANT(true, 32, 32, 64),   FM_VARIANT(true, 64, 64, 256),
     FM_VARIANT(true, 128, 128, 512), FM_VARIANT(false, 32, 16, 64),  FM_VARIANT(false, 32, 32, 64),
     FM_VARIANT(false, 32, 64, 128),  FM_VARIANT(false, 32, 128, 128), FM_VARIANT(false, 32, 256, 256),

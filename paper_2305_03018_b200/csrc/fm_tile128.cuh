@@ -25,14 +25,16 @@
 // residues mod 16 through the 17-stride), so every 64-bit access is
 // conflict-free; all per-element offsets are compile-time immediates.
 //
-// Tonal indices are staged as uint8 (T <= kTMax, sentinel T reads the zero
+// Tonal indices are staged as uint8 (T <= 254, sentinel T reads the zero
 // entry of the per-plane encode table), which is what frees the room for the
-// padded B2 layout beside the two 32 KB SE-spectrum buffers.
+// padded B2 layout beside two 32 KB SE-spectrum buffers; longer tonal axes
+// (8-bit data: c3) stage uint16 indices beside one buffer.
 #pragma once
 #include "fm_tile.cuh"
 
 namespace fm {
 
+template <typename TV>
 struct T128 {
   static constexpr int P = 128, NT = 512, NW = NT / 32;
   static constexpr int REG = 1088;                        // per-warp region (float2 slots)
@@ -40,13 +42,17 @@ struct T128 {
   static constexpr int kChunkF4 = 4 * NT;                 // 32 KB spectrum chunk: 4 float4 per thread
   static constexpr uint32_t kChunkBytes = kChunkF4 * 16;
   static constexpr int kSpecPairs = P * P / 2;            // float4 per tonal plane (4 chunks)
-  static constexpr int kSpecBytes = 2 * kChunkF4 * 16;    // two buffers
-  static constexpr int kTvBytes = P * P;                  // uint8 tonal indices
+  // uint8 indices leave room for two spectrum buffers (slot 0's chunks both a
+  // plane ahead); uint16 (long tonal axes) for one: chunk 1 follows chunk 0
+  // through it by per-thread cp.async
+  static constexpr int kNSB = sizeof(TV) == 1 ? 2 : 1;
+  static constexpr int kSpecBytes = kNSB * kChunkF4 * 16;
+  static constexpr int kTvBytes = P * P * (int)sizeof(TV);
   static constexpr int kTwBytes = 8 * 16 * 8;             // W_128^{m2 j1}, [j1][m2]
   static constexpr int kSmemFixed = kBufBytes + kSpecBytes + kTvBytes + kTwBytes;
   static constexpr int kEncSlots = (227 * 1024 - kSmemFixed - 256) / 8;   // two per-plane tables
   static constexpr int kSmemTotal = kSmemFixed + kEncSlots * 8;
-  static constexpr int kTMax = 254;
+  static constexpr int kTMax = sizeof(TV) == 1 ? 254 : (kEncSlots / 2 - 1) & ~1;
   static_assert(2 * (kTMax + 1) <= kEncSlots, "encode tables");
 };
 
@@ -54,14 +60,14 @@ struct T128 {
 // a compile-time k1 offset is one uniform constant load per element
 __constant__ float2 c_twy[4 * 32];
 
-template <bool SPEC>
+template <typename TV, bool SPEC>
 __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
-  using C = T128;
+  using C = T128<TV>;
   constexpr int P = C::P, NT = C::NT, REG = C::REG;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* buf = reinterpret_cast<float2*>(smem_raw);
   float4* sbuf = reinterpret_cast<float4*>(smem_raw + C::kBufBytes);
-  uint8_t* tv = smem_raw + C::kBufBytes + C::kSpecBytes;
+  TV* tv = reinterpret_cast<TV*>(smem_raw + C::kBufBytes + C::kSpecBytes);
   float2* twt = reinterpret_cast<float2*>(smem_raw + C::kBufBytes + C::kSpecBytes + C::kTvBytes);
   float2* enc_s = twt + 128;
 
@@ -95,7 +101,7 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
           // unit; reduce so their (unused) spectra stay finite
           if (a.se_def == nullptr || a.se_def[si]) t = (a.se_vals[si] + a.enc_bias) % T;
         }
-        tv[p] = (uint8_t)t;
+        tv[p] = (TV)t;
       }
     } else {
       constexpr int IT = P * P / NT, GB = 16;
@@ -125,7 +131,7 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
             if (v >= T) bad = 1;
             else t = v;
           }
-          tv[tid + (g0 + u) * NT] = (uint8_t)t;
+          tv[tid + (g0 + u) * NT] = (TV)t;
         }
       }
       if (bad) atomicOr(a.err, 1);
@@ -141,14 +147,14 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
   if (tid == 0) {
     s_kend = min(K, k_begin + a.k_chunk);
     if constexpr (!SPEC) {
-      mbar_init(&s_full[0], 1);
-      mbar_init(&s_full[1], 1);
+#pragma unroll
+      for (int b = 0; b < C::kNSB; ++b) mbar_init(&s_full[b], 1);
       s_rel[0] = 0;
       s_rel[1] = 0;
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       if (k_first < min(K, k_begin + a.k_chunk)) {
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < C::kNSB; ++b) {
           mbar_expect_tx(&s_full[b], C::kChunkBytes);
           bulk_g2s_nohint(sbuf + b * C::kChunkF4, spec_base + (size_t)k_first * C::kSpecPairs + (size_t)b * C::kChunkF4,
                           C::kChunkBytes, &s_full[b]);
@@ -263,8 +269,10 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
           const int ch = 2 * s + h;   // chunk: slot s, frequencies j2 in [8h, 8h+8)
           float4 s4[4];
           if (ch < 2) {
-            mbar_wait(&s_full[ch], (uint32_t)(pord & 1));
-            const float4* sp = sbuf + ch * C::kChunkF4 + tid;
+            const int b = C::kNSB == 2 ? ch : 0;
+            if (C::kNSB == 2 || ch == 0) mbar_wait(&s_full[b], (uint32_t)(pord & 1));
+            else cp_async_wait<0>();
+            const float4* sp = sbuf + b * C::kChunkF4 + tid;
 #pragma unroll
             for (int q = 0; q < 4; ++q) s4[q] = sp[q * NT];
           } else {
@@ -276,14 +284,20 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
             u[8 * h + 2 * q] = cmul(u[8 * h + 2 * q], make_float2(s4[q].x, s4[q].y));
             u[8 * h + 2 * q + 1] = cmul(u[8 * h + 2 * q + 1], make_float2(s4[q].z, s4[q].w));
           }
-          if (ch < 2) {
+          if (C::kNSB == 1 && ch == 0) {
+            // one buffer: this thread's slots of chunk 0 are consumed, its part of chunk 1 follows
+            const float4* src = spec_base + (size_t)k * C::kSpecPairs + (size_t)C::kChunkF4 + tid;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cp_async16(sbuf + tid + q * NT, src + q * NT);
+            cp_async_commit();
+          } else if (ch < 2) {
             // slot 0's chunks: the last warp to release the buffer refills it with
             // the next plane's chunk (a bulk copy a whole plane ahead); slot 1's
-            // chunks come straight from L2 into registers (loaded during F2)
+            // chunks come straight from L2 into registers (loaded at the plane start)
             __syncwarp();
             if (lane == 0) {
               __threadfence_block();
-              const int b = ch & 1;
+              const int b = C::kNSB == 2 ? ch : 0;
               int prev;
               asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(prev) : "r"(smem_addr(&s_rel[b])) : "memory");
               if (prev == C::NW - 1) {
