@@ -215,7 +215,8 @@ __device__ __forceinline__ void stock_run(A& a, A& b) {
 template <int N, class A>
 __device__ __forceinline__ int tonal_threshold(const A& res, float& dev) {
   int top = -1;
-  constexpr int U = IsSmemArr<A>::value ? 4 : N;
+  constexpr bool SMA = IsSmemArr<A>::value;
+  constexpr int U = SMA ? 4 : N;
 #pragma unroll U
   for (int n = 0; n < N; ++n) {
     const float2 z = res[n];
@@ -224,8 +225,19 @@ __device__ __forceinline__ int tonal_threshold(const A& res, float& dev) {
     const float2 m = cadd(z, make_float2(12582912.0f, 12582912.0f));
     const float2 d = csub(z, csub(m, make_float2(12582912.0f, 12582912.0f)));
     dev = fmaxf(dev, fmaxf(fabsf(d.x), fabsf(d.y)));
-    top = z.x > 0.5f ? 2 * n : top;
-    top = z.y > 0.5f ? 2 * n + 1 : top;
+    if constexpr (SMA) {
+      top = z.x > 0.5f ? 2 * n : top;
+      top = z.y > 0.5f ? 2 * n + 1 : top;
+    }
+  }
+  if constexpr (!SMA) {
+    // register spectrum: the highest count > 0.5, searched from the top down
+    // (a warp's pixels are neighbours with close tops, so it exits early)
+#pragma unroll
+    for (int n = N - 1; n >= 0; --n) {
+      if (res[n].y > 0.5f) { top = 2 * n + 1; break; }
+      if (res[n].x > 0.5f) { top = 2 * n; break; }
+    }
   }
   return top;
 }
