@@ -53,6 +53,36 @@ constexpr double kPi = 3.14159265358979323846;
 
 int set_all_smem_attrs();
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  return fn;
+}
+// [rows][wpx] float2 spectral scratch as a 2-D tensor of 8-byte elements; box {bx, by}
+bool encode_chat_map(CUtensorMap* m, void* chat, int64_t wpx, int64_t rows, int bx, int by) {
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn || bx < 1 || by < 1 || bx > 256 || by > 256) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)wpx, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)wpx * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, chat, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int ensure_twiddles(int device) {
   std::lock_guard<std::mutex> lk(g_tw_mu);
   if (device < 64 && (g_tw_init_mask >> device) & 1ull) return FM_OK;
@@ -177,19 +207,21 @@ constexpr bool tonal_sm() { return N > kTonalRegMax; }
 template <int N>
 constexpr int tonal_nt() { return N > kTonalRegMax ? 64 : 128; }
 
+typedef void (*tonal_pipe_launch_fn)(dim3, int, size_t, cudaStream_t, const TonalArgs&, const CUtensorMap*);
 struct TonalVariant {
   int n, nt, smem;
   tonal_launch_fn fn;
   cudaError_t (*attr)();
   // pipelined persistent kernel (register variants): threads, dynamic smem, launcher
   int pipe_nt, pipe_smem;
-  tonal_launch_fn pipe_fn;
+  tonal_pipe_launch_fn pipe_fn;
   cudaError_t (*pipe_attr)(int*);   // sets the smem attribute, returns CTAs per SM
 };
 template <int N>
-void launch_tonal_pipe(dim3 grid, int nt, size_t smem, cudaStream_t s, const TonalArgs& a) {
+void launch_tonal_pipe(dim3 grid, int nt, size_t smem, cudaStream_t s, const TonalArgs& a, const CUtensorMap* tms) {
   if constexpr (N <= kTonalRegMax)
-    tonal_kernel_pipe<N, tonal_pipe_nt<N>(), tonal_pipe_st<N>()><<<grid, tonal_pipe_nt<N>() + 32, smem, s>>>(a);
+    tonal_kernel_pipe<N, tonal_pipe_nt<N>(), tonal_pipe_st<N>()><<<grid, tonal_pipe_nt<N>() + 32, smem, s>>>(a, tms[0],
+                                                                                                             tms[1]);
 }
 template <int N>
 cudaError_t tonal_pipe_attr(int* occ) {
@@ -317,6 +349,9 @@ struct fm_plan {
   std::vector<int> ladder;
   std::vector<int64_t> spec_off;          // float4 offsets into spec
   std::vector<const TonalVariant*> ladder_var;
+  // per ladder entry: 2-D tensor maps of the spectral scratch for the pipelined
+  // tonal kernel (box {pipe_nt pixels, K planes} and {pipe_nt, K-1}); empty: per-plane copies
+  std::vector<CUtensorMap> tmaps;
   int units = 1, wpx = 1, npx = 1, win_y = 1, win_x = 1, unit_step_x = 0;  // wpx: even plane stride
   std::vector<int2> taps;                 // clamp-bound taps of fm_range.cuh, best first
   std::vector<int> full_prefix;           // prefix count of "full" units (window inside the image)
@@ -818,6 +853,20 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     free_plan(p);
     return fail(FM_ENOMEM, std::string("spectral scratch alloc: ") + cudaGetErrorString(e));
   }
+  // FM_TONAL_TMA=0: per-plane bulk copies in the pipelined tonal kernel (A/B)
+  {
+    const char* te = std::getenv("FM_TONAL_TMA");
+    bool ok = !(te && te[0] == '0') && !p->counts;
+    std::vector<CUtensorMap> maps(2 * L);
+    for (int li = 0; li < L && ok; ++li) {
+      const TonalVariant* tv = p->ladder_var[li];
+      const int K = p->ladder[li] + 1;
+      const int bx = tv ? tv->pipe_nt : 128;
+      ok = encode_chat_map(&maps[2 * li], p->chat, p->wpx, slots * p->K, bx, K) &&
+           encode_chat_map(&maps[2 * li + 1], p->chat, p->wpx, slots * p->K, bx, std::max(1, K - 1));
+    }
+    if (ok) p->tmaps = std::move(maps);
+  }
   std::vector<float2> tn(std::max(1, p->N)), wt(std::max(1, p->N));
   for (int j = 0; j < p->N; ++j) {
     const double a1 = 2.0 * kPi * j / p->N, a2 = 2.0 * kPi * j / T;
@@ -1239,7 +1288,9 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         t.njobs = cnt;
         const int64_t items = (int64_t)cnt * ((p->npx + tv->pipe_nt - 1) / tv->pipe_nt);
         const int grid = (int)std::min<int64_t>(items, (int64_t)g_num_sms * std::min(occ, g_tonal_occ_cap));
-        tv->pipe_fn(dim3((unsigned)grid), tv->pipe_nt, tv->pipe_smem, ts, t);
+        static const CUtensorMap kNoMap[2] = {};
+        t.use_tma = p->tmaps.empty() ? 0 : 1;
+        tv->pipe_fn(dim3((unsigned)grid), tv->pipe_nt, tv->pipe_smem, ts, t, t.use_tma ? &p->tmaps[2 * li] : kNoMap);
       } else if (tv) {
         const int nt = tv->nt;
         tv->fn(dim3((unsigned)cnt, (unsigned)((p->npx + nt - 1) / nt)), nt, tv->smem, ts, t);

@@ -2,6 +2,7 @@
 // path) helpers shared by the tile conv kernel (SE-spectrum ring) and the
 // pipelined tonal kernel (spectral-plane ring).
 #pragma once
+#include <cuda.h>           // CUtensorMap (the type only; maps are encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -47,6 +48,16 @@ __device__ __forceinline__ void bulk_g2s_nohint(void* dst, const void* src, uint
                    smem_addr(dst)),
                "l"(src), "r"(bytes), "r"(smem_addr(bar))
                : "memory");
+}
+
+// 2-D tensor tile global -> shared (TMA), completion on an mbarrier, L2 hint
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
 }
 
 }  // namespace fm

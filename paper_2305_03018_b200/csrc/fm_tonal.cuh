@@ -46,6 +46,7 @@ struct TonalArgs {
   // units flagged "full" (unit_param.w bit 1: window inside the image, no gaps)
   // have plane 0 = (defined SE entries) / T everywhere; the conv kernel skips it
   float x0_full;
+  int use_tma;            // pipelined kernel: stages by 2-D tensor copies (maps passed beside the args)
 };
 
 __device__ __forceinline__ void store_out(const TonalArgs& a, size_t i, int v) {
@@ -305,8 +306,14 @@ constexpr int tonal_pipe_smem() { return (N + 1) * tonal_pipe_nt<N>() * 8 * tona
 // NT consumer threads (one pixel each per item) + one producer warp; full[st]
 // completes when the stage's bulk copies land, empty[st] when every consumer
 // warp has read it.
+// With tensor maps (tm: box {NT pixels, K planes}; tm1: {NT, K-1} for units
+// whose plane 0 is known) the producer moves a whole stage with ONE 2-D TMA
+// copy instead of one bulk copy per plane (whose address set-up made the
+// single producer thread the bottleneck); out-of-range pixels of a unit's last
+// block are zero-filled by the TMA unit and never stored.
 template <int N, int NT, int ST>
-__global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a) {
+__global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a, const __grid_constant__ CUtensorMap tm,
+                                                             const __grid_constant__ CUtensorMap tm1) {
   constexpr int K = N + 1;
   constexpr int off = tonal_off(N);
   constexpr int NCW = NT / 32;
@@ -339,10 +346,17 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a) 
         if (item_next < items) job_next = a.list[item_next / bpj];
         if (i >= ST) mbar_wait(&empty[st], (uint32_t)(((i / ST) - 1) & 1));
         const int j = item / bpj, blk = item - j * bpj;
+        const int k0 = (job.y & kJobFull) ? 1 : 0;   // plane 0 known (not copied)
+        if (a.use_tma) {
+          stage_k0[st] = k0;   // published to the consumers by the arrive below
+          mbar_expect_tx(&full[st], (uint32_t)(NT * 8 * (K - k0)));
+          const int row = ((job.x * a.upl + ((job.y & ~kJobFull) - a.unit0)) * a.K_max) + k0;
+          tma_load_2d(tstg + (size_t)st * K * NT + k0 * NT, k0 ? &tm1 : &tm, blk * NT, row, &full[st], pol);
+          continue;
+        }
         const float2* src = a.chat + ((size_t)job.x * a.upl + ((job.y & ~kJobFull) - a.unit0)) * a.K_max * (size_t)a.wpx +
                             (size_t)blk * NT;
         const uint32_t bytes = (uint32_t)min(NT, a.wpx - blk * NT) * 8u;
-        const int k0 = (job.y & kJobFull) ? 1 : 0;   // plane 0 known (not copied)
         stage_k0[st] = k0;   // published to the consumers by the arrive below
         mbar_expect_tx(&full[st], bytes * (K - k0));
         float2* dst = tstg + (size_t)st * K * NT;
