@@ -58,3 +58,25 @@ def test_tile128_vs_oracle(mx, variant):
                                        erode=(mode == "erode"), crop=crop, fill=fill)
             assert np.array_equal(valid[i], rvalid.astype(bool)), (mode, crop, i)
             assert np.array_equal(out[i].astype(np.int64), ref.astype(np.int64)), (mode, crop, i)
+
+
+@pytest.mark.parametrize("env", ["FM_TONAL_TMA=0", "FM_TRIM_QX=0", "FM_TILE3=0"])
+def test_alternate_paths_bit_exact(env, monkeypatch):
+    """Every plan-time A/B switch keeps the result bit-exact: per-plane bulk copies
+    instead of 2-D tensor copies in the tonal kernel, the untrimmed window, the
+    four-pass tile kernel."""
+    import torch
+    from paper_2305_03018_b200.engine import MorphPlan
+    name, val = env.split("=")
+    monkeypatch.setenv(name, val)
+    rng = np.random.default_rng(2305)
+    img = _smooth(rng, (300, 280), 64)
+    se = rng.integers(0, 16, (31, 31))
+    for mode in ("dilate", "erode"):
+        fill = 0 if mode == "dilate" else 63
+        plan = MorphPlan(shape=img.shape, se_values=se, se_lo=(-15, -15), mode=mode, img_dtype=torch.uint8,
+                         img_min=0, img_max=63, fill=fill, batch=1)
+        out, valid = plan.execute(torch.from_numpy(img.astype(np.uint8)[None]).cuda())
+        ref, rvalid = cnaive.naive(img, None, se, None, (-15, -15), erode=(mode == "erode"), fill=fill)
+        assert np.array_equal(out[0].cpu().numpy().astype(np.int64), ref.astype(np.int64)), (env, mode)
+        assert np.array_equal(valid[0].cpu().numpy().astype(bool), rvalid.astype(bool)), (env, mode)
