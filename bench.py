@@ -68,6 +68,17 @@ def _ncu_traffic(images_per_launch):
     return None, None, None
 
 
+def method_floor(mpx_s, hbm_gbs):
+    """SURVEY §8(d) B_alg/px = [|F| (s_in + 4) + 8 V] / |F|, V = S_lin (l_R + 1), for the c5
+    workload (l_R = 63 + 15, full-mode S_lin = (2048 + 30)^2, uint8 in, int32 out), and the
+    path's fraction of HBM at that algorithmic traffic."""
+    f = EDGE * EDGE
+    v = (EDGE + 30) ** 2 * (63 + 15 + 1)
+    b_alg = (f * (1 + 4) + 8.0 * v) / f
+    achieved = b_alg * mpx_s * 1e6 / 1e9
+    return {"bytes_per_px": b_alg, "achieved_gbs": achieved, "peak_gbs": hbm_gbs, "frac": achieved / hbm_gbs}
+
+
 def _gen(i):
     from paper_2305_03018_b200 import workloads as W
     return W.c5_image(i)
@@ -325,7 +336,10 @@ def run_ours(args, rank, world, local_rank):
                      # the range kernels run one launch chunk ahead on a low-priority stream
                      # (overlapping the conv tail / tonal kernels): their event span is not a
                      # share of the step
-                     "share_of_step": {"conv": tim["conv_ms"] / max(ms, 1e-9), "tonal": tim["tonal_ms"] / max(ms, 1e-9)}},
+                     "share_of_step": {"conv": tim["conv_ms"] / max(ms, 1e-9), "tonal": tim["tonal_ms"] / max(ms, 1e-9)},
+                     # the whole path against the method's HBM floor (spectral volume of
+                     # minimal extent S_lin x (l_R + 1) written once and read once, plus the image I/O)
+                     "method_floor": method_floor(value, hbm)},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(imgs.nbytes),
                 "d2h_bytes_per_step": int(pin_out.numel() * pin_out.element_size() + pin_valid.numel())},
         "gpu_launches": int(launches),
