@@ -134,3 +134,37 @@ def test_umulhi_division_magic():
         magic = np.uint64(((1 << 32) + d - 1) // d)
         q = (p * magic) >> np.uint64(32)
         assert np.array_equal(q, p // np.uint64(d)), d
+
+
+def test_reference_file_formats_interoperate(tmp_path):
+    """SURVEY 8(f) row 3 (data formats either side of the path): the reference's own
+    PGM / SE readers and writers (pgmio.py:62-183) exchange grids with the drop-in
+    without conversion — reference grids are accepted as inputs (duck typing) and the
+    drop-in's grids are written by the reference writers.  Skipped where the
+    reference is absent (the GPU box)."""
+    import sys
+    ref_src = "/root/reference/pkg/src"
+    import os
+    if not os.path.isdir(ref_src):
+        pytest.skip("reference package not present")
+    sys.path.insert(0, ref_src)
+    try:
+        from fftmorph import pgmio
+        from fftmorph.umbra import GridFunction as RefGrid
+    finally:
+        sys.path.remove(ref_src)
+    from paper_2305_03018_b200 import GridFunction
+    rng = np.random.default_rng(5)
+    img = rng.integers(0, 256, (7, 9))
+    ours = GridFunction(img, tonal_max=255)
+    pgmio.write_pgm(ours, tmp_path / "a.pgm")
+    back = pgmio.read_pgm(tmp_path / "a.pgm")
+    assert isinstance(back, RefGrid)
+    assert ours == back and back == ours
+    se_vals = rng.integers(0, 5, (3, 5))
+    se_def = rng.random((3, 5)) > 0.3
+    se_def[1, 2] = True
+    se = GridFunction(se_vals, se_def, lo=(-1, -2), tonal_max=4)
+    pgmio.write_se(se, tmp_path / "b.se")
+    se_back = pgmio.read_se(tmp_path / "b.se")
+    assert se == se_back and se_back == se
