@@ -1000,7 +1000,14 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
   if (chunks) {
     plan_chunks = *chunks;
   } else {
-    for (int64_t c0 = cbeg; c0 < cend; c0 += p->ipc) plan_chunks.push_back({c0, (int)std::min<int64_t>(p->ipc, cend - c0)});
+    // balanced launch chunks (16 images with room for 12: 8 + 8, not 12 + 4)
+    const int64_t nimg = cend - cbeg;
+    const int64_t nch = (nimg + p->ipc - 1) / std::max<int64_t>(p->ipc, 1);
+    for (int64_t i = 0, c0 = cbeg; i < nch; ++i) {
+      const int64_t n = (nimg - (c0 - cbeg) + (nch - i) - 1) / (nch - i);
+      plan_chunks.push_back({c0, (int)n});
+      c0 += n;
+    }
   }
   for (size_t ci = 0; ci < plan_chunks.size(); ++ci)
     for (int u0 = 0; u0 < p->units; u0 += p->upl)
