@@ -8,6 +8,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
    python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launches_$TAG.log 2>&1
 echo launches_rc=$? >> gpurun_out/ncu_launches_$TAG.log
 timeout 300 python bench.py --images 4 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/bench_small_$TAG.log 2>&1 && \
-timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:"tile128_kernelILb0E|tonal_kernel_pipeILi18E|range_kernelILi0E" -s 3 -c 3 -o gpurun_out/prof_$TAG \
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:"tile128_kernelIhLb0E|tonal_kernel_pipeILi18E|range_kernelILi0E" -s 3 -c 3 -o gpurun_out/prof_$TAG \
    python bench.py --images 4 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_$TAG.log 2>&1
 echo ncu_rc=$? >> gpurun_out/ncu_$TAG.log
