@@ -85,3 +85,22 @@ def test_error_string_without_gpu(lib):
     assert b"null" in lib.fm_last_error()
     with pytest.raises(ValueError):
         _lib.check(rc)
+
+
+def test_no_cpu_fallback(tmp_path):
+    """The operators never compute on the CPU: without a usable library / device they raise."""
+    import os
+    import subprocess
+    import sys
+    code = ("import paper_2305_03018_b200 as fm\n"
+            "f = fm.GridFunction.from_tokens([3, 0, 7, 6, 2, 7], tonal_max=7)\n"
+            "b = fm.GridFunction.from_tokens([1, 2, None, 0], lo=(-1,), tonal_max=2)\n"
+            "try:\n"
+            "    fm.dilate_fft(f, b)\n"
+            "    print('computed')\n"
+            "except RuntimeError as e:\n"
+            "    print('raised')\n")
+    env = dict(os.environ, FM_LIB=str(tmp_path / "missing.so"), CUDA_VISIBLE_DEVICES="")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.stdout.strip().splitlines()[-1] == "raised", out.stdout + out.stderr
