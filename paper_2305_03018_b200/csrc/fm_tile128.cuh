@@ -17,6 +17,15 @@
 // only data inside the warp's own shared-memory region (warp w owns k1 in
 // {2w, 2w+1}); F1 -> F2 and I2 -> I1 are the two CTA barriers per plane, and
 // I1 -> the next plane's F1 needs none (same thread partition and slots).
+// All butterflies, twiddles and the product are packed f32x2 instructions
+// (fm_dft.cuh).  I1's columns start at the window (x = c + mx - 1), and the plan
+// trims the window to a multiple of 32 columns when that leaves one I1 warp per
+// scheduler without output columns: it runs ahead into the next plane's F1.
+//
+// SE spectrum of the product (thread order, four 32 KB chunks per plane): slot
+// 0's two chunks arrive by bulk async copies into shared memory a whole plane
+// ahead (issued by the last warp to release the buffer), slot 1's go straight
+// from L2 into registers, loaded at the start of the plane.
 //
 // Shared-memory layouts (float2 slots, per-warp regions of 1088):
 //   B1 (F1/I1 <-> F2/I2): (k1, n2, x) -> (k1>>1)*1088 + ((k1&1)*4 + n2)*128 + x
