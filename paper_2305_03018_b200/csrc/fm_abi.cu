@@ -1170,7 +1170,10 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       }
       return FM_OK;
     };
-    if (p->big) {
+    // 256x256 path: launched after the host has the per-ladder counts, with a
+    // plane grid of the largest tonal length in use (not the plan's K: most
+    // units need a few planes, the rest of the grid would only exit)
+    auto launch_big = [&](int kmax) -> int {
       if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
       BigArgs b{};
       b.img = a.img;
@@ -1202,15 +1205,18 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       b.err = p->stats + 1;
       const unsigned z = (unsigned)(nu * n);
       const unsigned inv_blocks = (unsigned)((kBig - (p->my - 1) + kBigRows - 1) / kBigRows);
-      big_rows_kernel<true, false><<<dim3(kBig / kBigRows, p->K, z), kBigNT, kBigRowsSmem, s>>>(b);
-      big_cols_kernel<false><<<dim3(kBig / kBigCols, p->K, z), kBigColsNT, kBigColsSmem, s>>>(b);
-      big_rows_kernel<false, false><<<dim3(inv_blocks, p->K, z), kBigNT, kBigRowsSmem, s>>>(b);
+      big_rows_kernel<true, false><<<dim3(kBig / kBigRows, kmax, z), kBigNT, kBigRowsSmem, s>>>(b);
+      big_cols_kernel<false><<<dim3(kBig / kBigCols, kmax, z), kBigColsNT, kBigColsSmem, s>>>(b);
+      big_rows_kernel<false, false><<<dim3(inv_blocks, kmax, z), kBigNT, kBigRowsSmem, s>>>(b);
       g_launches += 3;
       FM_CUDA(cudaGetLastError());
       if (p->timing) {
         FM_CUDA(cudaEventRecord(next_event(p), s));
         p->pending_conv.push_back({e0, e0 + 1});
       }
+      return FM_OK;
+    };
+    if (p->big) {
     } else if (!dyn) {
       // plan-time chunking (one chunk per unit for large launches); CTAs past
       // the actual job count exit at once
@@ -1222,6 +1228,15 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     // ---- the tonal kernels need the per-ladder unit counts (ready long before
     // the conv kernel finishes; the host waits only for the small copy)
     FM_CUDA(cudaEventSynchronize(p->count_ev[buf]));
+    if (p->big) {
+      int kmax = 0;
+      for (int li = 0; li < L; ++li)
+        if (reinterpret_cast<volatile int*>(p->h_counts[buf])[li] > 0) kmax = std::max(kmax, p->ladder[li] + 1);
+      if (kmax > 0) {
+        int rc = launch_big(kmax);
+        if (rc) return rc;
+      }
+    }
     if (dyn) {
       int64_t planes_tot = 0;
       for (int li = 0; li < L; ++li)
