@@ -1061,7 +1061,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       S = (int)std::min<int64_t>(std::min(max_s, 32), std::max<int64_t>(1, (4 * 148 + ctas - 1) / ctas));
     }
     r.splits = S;
-    r.skip0 = (p->big || g_no_skip0) ? 0 : 1;
+    r.skip0 = g_no_skip0 ? 0 : 1;
     r.warp_sync = g_range_sync;
     size_t rsm = 0;
     if (r.ntaps > 0) {
@@ -1336,7 +1336,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       FM_CUDA(cudaStreamWaitEvent(s, p->ev_join[i], 0));
     }
     // full units (fm_range.cuh) skip plane 0: fewer planes computed, stored and read
-    if (!p->big && !g_no_skip0 && img_defined == nullptr) {
+    if (!g_no_skip0 && img_defined == nullptr) {
       const double skipped = (double)n * (double)(p->full_prefix[u0 + nu] - p->full_prefix[u0]);
       planes -= skipped;
       tonal_b -= skipped * (double)p->npx * 8.0;

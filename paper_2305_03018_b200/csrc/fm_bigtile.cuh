@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
     K = up.y + 1;
     T = 2 * up.y;
     enc_bias = a.enc_sign > 0 ? -up.x : up.x;
+    if (k == 0 && (up.w & 2)) return;   // plane 0 of a full unit: the tonal pass knows it
   }
   if (k >= K) return;
   const int row0 = FWD ? blockIdx.x * kBigRows : (a.my - 1) + blockIdx.x * kBigRows;
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a
   if constexpr (!SPEC) {
     const int4 up = a.unit_param[(size_t)img * a.units + unit];
     K = up.y + 1;
-    if (k >= K) return;
+    if (k >= K || (k == 0 && (up.w & 2))) return;   // past the unit's planes / known plane 0
     spec_plane = a.spec + a.spec_off[up.z] + ((size_t)k * (kBig / kBigCols) + cb) * (SQ * kBigColsNT);
     // the product's spectrum chunk streams in while the forward passes run
 #pragma unroll
