@@ -94,28 +94,50 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
   if constexpr (FWD) {
     // ---- stage tonal indices of rows [row0, row0+32) of the tile's input window
     int bad = 0;
-#pragma unroll 8
-    for (int p = tid; p < kBigRows * PX; p += kBigNT) {
-      const int py = row0 + p / PX, px = p % PX;
-      uint16_t t = kSent;
-      if (SPEC) {
+    if constexpr (SPEC) {
+      for (int p = tid; p < kBigRows * PX; p += kBigNT) {
+        const int py = row0 + p / PX, px = p % PX;
+        uint16_t t = kSent;
         if (py < a.my && px < a.mx) {
           const int si = py * a.mx + px;
           if (a.se_def == nullptr || a.se_def[si]) t = (uint16_t)(a.se_vals[si] + a.enc_bias);
         }
-      } else {
-        const int iy = ty * a.QY + a.DY + py, ix = tx * a.QX + a.DX + px;
-        if (iy >= 0 && iy < a.H && ix >= 0 && ix < a.W) {
-          const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
-          if (a.img_def == nullptr || a.img_def[gi]) {
+        tv[p] = t;
+      }
+    } else {
+      // batches of GB independent (predicated) loads per thread, then the
+      // conversions: the image reads overlap instead of paying one latency each
+      constexpr int IT = kBigRows * PX / kBigNT, GB = 16;
+      static_assert(IT % GB == 0, "staging split");
+#pragma unroll 1
+      for (int g0 = 0; g0 < IT; g0 += GB) {
+        int raw[GB];
+        bool ok[GB];
+#pragma unroll
+        for (int u = 0; u < GB; ++u) {
+          const int p = tid + (g0 + u) * kBigNT;
+          const int py = row0 + p / PX, px = p % PX;
+          const int iy = ty * a.QY + a.DY + py, ix = tx * a.QX + a.DX + px;
+          ok[u] = iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+          raw[u] = 0;
+          if (ok[u]) {
+            const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
+            raw[u] = load_img(a.img, a.img_dtype, gi);
+            if (a.img_def != nullptr) ok[u] = a.img_def[gi] != 0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < GB; ++u) {
+          uint16_t t = kSent;
+          if (ok[u]) {
             // values below the unit's clamp level encode as the clamp (fm_range.cuh)
-            const int v = max(a.enc_sign * load_img(a.img, a.img_dtype, gi) + enc_bias, 0);
+            const int v = max(a.enc_sign * raw[u] + enc_bias, 0);
             if (v >= T) bad = 1;
             else t = (uint16_t)v;
           }
+          tv[tid + (g0 + u) * kBigNT] = t;
         }
       }
-      tv[p] = t;
     }
     if (!SPEC && bad) atomicOr(a.err, 1);
     __syncthreads();
