@@ -80,3 +80,29 @@ def test_alternate_paths_bit_exact(env, monkeypatch):
         ref, rvalid = cnaive.naive(img, None, se, None, (-15, -15), erode=(mode == "erode"), fill=fill)
         assert np.array_equal(out[0].cpu().numpy().astype(np.int64), ref.astype(np.int64)), (env, mode)
         assert np.array_equal(valid[0].cpu().numpy().astype(bool), rvalid.astype(bool)), (env, mode)
+
+
+@pytest.mark.parametrize("levels,se_range", [(250, 4), (256, 3), (600, 16), (740, 30), (1000, 16)])
+def test_long_tonal_axes_vs_oracle(levels, se_range):
+    """Tonal lengths around the limits: 254 (uint8 tile indices), the generic tonal
+    kernel's ~780 (T > 780 is refused at plan creation)."""
+    import torch
+    from paper_2305_03018_b200.engine import MorphPlan
+    rng = np.random.default_rng(levels * 7 + se_range)
+    img = rng.integers(0, levels, (200, 230))
+    se = rng.integers(0, se_range, (31, 29))
+    se_def = rng.random((31, 29)) > 0.2
+    se_def[15, 14] = True
+    for mode in ("dilate", "erode"):
+        fill = 0 if mode == "dilate" else levels - 1
+        try:
+            plan = MorphPlan(shape=img.shape, se_values=se, se_defined=se_def, se_lo=(-15, -14), mode=mode,
+                             img_dtype=torch.uint16, img_min=0, img_max=levels - 1, fill=fill, batch=1, tile=128)
+        except NotImplementedError:
+            assert levels + se_range > 780
+            return
+        out, valid = plan.execute(torch.from_numpy(img.astype(np.uint16)[None]).cuda())
+        assert plan.read_stats() < 0.25
+        ref, rvalid = cnaive.naive(img, None, se, se_def, (-15, -14), erode=(mode == "erode"), fill=fill)
+        assert np.array_equal(out[0].cpu().numpy().astype(np.int64), ref.astype(np.int64)), (levels, mode)
+        assert np.array_equal(valid[0].cpu().numpy().astype(bool), rvalid.astype(bool)), (levels, mode)
