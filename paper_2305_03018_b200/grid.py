@@ -56,7 +56,7 @@ class GridFunction:
     ``signed=True``.
     """
 
-    __slots__ = ("values", "defined", "lo", "tonal_max", "signed")
+    __slots__ = ("values", "defined", "lo", "tonal_max", "signed", "_gap_free", "_vmin", "_vmax")
 
     def __init__(self, values, defined=None, lo=None, tonal_max: int = 255,
                  signed: bool = False):
@@ -79,10 +79,14 @@ class GridFunction:
         tonal_max = int(tonal_max)
         if tonal_max < 1:
             raise ValueError("tonal_max must be positive")
-        dv = values[defined]
-        if dv.max() > tonal_max:
-            raise ValueError(f"value {dv.max()} exceeds tonal_max {tonal_max}")
-        if not signed and dv.min() < 0:
+        # min / max of the defined values, computed once (the grids are immutable);
+        # gap-free grids skip the boolean-indexed copy
+        gap_free = bool(defined.all())
+        dv = values if gap_free else values[defined]
+        vmin, vmax = int(dv.min()), int(dv.max())
+        if vmax > tonal_max:
+            raise ValueError(f"value {vmax} exceeds tonal_max {tonal_max}")
+        if not signed and vmin < 0:
             raise ValueError("negative value in an unsigned grid")
         values.flags.writeable = False
         defined.flags.writeable = False
@@ -91,6 +95,29 @@ class GridFunction:
         self.lo = lo
         self.tonal_max = tonal_max
         self.signed = bool(signed)
+        self._gap_free, self._vmin, self._vmax = gap_free, vmin, vmax
+
+    @classmethod
+    def _from_device(cls, values, lo, tonal_max: int, signed: bool, vmin: int, vmax: int) -> "GridFunction":
+        """Gap-free grid of freshly computed int64 values whose min / max are already
+        known (reduced on the device): the same checks as __init__ without another
+        pass over the host array."""
+        tonal_max = int(tonal_max)
+        if tonal_max < 1:
+            raise ValueError("tonal_max must be positive")
+        if vmax > tonal_max:
+            raise ValueError(f"value {vmax} exceeds tonal_max {tonal_max}")
+        if not signed and vmin < 0:
+            raise ValueError("negative value in an unsigned grid")
+        values = np.ascontiguousarray(values, dtype=np.int64)
+        defined = np.ones(values.shape, dtype=bool)
+        values.flags.writeable = False
+        defined.flags.writeable = False
+        g = cls.__new__(cls)
+        g.values, g.defined, g.lo = values, defined, tuple(int(x) for x in lo)
+        g.tonal_max, g.signed = tonal_max, bool(signed)
+        g._gap_free, g._vmin, g._vmax = True, int(vmin), int(vmax)
+        return g
 
     @classmethod
     def coerce(cls, g) -> "GridFunction":
@@ -120,13 +147,13 @@ class GridFunction:
 
     @property
     def gap_free(self) -> bool:
-        return bool(self.defined.all())
+        return self._gap_free
 
     def max_defined(self) -> int:
-        return int(self.values[self.defined].max())
+        return self._vmax
 
     def min_defined(self) -> int:
-        return int(self.values[self.defined].min())
+        return self._vmin
 
     def at(self, x) -> int | None:
         """Value at logical index x, or None at a gap."""

@@ -47,8 +47,7 @@ def _device():
 def _upload(g: GridFunction, dev):
     """Device copy of a grid's values in the narrowest supported dtype, plus its mask."""
     vals = g.values
-    dv = vals[g.defined]
-    lo_v, hi_v = int(dv.min()), int(dv.max())
+    lo_v, hi_v = g.min_defined(), g.max_defined()
     if lo_v >= 0 and hi_v <= 255:
         dt, npdt = torch.uint8, np.uint8
     elif lo_v >= 0 and hi_v <= 65535:
@@ -57,7 +56,7 @@ def _upload(g: GridFunction, dev):
         dt, npdt = torch.int32, np.int32
     else:
         raise NotImplementedError("image values beyond int32")
-    host = np.where(g.defined, vals, 0).astype(npdt)
+    host = vals.astype(npdt) if g.gap_free else np.where(g.defined, vals, 0).astype(npdt)
     t = torch.from_numpy(host).to(dev, non_blocking=False)
     mask = None if g.gap_free else torch.from_numpy(g.defined.astype(np.uint8)).to(dev)
     return t, mask, dt, lo_v, hi_v
@@ -67,10 +66,23 @@ def _run_fft(f: GridFunction, b: GridFunction, *, mode: str, crop: bool, fill: i
              stats: dict | None):
     dev = _device()
     img, mask, dt, vmin, vmax = _upload(f, dev)
+    # narrowest output element type holding every possible result (fewer bytes
+    # back over the bus; widened to int64 on the host like the reference's)
+    bmin, bmax = b.min_defined(), b.max_defined()
+    if mode == "dilate":
+        olo, ohi = min(fill, vmin + bmin), max(fill, vmax + bmax)
+    else:
+        olo, ohi = min(fill, vmin - bmax), max(fill, vmax - bmin)
+    if 0 <= olo and ohi <= 255:
+        odt = torch.uint8
+    elif -32768 <= olo and ohi <= 32767:
+        odt = torch.int16
+    else:
+        odt = torch.int32
     plan = engine.plan_cache.get(
         shape=f.shape, se_values=b.values, se_defined=None if b.gap_free else b.defined,
         se_lo=b.lo, mode=mode, crop=crop, img_dtype=dt, img_min=vmin, img_max=vmax,
-        fill=fill, batch=1, device=dev)
+        fill=fill, batch=1, device=dev, out_dtype=odt)
     plan.reset_stats()
     out, valid = plan.execute(img.unsqueeze(0), None if mask is None else mask.unsqueeze(0))
     dev_max = plan.read_stats()          # raises ArithmeticError at >= 0.25 (fft_conv.py:145-148)
@@ -80,9 +92,10 @@ def _run_fft(f: GridFunction, b: GridFunction, *, mode: str, crop: bool, fill: i
         info = plan.info
         tile = (info["tile_x"],) if f.ndim == 1 else (info["tile_y"], info["tile_x"])
         stats["padded_shape"] = tuple(tile) + (info["tonal_len"],)
+    mn, mx = torch.aminmax(out[0])
     values = out[0].cpu().numpy().astype(np.int64)
     vmask = valid[0].cpu().numpy().astype(bool)
-    return values, vmask, plan
+    return values, vmask, (int(mn), int(mx))
 
 
 def _empty_crop_quirk(f_ranges, conv_ranges):
@@ -108,10 +121,10 @@ def dilate_fft(f, b, *, crop: bool = True, return_validity: bool = False,
     conv = full_output_range(f.ranges, b.ranges)
     if crop:
         _empty_crop_quirk(f.ranges, conv)
-    values, valid, _ = _run_fft(f, b, mode="dilate", crop=crop, fill=0, stats=stats)
+    values, valid, rng = _run_fft(f, b, mode="dilate", crop=crop, fill=0, stats=stats)
     out_ranges = f.ranges if crop else conv
     tonal_max = max(f.tonal_max + b.max_defined(), 1)
-    g = GridFunction(values, lo=tuple(lo for lo, _ in out_ranges), tonal_max=tonal_max)
+    g = GridFunction._from_device(values, tuple(lo for lo, _ in out_ranges), tonal_max, False, *rng)
     return (g, valid) if return_validity else g
 
 
@@ -159,8 +172,8 @@ def erode_fft(f, b, l: int | None = None, *, return_validity: bool = False,
         raise ValueError("tonal lift needs non-negative values")
     rb_ranges = tuple((-hi, -lo) for lo, hi in b.ranges)
     _empty_crop_quirk(f.ranges, full_output_range(f.ranges, rb_ranges))
-    values, valid, _ = _run_fft(f, b, mode="erode", crop=True, fill=l, stats=stats)
-    g = GridFunction(values, lo=f.lo, tonal_max=max(f.tonal_max, l), signed=True)
+    values, valid, rng = _run_fft(f, b, mode="erode", crop=True, fill=l, stats=stats)
+    g = GridFunction._from_device(values, f.lo, max(f.tonal_max, l), True, *rng)
     return (g, valid) if return_validity else g
 
 
@@ -187,11 +200,11 @@ def _dilate_fft_signed(f, b, **kw):
     conv = full_output_range(f.ranges, b.ranges)
     if crop:
         _empty_crop_quirk(f.ranges, conv)
-    values, valid, _ = _run_fft(f, b, mode="dilate", crop=crop, fill=0, stats=stats)
+    values, valid, rng = _run_fft(f, b, mode="dilate", crop=crop, fill=0, stats=stats)
     out_ranges = f.ranges if crop else conv
     shift = -m
     tonal_max = max(f.tonal_max + shift + b.max_defined(), 1)
-    g = GridFunction(values, lo=tuple(lo for lo, _ in out_ranges), tonal_max=tonal_max, signed=True)
+    g = GridFunction._from_device(values, tuple(lo for lo, _ in out_ranges), tonal_max, True, *rng)
     return (g, valid) if want_validity else g
 
 
