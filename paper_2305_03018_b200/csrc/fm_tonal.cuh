@@ -389,8 +389,8 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a, 
       const float2 xk = xs[k * NT], xm = conjf2(xs[(N - k) * NT]);
       const float2 sk = cadd(xk, xm), dk = csub(xk, xm);
       const float2 m = cmul(c_ttw[off + k], dk);
-      A[k] = make_float2(sk.x - m.y, sk.y + m.x);
-      A[N - k] = make_float2(sk.x + m.y, m.x - sk.y);
+      A[k] = cadd_i(sk, m);                       // s + i m
+      A[N - k] = cadd_i(conjf2(sk), conjf2(m));   // s^* + i m^*
     }
     if constexpr (N % 2 == 0 && N > 0) {
       const float2 xh = xs[(N / 2) * NT];
