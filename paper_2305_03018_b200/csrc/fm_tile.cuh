@@ -580,6 +580,9 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
               if (atomicAdd(&s_rel[b], 1) == C::NW - 1) {
                 s_rel[b] = 0;
                 if (k + 1 < *kend_s) {
+                  // every warp's generic-proxy reads of the buffer happen before this
+                  // (the release counter); order them before the async-proxy refill
+                  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                   mbar_expect_tx(&s_full[b], C::kChunkBytes);
                   bulk_g2s_nohint(sbuf + b * C::kChunkF4,
                                   spec_base + (size_t)(k + 1) * C::kSpecPairs + (size_t)b * C::kChunkF4,

@@ -344,7 +344,13 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a, 
         const int2 job = job_next;
         const int item_next = item + gridDim.x;
         if (item_next < items) job_next = a.list[item_next / bpj];
-        if (i >= ST) mbar_wait(&empty[st], (uint32_t)(((i / ST) - 1) & 1));
+        if (i >= ST) {
+          mbar_wait(&empty[st], (uint32_t)(((i / ST) - 1) & 1));
+          // the consumers read the stage through the generic proxy (released by
+          // their arrives); order those reads before the async-proxy refill —
+          // without this fence a stage was occasionally overwritten while read
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
         const int j = item / bpj, blk = item - j * bpj;
         const int k0 = (job.y & kJobFull) ? 1 : 0;   // plane 0 known (not copied)
         if (a.use_tma) {

@@ -126,3 +126,16 @@ def test_large_int32_values_vs_int64_oracle(offset):
             ref, rvalid, _ = port.erode_naive(img, None, (0, 0), se, None, (-4, -5), neutral=fill)
         assert np.array_equal(out[0].cpu().numpy().astype(np.int64), ref)
         assert np.array_equal(valid[0].cpu().numpy().astype(bool), rvalid)
+
+
+def test_stage_reuse_race_regression():
+    """Fuzz case 124 (int32, gaps, 58x33 SE, T = 270) run repeatedly over a device
+    heap pre-filled with garbage: it caught a write-after-read race between the
+    consumers' generic-proxy reads of a pipeline stage and the producer's next
+    async-proxy (TMA) copy into it (fixed by fence.proxy.async before the
+    release); ~7% of runs failed without the fence."""
+    import torch
+    for r in range(15):
+        junk = torch.full((int(1e9) // 4,), float(r) + 0.5, dtype=torch.float32, device="cuda")
+        del junk
+        test_fuzz_engine_vs_oracle(124)
