@@ -6,12 +6,12 @@
 // 2^14-point 2-D transform runs as THREE shared-memory passes per direction
 // instead of four, with every thread holding 32 points:
 //
-//   F1  y: 32-point DFT over n1 (y = n2 + 4 n1), twiddle W_128^{n2 k1}     thread (x, n2)
-//   F2  y: 4-point DFT over n2 -> k2;  x: 8-point DFT over m1 -> j1
+//   F1  y: 32-point DFT over n1 (y = n2 + 4 n1)                           thread (x, n2)
+//   F2  y: twiddle W_128^{n2 k1}, 4-point DFT over n2 -> k2;  x: 8-point DFT over m1 -> j1
 //       (x = m2 + 16 m1), twiddle W_128^{m2 j1}                             thread (k1, m2)
 //   F3  x: 16-point DFT over m2 -> j2; product; inverse 16-point DFT         thread (k1, k2, j1)
-//   I2  inverse of F2 (conjugate twiddle first)                            thread (k1, m2)
-//   I1  conjugate twiddle, inverse 32-point DFT, store of the window rows   thread (x, n2)
+//   I2  inverse of F2 (conjugate twiddles)                                 thread (k1, m2)
+//   I1  inverse 32-point DFT, store of the window rows                      thread (x, n2)
 //
 // so frequency (ky, kx) = (k1 + 32 k2, j1 + 8 j2).  F2 -> F3 -> I2 exchange
 // only data inside the warp's own shared-memory region (warp w owns k1 in
@@ -65,8 +65,7 @@ struct T128 {
   static_assert(2 * (kTMax + 1) <= kEncSlots, "encode tables");
 };
 
-// F1/I1 twiddles W_128^{n2 k1} laid out [n2][k1]: the warp-uniform n2 row plus
-// a compile-time k1 offset is one uniform constant load per element
+// y twiddles W_128^{n2 k1} laid out [n2][k1] (applied in F2 / I2: three per thread)
 __constant__ float2 c_twy[4 * 32];
 
 template <typename TV, bool SPEC>
@@ -210,11 +209,7 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
       float2 v[32];
 #pragma unroll
       for (int n1 = 0; n1 < 32; ++n1) v[n1] = Mk[tv[(f_n2 + 4 * n1) * P + f_x]];
-      dft32p_fwd<false>(v);
-      if (f_n2 != 0) {
-#pragma unroll
-        for (int r = 1; r < 32; ++r) v[r] = cmul(v[r], c_twy[f_n2 * 32 + dft32p_freq(r)]);
-      }
+      dft32p_fwd<false>(v);   // the y twiddle W^{n2 k1} is applied in F2 (same work on every warp)
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         const int k1 = dft32p_freq(r);
@@ -234,6 +229,17 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
 #pragma unroll
         for (int m1 = 0; m1 < 8; ++m1) c[n2][m1] = b1_row[n2 * P + 16 * m1];
       __syncwarp();   // the warp's region is rewritten in the B2 layout below
+      // y twiddle W_128^{n2 k1} of the DFT32 outputs (k1 = 2 warp + hi: three
+      // runtime twiddles, each applied to the thread's 8 values of that n2)
+      {
+        const int k1 = 2 * warp + hi;
+#pragma unroll
+        for (int n2 = 1; n2 < 4; ++n2) {
+          const float2 w = c_twy[n2 * 32 + k1];
+#pragma unroll
+          for (int m1 = 0; m1 < 8; ++m1) c[n2][m1] = cmul(c[n2][m1], w);
+        }
+      }
 #pragma unroll
       for (int m1 = 0; m1 < 8; ++m1) {
         float2 t[4] = {c[0][m1], c[1][m1], c[2][m1], c[3][m1]};
@@ -353,6 +359,15 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
 #pragma unroll
         for (int n2 = 0; n2 < 4; ++n2) c[n2][m1] = t[n2];
       }
+      {
+        const int k1 = 2 * warp + hi;
+#pragma unroll
+        for (int n2 = 1; n2 < 4; ++n2) {
+          const float2 w = c_twy[n2 * 32 + k1];
+#pragma unroll
+          for (int m1 = 0; m1 < 8; ++m1) c[n2][m1] = cmulc(c[n2][m1], w);
+        }
+      }
 #pragma unroll
       for (int n2 = 0; n2 < 4; ++n2)
 #pragma unroll
@@ -368,11 +383,7 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
         const int k1 = dft32p_freq(r);
         v[r] = b1_col[(k1 >> 1) * REG + (k1 & 1) * 4 * P];
       }
-      if (f_n2 != 0) {
-#pragma unroll
-        for (int r = 1; r < 32; ++r) v[r] = cmulc(v[r], c_twy[f_n2 * 32 + dft32p_freq(r)]);
-      }
-      dft32p_inv<true>(v);
+      dft32p_inv<true>(v);   // its conjugate y twiddle was applied in I2
       // window pixel (y - (my-1)) * QX + (x - (mx-1)); rows y = n2 + 4 n1 in
       // [my-1, y_end) are stored: a per-thread row mask (bit n1) and a running
       // pointer keep the unrolled store loop at one predicate test and one
