@@ -396,11 +396,15 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
         const uint32_t below_hi = hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u);
         const uint32_t rows = hi > lo ? below_hi & ~((1u << lo) - 1u) : 0u;
         float2* dst = chat_unit + ((ptrdiff_t)k * a.wpx + (ptrdiff_t)(f_n2 - (a.my - 1)) * a.QX + f_c);
-        const int step = 4 * a.QX;
+        // the running row address is kept in a register by inline PTX (left to
+        // itself the compiler re-derives it from the kernel parameter every row)
+        uint64_t pa = reinterpret_cast<uint64_t>(dst);
+        const uint64_t step_b = (uint64_t)(4 * a.QX) * sizeof(float2);
 #pragma unroll
         for (int n1 = 0; n1 < 32; ++n1) {
-          if ((rows >> n1) & 1u) *dst = v[n1];
-          dst += step;
+          if ((rows >> n1) & 1u)
+            asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(pa), "f"(v[n1].x), "f"(v[n1].y) : "memory");
+          asm("add.s64 %0, %0, %1;" : "+l"(pa) : "l"(step_b));
         }
       }
       // no barrier: the next plane's F1 writes exactly the slots this thread read
