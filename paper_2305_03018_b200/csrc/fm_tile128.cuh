@@ -207,8 +207,14 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
     // ---------------- F1: encode + y DFT32 + twiddle W^{n2 k1}
     {
       float2 v[32];
+      // table entry t at byte address mkb + 8 t: one LEA per pixel (indexing Mk
+      // directly adds the plane's table offset to t first)
+      const uint32_t mkb = smem_addr(Mk);
 #pragma unroll
-      for (int n1 = 0; n1 < 32; ++n1) v[n1] = Mk[tv[(f_n2 + 4 * n1) * P + f_x]];
+      for (int n1 = 0; n1 < 32; ++n1) {
+        const uint32_t t = tv[(f_n2 + 4 * n1) * P + f_x];
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[n1].x), "=f"(v[n1].y) : "r"(mkb + (t << 3)));
+      }
       dft32p_fwd<false>(v);   // the y twiddle W^{n2 k1} is applied in F2 (same work on every warp)
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
