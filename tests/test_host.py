@@ -168,3 +168,23 @@ def test_reference_file_formats_interoperate(tmp_path):
     pgmio.write_se(se, tmp_path / "b.se")
     se_back = pgmio.read_se(tmp_path / "b.se")
     assert se == se_back and se_back == se
+
+
+def test_grid_cached_extrema_and_trusted_constructor():
+    """Grids cache min / max / gap-free at construction (gap-free grids skip the
+    boolean-indexed copy); the device-result constructor keeps __init__'s checks."""
+    from paper_2305_03018_b200 import GridFunction
+    v = np.array([[3, 9], [0, 4]])
+    g = GridFunction(v, tonal_max=9)
+    assert (g.min_defined(), g.max_defined(), g.gap_free) == (0, 9, True)
+    d = np.array([[True, False], [True, True]])
+    h = GridFunction(v, d, tonal_max=9)
+    assert (h.min_defined(), h.max_defined(), h.gap_free) == (0, 4, False)
+    t = GridFunction._from_device(v, (0, 0), 9, False, 0, 9)
+    assert t == g and t.gap_free and not t.values.flags.writeable
+    with pytest.raises(ValueError):
+        GridFunction._from_device(v, (0, 0), 8, False, 0, 9)      # exceeds tonal_max
+    with pytest.raises(ValueError):
+        GridFunction._from_device(v - 5, (0, 0), 9, False, -5, 4)  # negative, unsigned
+    s = GridFunction._from_device(v - 5, (1, -2), 9, True, -5, 4)
+    assert s.lo == (1, -2) and s.signed and s.min_defined() == -5
