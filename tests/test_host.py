@@ -188,3 +188,28 @@ def test_grid_cached_extrema_and_trusted_constructor():
         GridFunction._from_device(v - 5, (0, 0), 9, False, -5, 4)  # negative, unsigned
     s = GridFunction._from_device(v - 5, (1, -2), 9, True, -5, 4)
     assert s.lo == (1, -2) and s.signed and s.min_defined() == -5
+
+
+def test_committed_bench_line_contract():
+    """The newest committed bench line carries every key the driver and the judge
+    read (metric/value/unit/..., roofline, e2e, cpu_baseline, clocks, gpu_launches)."""
+    import json
+    from pathlib import Path
+    prof = Path(__file__).resolve().parents[1] / "profiles"
+    lines = sorted(prof.glob("r1*_bench_line.json"), key=lambda f: (len(f.stem), f.stem))
+    assert lines, "no committed bench line"
+    d = json.loads(lines[-1].read_text())
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches",
+                "clocks", "cpu_baseline"):
+        assert key in d, key
+    r = d["roofline"]
+    for key in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert key in r, key
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-6
+    for key in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert key in d["e2e"], key
+    for key in ("value", "unit", "cores", "kind", "sample"):
+        assert key in d["cpu_baseline"], key
+    assert d["gpu_launches"] > 0 and d["steps"] >= 1 and d["warmup"] >= 3
+    assert not set(d["clocks"].get("reasons", [])) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
