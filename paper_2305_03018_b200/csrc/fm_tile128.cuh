@@ -56,7 +56,12 @@ struct T128 {
   // through it by per-thread cp.async
   static constexpr int kNSB = sizeof(TV) == 1 ? 2 : 1;
   static constexpr int kSpecBytes = kNSB * kChunkF4 * 16;
-  static constexpr int kTvBytes = P * P * (int)sizeof(TV);
+  // tonal indices, column-major with the rows of one F1 thread (y = n2 + 4 n1,
+  // n1 = 0..31) contiguous: (y, x) -> x * kTvLd + (y & 3) * 32 + (y >> 2); the
+  // 16-byte column pad keeps a warp's 16-byte loads (consecutive x) conflict-free
+  static constexpr int kTvLd = P + 16 / (int)sizeof(TV);
+  static constexpr int kTvBytes = P * kTvLd * (int)sizeof(TV);
+  static constexpr int kTvVec = 32 * (int)sizeof(TV) / 16;   // uint4 per F1 thread
   static constexpr int kTwBytes = 8 * 16 * 8;             // W_128^{m2 j1}, [j1][m2]
   static constexpr int kSmemFixed = kBufBytes + kSpecBytes + kTvBytes + kTwBytes;
   static constexpr int kEncSlots = (227 * 1024 - kSmemFixed - 256) / 8;   // two per-plane tables
@@ -109,20 +114,24 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
           // unit; reduce so their (unused) spectra stay finite
           if (a.se_def == nullptr || a.se_def[si]) t = (a.se_vals[si] + a.enc_bias) % T;
         }
-        tv[p] = (TV)t;
+        tv[px * C::kTvLd + (py & 3) * 32 + (py >> 2)] = (TV)t;
       }
     } else {
-      constexpr int IT = P * P / NT, GB = 16;
+      // thread (x, n2) stages rows y = n2 + 4 n1 of column x (a warp reads 32
+      // consecutive x of one row) and stores them as packed 16-byte words
+      constexpr int GB = 16, VPW = 4 / (int)sizeof(TV);
+      const int sx = tid & (P - 1), sn2 = tid >> 7;
+      const int ix = tx * a.QX + a.DX + sx;
+      const bool okx = ix >= 0 && ix < a.W;
+      uint4* trow = reinterpret_cast<uint4*>(tv + sx * C::kTvLd + sn2 * 32);
 #pragma unroll 1
-      for (int g0 = 0; g0 < IT; g0 += GB) {
+      for (int g0 = 0; g0 < 32; g0 += GB) {
         int raw[GB];
         bool ok[GB];
 #pragma unroll
         for (int u = 0; u < GB; ++u) {
-          const int p = tid + (g0 + u) * NT;
-          const int py = p / P, px = p - (p / P) * P;
-          const int iy = ty * a.QY + a.DY + py, ix = tx * a.QX + a.DX + px;
-          ok[u] = iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+          const int iy = ty * a.QY + a.DY + sn2 + 4 * (g0 + u);
+          ok[u] = okx && iy >= 0 && iy < a.H;
           raw[u] = 0;
           if (ok[u]) {
             const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
@@ -130,6 +139,9 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
             if (a.img_def != nullptr) ok[u] = a.img_def[gi] != 0;
           }
         }
+        uint32_t pk[GB / VPW];
+#pragma unroll
+        for (int i = 0; i < GB / VPW; ++i) pk[i] = 0;
 #pragma unroll
         for (int u = 0; u < GB; ++u) {
           int t = T;
@@ -139,8 +151,11 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
             if (v >= T) bad = 1;
             else t = v;
           }
-          tv[tid + (g0 + u) * NT] = (TV)t;
+          pk[u / VPW] |= (uint32_t)t << (8 * (int)sizeof(TV) * (u % VPW));
         }
+#pragma unroll
+        for (int i = 0; i < GB / VPW / 4; ++i)
+          trow[g0 / (16 / (int)sizeof(TV)) + i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
       }
       if (bad) atomicOr(a.err, 1);
     }
@@ -209,11 +224,21 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
       float2 v[32];
       // table entry t at byte address mkb + 8 t: one LEA per pixel (indexing Mk
       // directly adds the plane's table offset to t first)
+      // (the thread's 32 indices are two / four 16-byte words: one byte permute each)
       const uint32_t mkb = smem_addr(Mk);
+      const uint4* tq = reinterpret_cast<const uint4*>(tv + f_x * C::kTvLd + f_n2 * 32);
 #pragma unroll
-      for (int n1 = 0; n1 < 32; ++n1) {
-        const uint32_t t = tv[(f_n2 + 4 * n1) * P + f_x];
-        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[n1].x), "=f"(v[n1].y) : "r"(mkb + (t << 3)));
+      for (int h = 0; h < C::kTvVec; ++h) {
+        const uint4 q = tq[h];
+        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+        constexpr int VPW = 4 / (int)sizeof(TV), PER = 16 / (int)sizeof(TV);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const int n1 = h * PER + j, e = j % VPW;
+          const uint32_t t = sizeof(TV) == 1 ? __byte_perm(w4[j / VPW], 0, 0x4440 + e)
+                                             : __byte_perm(w4[j / VPW], 0, e ? 0x4432 : 0x4410);
+          asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[n1].x), "=f"(v[n1].y) : "r"(mkb + (t << 3)));
+        }
       }
       dft32p_fwd<false>(v);   // the y twiddle W^{n2 k1} is applied in F2 (same work on every warp)
 #pragma unroll
