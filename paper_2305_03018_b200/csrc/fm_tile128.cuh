@@ -163,7 +163,14 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
   if (tid < 128) twt[tid] = c_tw[TwOff<128>::v + (tid & 15) * (tid >> 4)];
   const int k_begin = kchunk_idx * a.k_chunk;
   const int k_first = k_begin + ((skip0 && kchunk_idx == 0) ? 1 : 0);
+  // with a trimmed window (QX <= 96) the inverse-y warps of column block 3 have
+  // no output columns: they build the encode table two planes ahead while the
+  // others run I1 (slack they would otherwise spend at the next F1 barrier), so
+  // both buffers start filled; otherwise the table of plane k + 1 is built after
+  // plane k's F1 barrier
+  const bool tab_in_i1 = !SPEC && a.QX <= 96;
   build_mtab(k_first);
+  if (tab_in_i1 && k_first + 1 < min(K, k_begin + a.k_chunk)) build_mtab(k_first + 1);
   __shared__ __align__(8) uint64_t s_full[2];   // spectrum buffers: bulk-copy completion
   __shared__ int s_rel[2];                       // warps that released the buffer
   __shared__ int s_kend;
@@ -250,7 +257,7 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
     __syncthreads();
     // next plane's table into the other buffer (its last reader, the previous
     // plane's F1, finished before this barrier)
-    if (k + 1 < *kend_s) build_mtab(k + 1);
+    if (!tab_in_i1 && k + 1 < *kend_s) build_mtab(k + 1);
 
     // ---------------- F2: y DFT4 over n2, x DFT8 over m1, twiddle W^{m2 j1}
     {
@@ -439,6 +446,12 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
         }
       }
       // no barrier: the next plane's F1 writes exactly the slots this thread read
+    } else if (tab_in_i1 && f_xb == 3 && k + 2 < *kend_s) {
+      // plane k + 2's table into this plane's buffer (its F1 reads ended at the
+      // F1 barrier; plane k + 1's barriers publish it)
+      float2* M = enc_s + (k & 1) * (T + 1);
+      const int kk = k + 2;
+      for (int j = f_n2 * 32 + lane; j <= T; j += 128) M[j] = j < T ? enc_g[(kk * j) % T] : make_float2(0.f, 0.f);
     }
     ++pord;
   }
