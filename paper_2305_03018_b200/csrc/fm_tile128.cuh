@@ -20,7 +20,8 @@
 // All butterflies, twiddles and the product are packed f32x2 instructions
 // (fm_dft.cuh).  I1's columns start at the window (x = c + mx - 1), and the plan
 // trims the window to a multiple of 32 columns when that leaves one I1 warp per
-// scheduler without output columns: it runs ahead into the next plane's F1.
+// scheduler without output columns: it builds the encode table of plane k + 2
+// (double-buffered per-plane tables) and runs ahead into the next plane's F1.
 //
 // SE spectrum of the product (thread order, four 32 KB chunks per plane): slot
 // 0's two chunks arrive by bulk async copies into shared memory a whole plane
