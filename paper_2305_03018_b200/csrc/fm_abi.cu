@@ -752,6 +752,21 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   } else {
     p->ipc = std::max<int64_t>(1, std::min<int64_t>(p->batch, budget / std::max<int64_t>(per_unit * p->units, 1)));
     if (p->ipc > 65535) p->ipc = 65535;
+    // equal launches: the largest divisor of the batch within the budget when it
+    // is at least half of it, else balanced sizes (c5, 64 images: 8 x 8 instead
+    // of 5 x 12 + 4 -- no short last launch, and earlier output copies)
+    int64_t div = 0;
+    for (int64_t c = p->ipc; c >= 1 && 2 * c >= p->ipc; --c)
+      if (p->batch % c == 0) {
+        div = c;
+        break;
+      }
+    if (div > 0) {
+      p->ipc = div;
+    } else {
+      const int64_t nl = (p->batch + p->ipc - 1) / p->ipc;
+      p->ipc = (p->batch + nl - 1) / nl;
+    }
   }
   const int64_t slots = p->ipc * p->upl;
   const int occ = p->two_d ? std::max(1, (kSmemLimit) / (int)(p->conv_smem + 1024)) : 2;
