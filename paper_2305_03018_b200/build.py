@@ -4,6 +4,7 @@
 """
 from __future__ import annotations
 
+import fcntl
 import os
 import shutil
 import subprocess
@@ -36,22 +37,50 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile the library if a source is newer than it.  Safe under concurrent callers
+    (ranks of one node, parallel test workers): an exclusive file lock serialises the
+    build, and each process writes its own temporary file before the atomic rename."""
     if not force and not needs_build():
         return LIB
     OUT_DIR.mkdir(parents=True, exist_ok=True)
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3",
-           *os.environ.get("FM_NVCC_EXTRA", "").split(),
-           "-I", str(ROOT / "include"), "-I", str(CSRC),
-           *[str(s) for s in SOURCES], "-o", str(tmp), "-lcudart"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode})")
-    if verbose:
-        sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
+    with open(OUT_DIR / ".build.lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if not force and not needs_build():   # another process built it meanwhile
+                return LIB
+            tmp = LIB.with_name(f"{LIB.name}.{os.getpid()}.tmp")
+            cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+                   "-Xptxas", "-v" if verbose else "-O3",
+                   *os.environ.get("FM_NVCC_EXTRA", "").split(),
+                   "-I", str(ROOT / "include"), "-I", str(CSRC),
+                   *[str(s) for s in SOURCES], "-o", str(tmp), "-lcudart"]
+            res = subprocess.run(cmd, capture_output=True, text=True)
+            if res.returncode != 0:
+                sys.stderr.write(res.stdout + res.stderr)
+                try:
+                    tmp.unlink()
+                except FileNotFoundError:
+                    pass
+                raise RuntimeError(f"nvcc failed ({res.returncode})")
+            if verbose:
+                sys.stderr.write(res.stderr)
+            os.replace(tmp, LIB)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
+    return LIB
+
+
+def build_rank_safe(rank: int = 0, world: int = 1) -> Path:
+    """Multi-process launch (torchrun): rank 0 builds, every rank waits at a barrier of the
+    already-initialised process group, then checks the library exists."""
+    import torch.distributed as dist
+    multi = world > 1 and dist.is_available() and dist.is_initialized()
+    if not multi or rank == 0:
+        build()
+    if multi:
+        dist.barrier()
+    if not LIB.exists():
+        raise RuntimeError(f"{LIB} missing after the build")
     return LIB
 
 

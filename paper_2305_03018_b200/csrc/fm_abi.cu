@@ -768,6 +768,11 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
       p->ipc = (p->batch + nl - 1) / nl;
     }
   }
+  // the 256x256 path launches gridDim.z = units x images of a launch (<= 65535)
+  if (p->big && (int64_t)p->upl * p->ipc > 65535) {
+    if (p->upl > 65535) p->upl = 65535;
+    p->ipc = std::max<int64_t>(1, 65535 / p->upl);
+  }
   const int64_t slots = p->ipc * p->upl;
   const int occ = p->two_d ? std::max(1, (kSmemLimit) / (int)(p->conv_smem + 1024)) : 2;
   const int64_t target = 148LL * 2 * occ;
@@ -1455,16 +1460,45 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, v
   const size_t osz = out_size(p->d.out_dtype);
   char* out_host = reinterpret_cast<char*>(out_host_v);
   if (!p->h_img) {
-    FM_CUDA(cudaMalloc(&p->h_img, in_n * dsz));
-    FM_CUDA(cudaMalloc(&p->h_def, in_n));
-    FM_CUDA(cudaMalloc(&p->h_out, out_n * osz));
-    FM_CUDA(cudaMalloc(&p->h_valid, out_n));
-    FM_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
-    FM_CUDA(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
+    // allocate into locals and commit to the plan only when every call succeeded (a
+    // partial failure leaves the plan without staging, so the next call retries)
+    void* hi = nullptr;
+    uint8_t *hd = nullptr, *hv = nullptr;
+    int32_t* ho = nullptr;
+    cudaStream_t cs = nullptr, ds2 = nullptr;
+    cudaEvent_t evi = nullptr;
     const int64_t nchunks = (p->batch + p->ipc - 1) / p->ipc;
-    p->ev_chunks.resize(2 * nchunks);
-    for (auto& ev : p->ev_chunks) FM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    FM_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+    std::vector<cudaEvent_t> evs(2 * nchunks, nullptr);
+    cudaError_t e = cudaMalloc(&hi, in_n * dsz);
+    if (e == cudaSuccess) e = cudaMalloc(&hd, in_n);
+    if (e == cudaSuccess) e = cudaMalloc(&ho, out_n * osz);
+    if (e == cudaSuccess) e = cudaMalloc(&hv, out_n);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ds2, cudaStreamNonBlocking);
+    for (auto& ev : evs)
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&evi, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      cudaFree(hi);
+      cudaFree(hd);
+      cudaFree(ho);
+      cudaFree(hv);
+      if (cs) cudaStreamDestroy(cs);
+      if (ds2) cudaStreamDestroy(ds2);
+      for (auto ev : evs)
+        if (ev) cudaEventDestroy(ev);
+      if (evi) cudaEventDestroy(evi);
+      return fail(e == cudaErrorMemoryAllocation ? FM_ENOMEM : FM_ECUDA,
+                  std::string("host-path staging: ") + cudaGetErrorString(e));
+    }
+    p->h_img = hi;
+    p->h_def = hd;
+    p->h_out = ho;
+    p->h_valid = hv;
+    p->copy_stream = cs;
+    p->d2h_stream = ds2;
+    p->ev_chunks = std::move(evs);
+    p->ev_in = evi;
   }
   // Chunk pipeline: every H2D is queued up front on one copy stream, each
   // chunk's compute on `s` waits only for its own input, and its D2H runs on a

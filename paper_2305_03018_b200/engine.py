@@ -107,29 +107,57 @@ class MorphPlan:
         self.out_lo_offset = tuple(self.info["out_lo_offset"][:nd])
 
     # ------------------------------------------------------------------
+    # ------------------------------------------------------------------
+    def _check(self, t, name, shape, dtype, device, *, numel_only=False):
+        """Raise (ValueError / TypeError) unless `t` is a contiguous tensor of `shape` and `dtype`
+        on `device`: raw pointers go to the library, so a wrong buffer must never reach it."""
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch.Tensor, got {type(t).__name__}")
+        if t.dtype != dtype:
+            raise TypeError(f"{name} dtype {t.dtype} != expected {dtype}")
+        if t.device != device:
+            raise ValueError(f"{name} on {t.device}, expected {device}")
+        n = int(np.prod(shape))
+        if t.numel() != n or (not numel_only and tuple(t.shape) != tuple(shape)):
+            raise ValueError(f"{name} shape {tuple(t.shape)} != expected {tuple(shape)}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+
+    def _out_shapes(self):
+        oshape = (self.batch, *self.out_shape)
+        vshape = oshape
+        if self.counts:   # count volume [batch, *out_shape, count_len] int32
+            oshape = (*oshape, self.info["count_len"])
+        return oshape, vshape, (torch.int32 if self.counts else self.out_dtype)
+
     def execute(self, img: torch.Tensor, defined: torch.Tensor | None = None, *,
                 out: torch.Tensor | None = None, valid: torch.Tensor | None = None,
                 want_valid: bool = True, stream=None):
         """Run on a device batch ``img[batch, *shape]``; returns (out of out_dtype, valid uint8|None)."""
         L = _lib.load()
+        exp = (self.batch, *self.shape)
+        if not isinstance(img, torch.Tensor):
+            raise TypeError("img must be a torch.Tensor on the plan's device")
         if img.device != self.device:
             raise ValueError(f"image on {img.device}, plan on {self.device}")
         if img.dtype != self.img_dtype:
             raise TypeError(f"image dtype {img.dtype} != plan dtype {self.img_dtype}")
-        exp = (self.batch, *self.shape)
-        if tuple(img.shape) != exp:
-            img = img.reshape(exp)
-        img = img.contiguous()
+        if img.numel() != int(np.prod(exp)):
+            raise ValueError(f"image shape {tuple(img.shape)} does not hold a batch of {exp}")
+        img = img.reshape(exp).contiguous()
         if defined is not None:
+            if not isinstance(defined, torch.Tensor) or defined.numel() != img.numel():
+                raise ValueError("defined mask must be a tensor with the image's element count")
             defined = defined.to(device=self.device, dtype=torch.uint8).reshape(exp).contiguous()
-        oshape = (self.batch, *self.out_shape)
+        oshape, vshape, odt = self._out_shapes()
         if out is None:
-            if self.counts:   # count volume [batch, *out_shape, count_len] int32
-                out = torch.empty((*oshape, self.info["count_len"]), dtype=torch.int32, device=self.device)
-            else:
-                out = torch.empty(oshape, dtype=self.out_dtype, device=self.device)
+            out = torch.empty(oshape, dtype=odt, device=self.device)
+        else:
+            self._check(out, "out", oshape, odt, self.device)
         if valid is None and want_valid:
-            valid = torch.empty(oshape, dtype=torch.uint8, device=self.device)
+            valid = torch.empty(vshape, dtype=torch.uint8, device=self.device)
+        elif valid is not None:
+            self._check(valid, "valid", vshape, torch.uint8, self.device)
         rc = L.fm_execute(self._h, ctypes.c_void_p(img.data_ptr()),
                           None if defined is None else ctypes.c_void_p(defined.data_ptr()),
                           ctypes.c_void_p(out.data_ptr()),
@@ -142,18 +170,30 @@ class MorphPlan:
                      want_valid=True, stream=None):
         """Host buffers in, host buffers out (copies inside; pinned memory recommended)."""
         L = _lib.load()
-        def host(t, dtype):
+        if self.counts:
+            raise NotImplementedError("count-volume plans run on device buffers (execute)")
+        cpu = torch.device("cpu")
+        exp = (self.batch, *self.shape)
+
+        def host(t, dtype, name):
             if isinstance(t, torch.Tensor):
-                assert t.device.type == "cpu" and t.is_contiguous()
+                self._check(t, name, exp, dtype, cpu, numel_only=True)
                 return t
-            return torch.from_numpy(np.ascontiguousarray(t)).to(dtype)
-        img_t = host(img, self.img_dtype)
-        def_t = None if defined is None else host(defined, torch.uint8)
+            a = np.ascontiguousarray(t)
+            if a.size != int(np.prod(exp)):
+                raise ValueError(f"{name} shape {a.shape} does not hold a batch of {exp}")
+            return torch.from_numpy(a).to(dtype)
+        img_t = host(img, self.img_dtype, "img")
+        def_t = None if defined is None else host(defined, torch.uint8, "defined")
         oshape = (self.batch, *self.out_shape)
         if out is None:
             out = torch.empty(oshape, dtype=self.out_dtype)
+        else:
+            self._check(out, "out", oshape, self.out_dtype, cpu)
         if valid is None and want_valid:
             valid = torch.empty(oshape, dtype=torch.uint8)
+        elif valid is not None:
+            self._check(valid, "valid", oshape, torch.uint8, cpu)
         rc = L.fm_execute_host(self._h, ctypes.c_void_p(img_t.data_ptr()),
                                None if def_t is None else ctypes.c_void_p(def_t.data_ptr()),
                                ctypes.c_void_p(out.data_ptr()),
@@ -196,13 +236,49 @@ class MorphPlan:
             pass
 
 
-class _PlanCache:
-    """Small LRU of plans keyed by everything fm_plan_create depends on."""
+def normalized_range(vmin: int, vmax: int) -> tuple[int, int]:
+    """Plan key for a data range: the smallest [0, 2^k - 1] holding it (non-negative data), else
+    [-(2^k), 2^k - 1].  Plans are built for the normalised range -- exact for every value inside
+    it (the per-tile range kernel still adapts each tile's tonal length to the data) -- so a new
+    image with a slightly different min/max reuses the cached plan instead of building one."""
+    vmin, vmax = int(vmin), int(vmax)
+    if vmin >= 0:
+        top = 1
+        while top < vmax:
+            top = 2 * top + 1
+        return 0, top
+    m = 1
+    while -m > vmin or m - 1 < vmax:
+        m *= 2
+    return -m, m - 1
 
-    def __init__(self, capacity: int = 16):
+
+class _PlanCache:
+    """LRU of plans keyed by everything fm_plan_create depends on, bounded by the device scratch
+    the cached plans hold (default 24 GiB, FM_PLAN_CACHE_GIB), not by their count.  A plan whose
+    creation runs out of device memory evicts every cached plan and is retried once."""
+
+    def __init__(self, capacity: int = 32, max_bytes: int | None = None):
+        import os
         self.capacity = capacity
+        self.max_bytes = max_bytes if max_bytes is not None else int(
+            float(os.environ.get("FM_PLAN_CACHE_GIB", "24")) * (1 << 30))
         self._d: collections.OrderedDict = collections.OrderedDict()
         self._mu = threading.Lock()
+
+    @staticmethod
+    def _bytes(p: MorphPlan) -> int:
+        return int(p.info.get("scratch_bytes", 0))
+
+    def held_bytes(self) -> int:
+        with self._mu:
+            return sum(self._bytes(p) for p in self._d.values())
+
+    def _evict_locked(self, need: int = 0):
+        while self._d and (len(self._d) >= self.capacity or
+                           sum(self._bytes(p) for p in self._d.values()) + need > self.max_bytes):
+            _, old = self._d.popitem(last=False)
+            old.close()
 
     def get(self, **kw) -> MorphPlan:
         sev = np.ascontiguousarray(np.asarray(kw["se_values"], dtype=np.int64))
@@ -212,18 +288,22 @@ class _PlanCache:
                bool(kw.get("crop", True)), str(kw.get("img_dtype")), int(kw.get("img_min", 0)),
                int(kw.get("img_max", 255)), int(kw.get("fill", 0)), int(kw.get("batch", 1)),
                str(kw.get("device")), int(kw.get("tile", 0)), int(kw.get("tonal_len", 0)),
-               str(kw.get("out_dtype", torch.int32)), int(kw.get("scratch_bytes", 0)))
+               str(kw.get("out_dtype", torch.int32)), int(kw.get("scratch_bytes", 0)),
+               bool(kw.get("counts", False)))
         with self._mu:
             p = self._d.get(key)
             if p is not None:
                 self._d.move_to_end(key)
                 return p
-        p = MorphPlan(**kw)
+        try:
+            p = MorphPlan(**kw)
+        except MemoryError:
+            self.clear()
+            torch.cuda.empty_cache()
+            p = MorphPlan(**kw)
         with self._mu:
+            self._evict_locked(self._bytes(p))
             self._d[key] = p
-            while len(self._d) > self.capacity:
-                _, old = self._d.popitem(last=False)
-                old.close()
         return p
 
     def clear(self) -> None:

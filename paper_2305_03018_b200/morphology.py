@@ -66,23 +66,43 @@ def _run_fft(f: GridFunction, b: GridFunction, *, mode: str, crop: bool, fill: i
              stats: dict | None):
     dev = _device()
     img, mask, dt, vmin, vmax = _upload(f, dev)
-    # narrowest output element type holding every possible result (fewer bytes
-    # back over the bus; widened to int64 on the host like the reference's)
-    bmin, bmax = b.min_defined(), b.max_defined()
-    if mode == "dilate":
-        olo, ohi = min(fill, vmin + bmin), max(fill, vmax + bmax)
-    else:
-        olo, ohi = min(fill, vmin - bmax), max(fill, vmax - bmin)
-    if 0 <= olo and ohi <= 255:
-        odt = torch.uint8
-    elif -32768 <= olo and ohi <= 32767:
-        odt = torch.int16
-    else:
-        odt = torch.int32
-    plan = engine.plan_cache.get(
-        shape=f.shape, se_values=b.values, se_defined=None if b.gap_free else b.defined,
-        se_lo=b.lo, mode=mode, crop=crop, img_dtype=dt, img_min=vmin, img_max=vmax,
-        fill=fill, batch=1, device=dev, out_dtype=odt)
+    # plans are keyed on the normalised range [0, 2^k - 1] holding the data (the per-tile
+    # range kernel adapts every tile's tonal length to the data itself), so images of one
+    # bit depth share a cached plan; the exact range is the fallback when the wider one
+    # exceeds a tonal-length limit
+    def get(pmin, pmax):
+        # narrowest output element type holding every possible result (fewer bytes
+        # back over the bus; widened to int64 on the host like the reference's)
+        bmin, bmax = b.min_defined(), b.max_defined()
+        if mode == "dilate":
+            olo, ohi = min(fill, pmin + bmin), max(fill, pmax + bmax)
+        else:
+            olo, ohi = min(fill, pmin - bmax), max(fill, pmax - bmin)
+        if 0 <= olo and ohi <= 255:
+            odt = torch.uint8
+        elif -32768 <= olo and ohi <= 32767:
+            odt = torch.int16
+        else:
+            odt = torch.int32
+        return engine.plan_cache.get(
+            shape=f.shape, se_values=b.values, se_defined=None if b.gap_free else b.defined,
+            se_lo=b.lo, mode=mode, crop=crop, img_dtype=dt, img_min=pmin, img_max=pmax,
+            fill=fill, batch=1, device=dev, out_dtype=odt)
+    nmin, nmax = engine.normalized_range(vmin, vmax)
+    if mode == "erode":
+        # erode_fft passes l as the fill; the erosion encode uses the plan's max (exact for
+        # any bound >= the data max), kept <= l so the fill stays the largest output
+        nmax = min(nmax, max(vmax, fill))
+    if dt == torch.uint8:
+        nmax = min(nmax, 255)
+    elif dt == torch.uint16:
+        nmax = min(nmax, 65535)
+    try:
+        plan = get(nmin, nmax)
+    except NotImplementedError:
+        if (nmin, nmax) == (vmin, vmax):
+            raise
+        plan = get(vmin, vmax)
     plan.reset_stats()
     out, valid = plan.execute(img.unsqueeze(0), None if mask is None else mask.unsqueeze(0))
     dev_max = plan.read_stats()          # raises ArithmeticError at >= 0.25 (fft_conv.py:145-148)

@@ -63,17 +63,32 @@ def _bounds(img: torch.Tensor, defined, img_min, img_max):
     return int(img_min), int(img_max)
 
 
-def _run(mode, img, se, se_lo, se_defined, defined, img_min, img_max, fill, out_dtype):
+def _run(mode, img, se, se_lo, se_defined, defined, img_min, img_max, fill, out_dtype, *, data_bounds=False):
     se_v, se_d, se_lo, smin, _ = _se_arrays(se, se_defined, se_lo)
     if smin < 0:
         raise ValueError("tonal lift needs non-negative values")
     x = _batched(img, se_v.ndim)
     lo, hi = _bounds(x, defined, img_min, img_max)
     x, dt = _img_dtype(x, lo, hi)
-    plan = engine.plan_cache.get(shape=tuple(x.shape[1:]), se_values=se_v, se_defined=se_d, se_lo=se_lo,
-                                 mode=mode, crop=True, img_dtype=dt, img_min=lo, img_max=hi,
-                                 fill=fill, batch=x.shape[0], device=x.device, out_dtype=out_dtype)
     dmask = None if defined is None else _batched(defined, se_v.ndim)
+
+    def get(pmin, pmax):
+        return engine.plan_cache.get(shape=tuple(x.shape[1:]), se_values=se_v, se_defined=se_d, se_lo=se_lo,
+                                     mode=mode, crop=True, img_dtype=dt, img_min=pmin, img_max=pmax,
+                                     fill=fill, batch=x.shape[0], device=x.device, out_dtype=out_dtype)
+    if data_bounds and img_min is None and img_max is None:
+        # bounds measured from the data: plan on the normalised range (a cached plan serves
+        # every batch of that bit depth; tiles still adapt to the data), exact range fallback
+        nmin, nmax = engine.normalized_range(lo, hi)
+        if mode == "erode":
+            nmax = min(nmax, max(hi, fill))
+        nmax = min(nmax, {torch.uint8: 255, torch.uint16: 65535}.get(dt, nmax))
+        try:
+            plan = get(nmin, nmax)
+        except (NotImplementedError, ValueError):
+            plan = get(lo, hi)
+    else:
+        plan = get(lo, hi)
     out, valid = plan.execute(x, dmask)
     if img.dim() == se_v.ndim:
         out, valid = out[0], valid[0]
@@ -83,7 +98,8 @@ def _run(mode, img, se, se_lo, se_defined, defined, img_min, img_max, fill, out_
 def dilate(img, se, se_lo=None, *, se_defined=None, defined=None, img_min=None, img_max=None,
            out_dtype=torch.int32):
     """Exact dilation of a CUDA image or batch; returns (values, validity)."""
-    return _run("dilate", img, se, se_lo, se_defined, defined, img_min, img_max, 0, out_dtype)
+    return _run("dilate", img, se, se_lo, se_defined, defined, img_min, img_max, 0, out_dtype,
+                data_bounds=True)
 
 
 def erode(img, se, se_lo=None, *, l=None, se_defined=None, defined=None, img_min=None, img_max=None,
@@ -95,6 +111,8 @@ def erode(img, se, se_lo=None, *, l=None, se_defined=None, defined=None, img_min
         l = hi
     if l < hi:
         raise ValueError(f"l={l} below max value {hi}")
+    if img_min is None and img_max is None:
+        return _run("erode", img, se, se_lo, se_defined, defined, None, None, int(l), out_dtype, data_bounds=True)
     return _run("erode", img, se, se_lo, se_defined, defined, lo, hi, int(l), out_dtype)
 
 
