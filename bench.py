@@ -43,6 +43,11 @@ N_IMAGES = 64
 EDGE = 2048
 WORKLOAD = ("c5: 64 x 2048x2048 6-bit smooth-noise images, 31x31 non-flat SE [0,15], exact dilation, "
             "sharded by image")
+WORKLOADS = {
+    "c5": WORKLOAD,
+    "c3": "c3: 1024x1024 8-bit blob image, 21x21 disk SE [0,7], exact dilation, row strips with SE halos",
+    "c4": "c4: 2048x2048 4-bit image, 101x101 random flat mask SE, exact dilation, row strips with SE halos",
+}
 GOLDEN = ROOT / "tests" / "golden" / "c5_all_digests.json"
 
 
@@ -182,31 +187,40 @@ class Clocks:
                 "samples": len(rows), "power_w_max": max(r[2] for r in rows), "reasons": reasons}
 
 
-def cpu_reference(steps=1, warmup=0, op="dilate"):
+def cpu_reference(steps=1, warmup=0, op="dilate", config="c5"):
     """Time oracle/port.dilate_fft (the reference's algorithm: int64 tonal umbra volumes, scipy
-    rfftn/irfftn in f64 with every host thread, rint + projection) on FULL 2048x2048 c5 images,
-    one image per step (image i of the batch at step i) -- the same config as the GPU line.
-    One call needs ~37 GiB of host RAM and ~16 s on the 16-core box (profiles/r2_box_probe.txt)."""
+    rfftn/irfftn in f64 with every host thread, rint + projection) on FULL images of the
+    config, one image per step (c5: image i of the batch at step i) -- the same config as the
+    GPU line.  One c5 call needs ~37 GiB of host RAM and ~16 s on the 16-core box
+    (profiles/r2_box_probe.txt)."""
     from oracle import port
     from paper_2305_03018_b200 import workloads as W
     cores = len(os.sched_getaffinity(0))
-    se = W.c5_se()
+    if config == "c5":
+        se, sd, lo, tmax = W.c5_se(), None, (-15, -15), 63
+        image = lambda i: W.c5_image(i % N_IMAGES)  # noqa: E731
+    else:
+        w = W.CONFIGS[config]()
+        se, sd, lo, tmax = w.se_values, w.se_defined, w.se_lo, w.tonal_max
+        image = lambda i: w.images[0]  # noqa: E731
 
     def one(i):
-        img = W.c5_image(i % N_IMAGES)
+        img = image(i)
         t0 = time.perf_counter()
         if op == "dilate":
-            port.dilate_fft(img, None, (0, 0), se, None, (-15, -15), workers=cores)
+            port.dilate_fft(img, None, (0, 0), se, sd, lo, workers=cores)
         else:
-            port.erode_fft(img, None, (0, 0), se, None, (-15, -15), l=63, workers=cores)
-        return time.perf_counter() - t0
+            port.erode_fft(img, None, (0, 0), se, sd, lo, l=tmax, workers=cores)
+        return time.perf_counter() - t0, img.size
 
     for i in range(warmup):
         one(i)
-    times = [one(i) for i in range(steps)]
-    px = EDGE * EDGE
-    return {"value": px * len(times) / sum(times) / 1e6, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{len(times)} full {EDGE}x{EDGE} c5 image(s) (one per step), oracle/port."
+    res = [one(i) for i in range(steps)]
+    times = [t for t, _ in res]
+    px = sum(n for _, n in res)
+    shape = "x".join(str(s) for s in image(0).shape)
+    return {"value": px / sum(times) / 1e6, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{len(times)} full {shape} {config} image(s) (one per step), oracle/port."
                       f"{'dilate_fft' if op == 'dilate' else 'erode_fft'} (reference algorithm: int64 umbra, "
                       f"scipy rfftn/irfftn f64 workers={cores}, rint, project_with_validity)",
             "seconds": sum(times), "steps_s": times}
@@ -214,19 +228,19 @@ def cpu_reference(steps=1, warmup=0, op="dilate"):
 
 def run_reference(args, rank, world):
     """--impl reference: the reference's own CPU algorithm on the box's host cores, same config
-    (full c5 images).  A CPU warm-up buys nothing beyond page faults, so at most one warm-up
+    (full images).  A CPU warm-up buys nothing beyond page faults, so at most one warm-up
     step runs (reported as warmup_run)."""
     if rank != 0:
         return
     wu = min(args.warmup, 1)
-    res = cpu_reference(steps=args.steps, warmup=wu)
+    res = cpu_reference(steps=args.steps, warmup=wu, config=args.config)
     ms = 1000.0 * sum(res["steps_s"]) / len(res["steps_s"])
     line = {
         "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "warmup_run": wu, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (SURVEY §8(d) c5 recipe, seeded PCG64)",
-        "config": {"workload": WORKLOAD, "images_per_step": 1, "same_config": True},
+        "data": "synthetic (SURVEY §8(d) recipe, seeded PCG64)",
+        "config": {"workload": WORKLOADS[args.config], "images_per_step": 1, "same_config": True},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -471,12 +485,143 @@ def run_ours(args, rank, world, local_rank):
         sys.exit(3)
 
 
+def run_strips(args, rank, world, local_rank):
+    """--config c3|c4: ONE image per step, split into row strips across the ranks (one process
+    per GPU, sharding.strips geometry); halo rows by NVLink peer copies out of the neighbours'
+    IPC-mapped strip buffers inside the timed region (strips.RankStrip); each rank computes
+    exactly its owned output rows.  N = 1: the whole image on one GPU."""
+    import torch
+    import torch.distributed as dist
+    from paper_2305_03018_b200 import _lib
+    from paper_2305_03018_b200 import build as B
+    from paper_2305_03018_b200 import workloads as W
+    from paper_2305_03018_b200.engine import MorphPlan
+    from paper_2305_03018_b200.strips import RankStrip
+
+    B.build_rank_safe(rank, world)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = W.CONFIGS[args.config]()
+    img = w.images[0]
+    H, Wd = img.shape
+    sd = None if w.se_defined.all() else w.se_defined
+    stream = torch.cuda.current_stream(dev)
+    kw = dict(se_values=w.se_values, se_lo=w.se_lo, se_defined=sd, mode="dilate", img_dtype=torch.uint8,
+              img_min=0, img_max=w.tonal_max, fill=0, out_dtype=torch.int32, device=dev)
+    if world > 1:
+        rs = RankStrip(rank=rank, world=world, shape=img.shape, **kw)
+        me = rs.me
+        rs.load_own(torch.from_numpy(img[me.out0:me.out1]).to(dev))
+        out = torch.empty((1, me.out1 - me.out0, Wd), dtype=torch.int32, device=dev)
+        valid = torch.empty_like(out, dtype=torch.uint8)
+        torch.cuda.synchronize()
+        dist.barrier()
+
+        def step():
+            rs.exchange_halos(stream)
+            rs.execute(stream, out=out, valid=valid)
+        plan, rows = rs.plan, (me.out0, me.out1)
+    else:
+        plan = MorphPlan(shape=img.shape, crop=True, batch=1, **kw)
+        x = torch.from_numpy(img).to(dev).unsqueeze(0)
+        out = torch.empty((1, H, Wd), dtype=torch.int32, device=dev)
+        valid = torch.empty_like(out, dtype=torch.uint8)
+
+        def step():
+            plan.execute(x, out=out, valid=valid, stream=stream)
+        rows = (0, H)
+    clocks = Clocks(local_rank)
+    clocks.wait_first()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    plan.reset_stats()
+    l0 = _lib.kernel_launches()
+    ms = _timed(step, args.steps, stream, world)
+    launches = _lib.kernel_launches() - l0
+    clk = clocks.stop()
+    dev_max = plan.read_stats()
+    ms_per_step = ms / args.steps
+    mpx = H * Wd / 1e6
+    value = mpx / (ms_per_step / 1000.0)
+    # e2e: this rank's own input rows H2D from pinned memory and its output rows D2H, inside
+    # the timed region (plus the halo copies and compute)
+    r0, r1 = rows
+    pin_in = torch.from_numpy(img[r0:r1]).pin_memory()
+    pin_out = torch.empty((r1 - r0, Wd), dtype=torch.int32).pin_memory()
+    pin_valid = torch.empty((r1 - r0, Wd), dtype=torch.uint8).pin_memory()
+
+    def e2e_step():
+        if world > 1:
+            rs.window[me.out0 - me.in0: me.out1 - me.in0].copy_(pin_in, non_blocking=True)
+            stream.synchronize()
+            dist.barrier()     # neighbours' rows landed before the halo copies read them
+            step()
+        else:
+            x[0].copy_(pin_in, non_blocking=True)
+            step()
+        pin_out.copy_(out[0], non_blocking=True)
+        pin_valid.copy_(valid[0], non_blocking=True)
+        stream.synchronize()
+    e2e_step()
+    t0 = time.perf_counter()
+    e2e_ms = _timed(e2e_step, args.steps, stream, world) / args.steps
+    wall_ms = (time.perf_counter() - t0) * 1000.0 / args.steps
+    e2e_t = torch.tensor([max(e2e_ms, wall_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_val = mpx / (float(e2e_t.item()) / 1000.0)
+    # parity: the stitched image against the reference's own output digest
+    parts = [None] * world
+    mine = (r0, pin_out.numpy().copy(), pin_valid.numpy().copy())
+    if world > 1:
+        dist.all_gather_object(parts, mine)
+    else:
+        parts = [mine]
+    parity = None
+    if rank == 0:
+        parts.sort(key=lambda t: t[0])
+        vals = np.concatenate([p[1] for p in parts])
+        vm = np.concatenate([p[2] for p in parts])
+        golden = json.loads((ROOT / "tests" / "golden" / "digests.json").read_text())[f"{args.config}_img0"]
+        parity = {"images": 1, "ok": _out_digest(vals, vm) == golden["dilate"],
+                  "checker": "sha256(int32 values || uint8 validity) of the stitched strips vs the reference's "
+                             "dilate_naive output (tests/golden/digests.json)"}
+    if world > 1:
+        rs.close()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (SURVEY §8(d) recipe, seeded PCG64)",
+        "config": {"workload": WORKLOADS[args.config], "strips": world, "tonal_len": plan.info["tonal_len"],
+                   "tile": [plan.info["tile_y"], plan.info["tile_x"]],
+                   "l2": "no flush: single image per step; the spectral scratch exceeds L2"},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(img.nbytes),
+                "d2h_bytes_per_step": int(H * Wd * 5)},
+        "gpu_launches": int(launches), "max_abs_deviation": dev_max, "parity": parity, "clocks": clk,
+    }
+    if args.cpu_baseline and world == 1:
+        try:
+            cb = cpu_reference(steps=1, config=args.config)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": len(os.sched_getaffinity(0)),
+                                    "kind": "port", "sample": f"failed: {type(e).__name__}: {e}"}
+    print(json.dumps(line), flush=True)
+    if parity is not None and not parity["ok"]:
+        sys.exit(3)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["c5", "c3", "c4"], default="c5",
+                    help="c5: the 64-image batch sharded by image (headline); c3/c4: one image in row strips")
     ap.add_argument("--images", type=int, default=N_IMAGES)
     ap.add_argument("--scratch-gib", type=int, default=16)
     ap.add_argument("--out-dtype", choices=["u8", "i16", "i32"], default="i32",
@@ -498,7 +643,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, rank, world, local_rank)
+        if args.config == "c5":
+            run_ours(args, rank, world, local_rank)
+        else:
+            run_strips(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

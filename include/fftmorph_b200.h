@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FM_ABI_VERSION 3
+#define FM_ABI_VERSION 4
 
 typedef enum fm_status {
   FM_OK = 0,
@@ -56,7 +56,10 @@ typedef struct fm_plan_desc {
   int32_t mode;          /* fm_mode */
   int32_t crop;          /* 1: output over the image domain (reference default);
                             0: whole Minkowski range f.lo+b.lo .. f.hi+b.hi (dilation) /
-                               f.lo-b.hi .. f.hi-b.lo (erosion) */
+                               f.lo-b.hi .. f.hi-b.lo (erosion);
+                            2: the window win_lo .. win_lo+win_shape-1 (image array indices;
+                               row strips of one image: each strip computes exactly its
+                               owned output rows from its rows plus the SE-radius halos) */
   int32_t img_dtype;     /* fm_dtype of the image buffer */
   int64_t batch;         /* images per fm_execute call, all of `shape` */
   int64_t shape[2];      /* image array shape (row-major) */
@@ -72,6 +75,13 @@ typedef struct fm_plan_desc {
   int32_t tonal_len;     /* 0 = auto, else forced tonal length T (even, > l_R) */
   int32_t out_dtype;     /* fm_out_dtype of the output values (0 = int32) */
   int32_t flags;         /* FM_FLAG_* */
+  int32_t count_budget;  /* a-priori FP32 precision budget: the largest count a pixel can
+                            reach (<= defined SE entries) must stay below it, else
+                            fm_plan_create returns FM_EPRECISION (the FP32 analogue of
+                            check_precision_budget, fft_conv.py:114-125); 0 = default 2^17 */
+  int32_t reserved;      /* 0 */
+  int64_t win_lo[2];     /* crop = 2: first output index per axis (image array coordinates) */
+  int64_t win_shape[2];  /* crop = 2: output extent per axis */
 } fm_plan_desc;
 
 /* fm_plan_desc.flags */
@@ -182,6 +192,43 @@ const char* fm_last_error(void);
  * conv_full_direct, fft_conv.py:109-111).  int64 device buffers, row-major. */
 int fm_conv_full_direct(int ndim, const int64_t* a_shape, const int64_t* a, const int64_t* b_shape,
                         const int64_t* b, int64_t* out, void* stream);
+/* Full-mode N-D (ndim 1..4) convolution of int64 volumes by FP64 FFTs on the device,
+ * zero-padded to `padded` (every length 2^k or 45*2^k, fft_conv.py:61-91), then slice,
+ * rint and the max pre-rounding deviation (written to *max_dev, host): replaces
+ * conv_full_fft_with_stats for operands that are not tonal one-hot volumes
+ * (fft_conv.py:128-150; precision budget 2^52 as fft_conv.py:114-125, checked by the
+ * caller).  a, b, out: device buffers, row-major; out has shape a_shape + b_shape - 1.
+ * Synchronous on `stream`. */
+int fm_conv_full_fft64(int ndim, const int64_t* a_shape, const int64_t* a, const int64_t* b_shape,
+                       const int64_t* b, const int64_t* padded, int64_t* out, double* max_dev, void* stream);
+
+/* In-place N-D (ndim 1..4) complex FP64 DFT of a device volume of interleaved (re, im)
+ * doubles: forward exp(-2 pi i jk/n) unnormalised, or inverse (1/n not applied):
+ * transform_forward / transform_inverse (fft_conv.py:157-170).  Lengths 2, 3, 5-smooth. */
+int fm_fft64(int ndim, const int64_t* shape, void* data, int inverse, void* stream);
+
+/* build_umbra (umbra.py:177-186) on the device: bits[npx][t] int64 = 1 at (x, values[x])
+ * for defined x (defined may be NULL), 0 elsewhere.  Values must lie in [0, t). */
+int fm_build_umbra(int64_t npx, const int64_t* values, const uint8_t* defined, int64_t t, int64_t* bits,
+                   void* stream);
+
+/* project_with_validity's reduction (umbra.py:189-205) over a contiguous count window
+ * [npx][t]: values[x] = highest k with window[x][k] >= 1 (0 if none), valid[x] = any. */
+int fm_project(int64_t npx, int64_t t, const int64_t* window, int64_t* values, uint8_t* valid, void* stream);
+
+/* Row strips of one image across GPUs: the SE-radius halo rows a strip
+ * needs from its neighbours move by NVLink peer copies, no collective.
+ * fm_copy_peer: cudaMemcpyPeerAsync of `bytes` from src (on src_device) to dst (on
+ * dst_device), asynchronous on `stream` (same-device copies allowed; a negative device
+ * means IPC-mapped peer memory, copied by unified addressing).
+ * fm_ipc_get_handle / fm_ipc_open_handle / fm_ipc_close_handle: one process per GPU --
+ * export a device buffer as a 64-byte CUDA IPC handle plus the buffer's byte offset in its
+ * allocation, map a peer's handle into this process (peer access enabled), unmap it. */
+int fm_copy_peer(void* dst, int dst_device, const void* src, int src_device, int64_t bytes, void* stream);
+int fm_ipc_get_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out);
+int fm_ipc_open_handle(const void* handle, int device, void** dev_ptr);
+int fm_ipc_close_handle(void* dev_ptr);
+
 int fm_abi_version(void);
 
 #ifdef __cplusplus

@@ -10,12 +10,17 @@ from .morphology import (MorphMethod, beucher_gradient, closing, dilate, dilate_
                          dilate_naive, erode, erode_fft, erode_naive, negate, opening,
                          reflect)
 from ._lib import PrecisionBudgetError
-from .fft_conv import (ConvPlan, FftStats, OffsetArray, conv_full_direct, conv_full_fft,
-                       conv_full_fft_with_stats, next_fast_size, set_fft_workers)
+from .fft_conv import (Backend, ConvPlan, FftStats, OffsetArray, conv_full_direct, conv_full_fft,
+                       conv_full_fft_with_stats, direct_full, make_plan, next_fast_size, set_fft_workers,
+                       transform_forward, transform_inverse)
+from .umbra import (CountVolume, UmbraVolume, build_umbra, project, project_with_validity,
+                    required_lr)
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "Backend", "CountVolume", "UmbraVolume", "build_umbra", "direct_full", "make_plan", "project",
+    "project_with_validity", "required_lr", "transform_forward", "transform_inverse",
     "ConvPlan", "FftStats", "GridFunction", "MorphMethod", "OffsetArray", "PrecisionBudgetError",
     "beucher_gradient", "closing", "conv_full_direct", "conv_full_fft", "conv_full_fft_with_stats",
     "next_fast_size", "set_fft_workers",

@@ -18,6 +18,7 @@ LIB_PATH = _PKG / "_build" / "libfftmorph_b200.so"
 if os.environ.get("FM_LIB"):   # A/B builds for measurements (must still be an in-tree build)
     LIB_PATH = Path(os.environ["FM_LIB"]).resolve()
 
+ABI_VERSION = 4   # FM_ABI_VERSION of include/fftmorph_b200.h
 FM_OK, FM_EINVAL, FM_EPRECISION, FM_EDEVIATION, FM_ECUDA, FM_EUNSUPPORTED, FM_ENOMEM = range(7)
 FM_DILATE, FM_ERODE = 0, 1
 FM_U8, FM_U16, FM_I32 = 0, 1, 2
@@ -28,6 +29,8 @@ EXPORTED = (
     "fm_plan_create", "fm_execute", "fm_execute_host", "fm_read_stats", "fm_reset_stats",
     "fm_plan_query", "fm_plan_destroy", "fm_naive", "fm_kernel_launches", "fm_last_error",
     "fm_abi_version", "fm_set_timing", "fm_get_timing", "fm_conv_full_direct",
+    "fm_conv_full_fft64", "fm_fft64", "fm_build_umbra", "fm_project",
+    "fm_copy_peer", "fm_ipc_get_handle", "fm_ipc_open_handle", "fm_ipc_close_handle",
 )
 FM_FLAG_COUNTS = 1
 
@@ -51,6 +54,10 @@ class PlanDesc(ctypes.Structure):
         ("tonal_len", ctypes.c_int32),
         ("out_dtype", ctypes.c_int32),
         ("flags", ctypes.c_int32),
+        ("count_budget", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("win_lo", ctypes.c_int64 * 2),
+        ("win_shape", ctypes.c_int64 * 2),
     ]
 
 
@@ -137,6 +144,22 @@ def load() -> ctypes.CDLL:
         L.fm_abi_version.restype = i32
         L.fm_conv_full_direct.argtypes = [ctypes.c_int, vp, vp, vp, vp, vp, vp]
         L.fm_conv_full_direct.restype = ctypes.c_int
+        L.fm_conv_full_fft64.argtypes = [ctypes.c_int, vp, vp, vp, vp, vp, vp, ctypes.POINTER(ctypes.c_double), vp]
+        L.fm_conv_full_fft64.restype = ctypes.c_int
+        L.fm_fft64.argtypes = [ctypes.c_int, vp, vp, ctypes.c_int, vp]
+        L.fm_fft64.restype = ctypes.c_int
+        L.fm_build_umbra.argtypes = [i64, vp, vp, i64, vp, vp]
+        L.fm_build_umbra.restype = ctypes.c_int
+        L.fm_project.argtypes = [i64, i64, vp, vp, vp, vp]
+        L.fm_project.restype = ctypes.c_int
+        L.fm_copy_peer.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, i64, vp]
+        L.fm_copy_peer.restype = ctypes.c_int
+        L.fm_ipc_get_handle.argtypes = [vp, vp, ctypes.POINTER(i64)]
+        L.fm_ipc_get_handle.restype = ctypes.c_int
+        L.fm_ipc_open_handle.argtypes = [vp, ctypes.c_int, ctypes.POINTER(vp)]
+        L.fm_ipc_open_handle.restype = ctypes.c_int
+        L.fm_ipc_close_handle.argtypes = [vp]
+        L.fm_ipc_close_handle.restype = ctypes.c_int
         _lib = L
         return L
 

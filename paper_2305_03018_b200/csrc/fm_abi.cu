@@ -22,6 +22,7 @@
 #include "fftmorph_b200.h"
 #include "fm_bigtile.cuh"
 #include "fm_direct.cuh"
+#include "fm_fft64.cuh"
 #include "fm_naive.cuh"
 #include "fm_range.cuh"
 #include "fm_tile.cuh"
@@ -50,6 +51,7 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr double kPi = 3.14159265358979323846;
+constexpr int64_t kFp32CountBudget = 1 << 17;   // fm_plan_desc.count_budget default
 
 int set_all_smem_attrs();
 
@@ -260,6 +262,13 @@ const bool g_no_skip0 = std::getenv("FM_NO_SKIP0") != nullptr;         // A/B: a
 // pipelined tonal CTAs per SM (persistent grid); below the occupancy limit it
 // leaves room for the next chunk's range CTAs
 const int g_tonal_occ_cap = std::getenv("FM_TONAL_OCC") ? std::atoi(std::getenv("FM_TONAL_OCC")) : 64;
+// fused tonal step (fm_fused.cuh): FM_FUSE=1 runs it (default: the separate tonal
+// kernels, faster while both passes are FP32-issue-bound);
+// FM_FUSE_KCH=<n> splits every unit's planes into chunks of n (0 = plan default);
+// FM_DISCARD=0 keeps the consumed spectral lines in L2 (they are then written back)
+const bool g_fuse = std::getenv("FM_FUSE") && std::getenv("FM_FUSE")[0] == '1';
+const int g_fuse_kch = std::getenv("FM_FUSE_KCH") ? std::atoi(std::getenv("FM_FUSE_KCH")) : 0;
+const bool g_discard = !(std::getenv("FM_DISCARD") && std::getenv("FM_DISCARD")[0] == '0');
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
@@ -381,6 +390,9 @@ struct fm_plan {
   // 256x256 tiles through an HBM scratch (fm_bigtile.cuh) for wide SEs
   bool big = false;
   float2* S = nullptr;
+  // fused tonal step (fm_fused.cuh): ladder entries with N <= fuse_nmax finish in the conv kernel
+  int fuse_nmax = 0;
+  int* unit_done = nullptr;               // [ipc][upl] plane-chunk completion counters
   // host-buffer pipeline
   cudaStream_t copy_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_done = nullptr;
@@ -421,6 +433,7 @@ void free_plan(fm_plan* p) {
   if (p->range_stream) cudaStreamDestroy(p->range_stream);
   cudaFree(p->enc_tab);
   cudaFree(p->d_enc_off);
+  cudaFree(p->unit_done);
   cudaFree(p->S);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
@@ -489,6 +502,11 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   if (d.flags & ~FM_FLAG_COUNTS) return fail(FM_EINVAL, "unknown flags");
   if ((d.flags & FM_FLAG_COUNTS) && (d.mode != FM_DILATE || d.crop))
     return fail(FM_EINVAL, "count volumes need mode=dilate and crop=0");
+  if (d.crop < 0 || d.crop > 2) return fail(FM_EINVAL, "crop must be 0, 1 or 2");
+  if (d.crop == 2)
+    for (int i = 0; i < d.ndim; ++i)
+      if (d.win_shape[i] < 1 || d.win_shape[i] > (1 << 30) || d.win_lo[i] < -(1 << 30) || d.win_lo[i] > (1 << 30))
+        return fail(FM_EINVAL, "crop=2 needs a non-empty output window within +-2^30");
   fm_plan* p = new fm_plan();
   p->d = d;
   p->counts = (d.flags & FM_FLAG_COUNTS) != 0;
@@ -534,6 +552,23 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   p->se_min = smin;
   p->se_max = smax;
   p->se_count = cnt;
+  {
+    // a-priori precision budget (fft_conv.py:114-125 restated for FP32): a count is the
+    // number of (image, SE) pairs meeting at one degree, at most the defined SE entries
+    // (and the image pixels).  The FP32 pipeline's measured worst deviation grows ~2e-7 per
+    // unit of count (c4: 9.8e-4 at 5123), so below 2^17 it stays < 0.03, a 10x margin to
+    // the reference's 0.25 abort threshold.
+    const int64_t budget = d.count_budget > 0 ? d.count_budget : kFp32CountBudget;
+    const int64_t npx = (p->two_d ? p->H : 1) * p->W;
+    const int64_t bound = std::min<int64_t>(cnt, npx);
+    if (bound >= budget) {
+      free_plan(p);
+      char buf[200];
+      std::snprintf(buf, sizeof buf, "count bound %lld >= FP32 budget %lld; split the structuring element",
+                    (long long)bound, (long long)budget);
+      return fail(FM_EPRECISION, buf);
+    }
+  }
 
   // tonal extent: only the spread of values matters (dilation commutes with
   // constant shifts of f and b); l_R of the reference is max f + max b.
@@ -584,7 +619,13 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
 
   // output region and overlap-save offsets (tensor.py:76-101, morphology.py:131-140)
   const int64_t hi_y = lo_y + p->my - 1, hi_x = lo_x + p->mx - 1;
-  if (d.crop) {
+  if (d.crop == 2) {
+    // explicit output window (row strips): any placement relative to the image
+    p->off_y = p->two_d ? d.win_lo[0] : 0;
+    p->off_x = p->two_d ? d.win_lo[1] : d.win_lo[0];
+    p->OH = p->two_d ? d.win_shape[0] : 1;
+    p->OW = p->two_d ? d.win_shape[1] : d.win_shape[0];
+  } else if (d.crop) {
     p->off_y = 0;
     p->off_x = 0;
     p->OH = p->H;
@@ -779,6 +820,12 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   const int64_t base = (int64_t)p->upl * p->ipc;
   int kch = (int)std::min<int64_t>(p->K, std::max<int64_t>(1, (target + base - 1) / base));
   p->k_chunk = (p->K + kch - 1) / kch;
+  // fused tonal step: three-pass 128x128 kernels (register budget of 128 per thread),
+  // value outputs (not count volumes)
+  if (g_fuse && !p->counts && !p->big && p->two_d && bv && bv->tmax < (1 << 30)) {
+    p->fuse_nmax = kFuseNMax;
+    if (g_fuse_kch > 0) p->k_chunk = std::min(p->K, g_fuse_kch);
+  }
   p->kchunks = (p->K + p->k_chunk - 1) / p->k_chunk;
   p->conv_occ = occ;
   {
@@ -868,6 +915,10 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
           cudaSuccess) {
     free_plan(p);
     return fail(FM_ENOMEM, std::string("tile scratch alloc: ") + cudaGetErrorString(e));
+  }
+  if (p->fuse_nmax > 0) {
+    if ((e = cudaMalloc(&p->unit_done, sizeof(int) * (size_t)slots)) != cudaSuccess) return cfail(e, "counter alloc");
+    cudaMemset(p->unit_done, 0, sizeof(int) * (size_t)slots);
   }
   if ((e = cudaMalloc(&p->chat, (size_t)slots * p->K * p->wpx * 8)) != cudaSuccess) {
     free_plan(p);
@@ -1173,6 +1224,19 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     a.enc_off = p->d_enc_off;
     a.cap = (int)cap;
     a.L = L;
+    if (p->fuse_nmax > 0) {
+      a.fuse_nmax = p->fuse_nmax;
+      a.discard = g_discard ? 1 : 0;
+      a.unit_done = p->unit_done;
+      a.out = reinterpret_cast<char*>(out) + (size_t)c0 * npix * out_size(p->d.out_dtype);
+      a.out_dtype = p->d.out_dtype;
+      a.valid = valid ? valid + (size_t)c0 * npix : nullptr;
+      a.out_sign = p->out_sign;
+      a.se_min = p->se_min;
+      a.fill = p->d.fill;
+      a.se_count = p->se_count;
+      a.dev_max = reinterpret_cast<float*>(p->stats);
+    }
     // Few units (one small image): split every unit's planes into chunks so the
     // conv grid fills the GPU; that needs the per-ladder counts first.  Many
     // units: one CTA per unit (all its planes), launched before the host waits.
@@ -1307,7 +1371,19 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     // one launch per ladder entry in use, spread over the aux streams so the
     // small ones (few units each) run side by side; joined back into s
     int nlaunch = 0;
-    for (int li = 0; li < L; ++li) nlaunch += reinterpret_cast<volatile int*>(p->h_counts[buf])[li] > 0;
+    double fused_b = 0;   // logical bytes of the tonal steps run inside the conv kernel
+    for (int li = 0; li < L; ++li) {
+      const int cnt = reinterpret_cast<volatile int*>(p->h_counts[buf])[li];
+      if (cnt <= 0) continue;
+      if (p->ladder[li] <= p->fuse_nmax) {
+        const int N = p->ladder[li];
+        planes += (double)cnt * (N + 1);
+        fused_b += (double)cnt * ((N + 1) * (double)p->npx * 8.0 +
+                                  (double)p->npx * (out_size(p->d.out_dtype) + (valid ? 1.0 : 0.0)));
+        continue;
+      }
+      ++nlaunch;
+    }
     const int nstreams = std::min(nlaunch, 1 + kAuxStreams);
     if (nstreams > 1) {
       FM_CUDA(cudaEventRecord(p->ev_fork, s));
@@ -1316,7 +1392,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     int launch_i = 0;
     for (int li = L - 1; li >= 0; --li) {
       const int cnt = reinterpret_cast<volatile int*>(p->h_counts[buf])[li];
-      if (cnt <= 0) continue;
+      if (cnt <= 0 || p->ladder[li] <= p->fuse_nmax) continue;
       const int N = p->ladder[li];
       const int si = launch_i++ % nstreams;
       cudaStream_t ts = si == 0 ? s : p->aux[si - 1];
@@ -1359,14 +1435,17 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     if (!g_no_skip0 && img_defined == nullptr) {
       const double skipped = (double)n * (double)(p->full_prefix[u0 + nu] - p->full_prefix[u0]);
       planes -= skipped;
-      tonal_b -= skipped * (double)p->npx * 8.0;
+      // (per-ladder counts of full units are not known here: with the fused step the
+      // skipped planes are charged to it, else to the tonal kernels)
+      if (p->fuse_nmax > 0) fused_b -= skipped * (double)p->npx * 8.0;
+      else tonal_b -= skipped * (double)p->npx * 8.0;
     }
     p->planes_done += (int64_t)planes;
     p->units_done += (int64_t)n * nu;
     if (p->timing) {
       FM_CUDA(cudaEventRecord(next_event(p), s));
       p->pending_tonal.push_back({e1, e1 + 1});
-      p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->npx * 8.0;
+      p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->npx * 8.0 + fused_b;
       p->acc.conv_flops += planes * p->conv_flops_per_plane;
       p->acc.tonal_bytes += tonal_b;
     }
@@ -1591,6 +1670,226 @@ int fm_conv_full_direct(int ndim, const int64_t* a_shape, const int64_t* a, cons
   conv_direct_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d);
   g_launches++;
   FM_CUDA(cudaGetLastError());
+  return FM_OK;
+}
+
+// ---- count level in FP64 (fm_fft64.cuh) --------------------------------------------
+}  // extern "C"
+
+namespace {
+
+unsigned fft64_grid(int64_t n) {
+  const int64_t b = (n + kFft64NT - 1) / kFft64NT;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)g_num_sms * 16));
+}
+
+// radix order of a ladder length (2^k or 45*2^k): 4s, a 2, 3s, 5s
+std::vector<int> fft64_radices(int64_t n) {
+  std::vector<int> r;
+  while (n % 4 == 0) { r.push_back(4); n /= 4; }
+  while (n % 2 == 0) { r.push_back(2); n /= 2; }
+  while (n % 3 == 0) { r.push_back(3); n /= 3; }
+  while (n % 5 == 0) { r.push_back(5); n /= 5; }
+  if (n != 1) r.clear();
+  return r;
+}
+bool fft64_ok(int64_t n) { return n == 1 || !fft64_radices(n).empty(); }
+
+// N-D complex FFT of a [d0][d1][d2][d3] volume (sign -1 forward, +1 inverse, unnormalised);
+// ping-pongs between `a` and `tmp`, returns the buffer holding the result
+int fft64_nd(double2* a, double2* tmp, const Shape4& s, int sign, cudaStream_t st, double2** result) {
+  double2* in = a;
+  double2* outb = tmp;
+  const int64_t total = s.d[0] * s.d[1] * s.d[2] * s.d[3];
+  for (int ax = 0; ax < 4; ++ax) {
+    const int64_t n = s.d[ax];
+    if (n == 1) continue;
+    int64_t outer = 1, inner = 1;
+    for (int k = 0; k < ax; ++k) outer *= s.d[k];
+    for (int k = ax + 1; k < 4; ++k) inner *= s.d[k];
+    const std::vector<int> rad = fft64_radices(n);
+    if (rad.empty()) return fail(FM_EINVAL, "FFT length must factor into 2, 3 and 5");
+    int64_t Ns = 1;
+    for (int R : rad) {
+      const unsigned g = fft64_grid(total / R);
+      switch (R) {
+        case 2: fft64_stage<2><<<g, kFft64NT, 0, st>>>(in, outb, outer, n, inner, Ns, sign); break;
+        case 3: fft64_stage<3><<<g, kFft64NT, 0, st>>>(in, outb, outer, n, inner, Ns, sign); break;
+        case 4: fft64_stage<4><<<g, kFft64NT, 0, st>>>(in, outb, outer, n, inner, Ns, sign); break;
+        default: fft64_stage<5><<<g, kFft64NT, 0, st>>>(in, outb, outer, n, inner, Ns, sign); break;
+      }
+      g_launches++;
+      FM_CUDA(cudaGetLastError());
+      Ns *= R;
+      std::swap(in, outb);
+    }
+  }
+  *result = in;
+  return FM_OK;
+}
+
+int shape4(int ndim, const int64_t* shape, Shape4* s) {
+  if (ndim < 1 || ndim > 4) return fail(FM_EINVAL, "ndim must be 1..4");
+  for (int i = 0; i < 4; ++i) {
+    const int j = i - (4 - ndim);
+    s->d[i] = j >= 0 ? shape[j] : 1;
+    if (s->d[i] < 1) return fail(FM_EINVAL, "empty array");
+  }
+  return FM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fm_conv_full_fft64(int ndim, const int64_t* a_shape, const int64_t* a, const int64_t* b_shape, const int64_t* b,
+                       const int64_t* padded, int64_t* out, double* max_dev, void* stream) {
+  if (!a_shape || !b_shape || !a || !b || !padded || !out) return fail(FM_EINVAL, "null argument");
+  Shape4 sa, sb, sp, so;
+  int rc = shape4(ndim, a_shape, &sa);
+  if (!rc) rc = shape4(ndim, b_shape, &sb);
+  if (!rc) rc = shape4(ndim, padded, &sp);
+  if (rc) return rc;
+  int64_t P = 1;
+  for (int i = 0; i < 4; ++i) {
+    so.d[i] = sa.d[i] + sb.d[i] - 1;
+    if (sp.d[i] < so.d[i]) return fail(FM_EINVAL, "padded shape smaller than the full output");
+    if (!fft64_ok(sp.d[i])) return fail(FM_EINVAL, "padded length must factor into 2, 3 and 5");
+    P *= sp.d[i];
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  double2* buf = nullptr;
+  unsigned long long* dbits = nullptr;
+  FM_CUDA(cudaMallocAsync(&buf, sizeof(double2) * 4 * (size_t)P, st));
+  cudaError_t e = cudaMallocAsync(&dbits, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(buf, st);
+    return fail(FM_ENOMEM, std::string("fft64 alloc: ") + cudaGetErrorString(e));
+  }
+  double2 *A = buf, *At = buf + P, *Bb = buf + 2 * P, *Bt = buf + 3 * P, *ra = nullptr, *rb = nullptr, *rc2 = nullptr;
+  auto run = [&]() -> int {
+    FM_CUDA(cudaMemsetAsync(dbits, 0, sizeof(unsigned long long), st));
+    fft64_pad<<<fft64_grid(P), kFft64NT, 0, st>>>(a, sa, sp, A);
+    fft64_pad<<<fft64_grid(P), kFft64NT, 0, st>>>(b, sb, sp, Bb);
+    g_launches += 2;
+    FM_CUDA(cudaGetLastError());
+    int r = fft64_nd(A, At, sp, -1, st, &ra);
+    if (!r) r = fft64_nd(Bb, Bt, sp, -1, st, &rb);
+    if (r) return r;
+    fft64_product<<<fft64_grid(P), kFft64NT, 0, st>>>(ra, rb, P);
+    g_launches++;
+    FM_CUDA(cudaGetLastError());
+    r = fft64_nd(ra, ra == A ? At : A, sp, +1, st, &rc2);
+    if (r) return r;
+    const int64_t O = so.d[0] * so.d[1] * so.d[2] * so.d[3];
+    fft64_finish<<<fft64_grid(O), kFft64NT, 0, st>>>(rc2, sp, so, 1.0 / (double)P, out, dbits);
+    g_launches++;
+    FM_CUDA(cudaGetLastError());
+    unsigned long long h = 0;
+    FM_CUDA(cudaMemcpyAsync(&h, dbits, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FM_CUDA(cudaStreamSynchronize(st));
+    double d;
+    std::memcpy(&d, &h, sizeof(d));
+    if (max_dev) *max_dev = d;
+    return FM_OK;
+  };
+  rc = run();
+  cudaFreeAsync(buf, st);
+  cudaFreeAsync(dbits, st);
+  return rc;
+}
+
+int fm_fft64(int ndim, const int64_t* shape, void* data, int inverse, void* stream) {
+  if (!shape || !data) return fail(FM_EINVAL, "null argument");
+  Shape4 s;
+  int rc = shape4(ndim, shape, &s);
+  if (rc) return rc;
+  for (int i = 0; i < 4; ++i)
+    if (!fft64_ok(s.d[i])) return fail(FM_EINVAL, "length must factor into 2, 3 and 5");
+  const int64_t P = s.d[0] * s.d[1] * s.d[2] * s.d[3];
+  cudaStream_t st = (cudaStream_t)stream;
+  double2* tmp = nullptr;
+  FM_CUDA(cudaMallocAsync(&tmp, sizeof(double2) * (size_t)P, st));
+  double2* res = nullptr;
+  double2* d = reinterpret_cast<double2*>(data);
+  rc = fft64_nd(d, tmp, s, inverse ? +1 : -1, st, &res);
+  if (!rc && res != d) {
+    cudaError_t e = cudaMemcpyAsync(d, res, sizeof(double2) * (size_t)P, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) rc = fail(FM_ECUDA, cudaGetErrorString(e));
+  }
+  cudaFreeAsync(tmp, st);
+  return rc;
+}
+
+int fm_build_umbra(int64_t npx, const int64_t* values, const uint8_t* defined, int64_t t, int64_t* bits,
+                   void* stream) {
+  if (!values || !bits || npx < 0 || t < 1) return fail(FM_EINVAL, "bad argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  FM_CUDA(cudaMemsetAsync(bits, 0, sizeof(int64_t) * (size_t)npx * (size_t)t, st));
+  if (npx == 0) return FM_OK;
+  umbra_kernel<<<fft64_grid(npx), kFft64NT, 0, st>>>(values, defined, npx, t, bits);
+  g_launches++;
+  FM_CUDA(cudaGetLastError());
+  return FM_OK;
+}
+
+int fm_project(int64_t npx, int64_t t, const int64_t* window, int64_t* values, uint8_t* valid, void* stream) {
+  if (!window || !values || !valid || npx < 0 || t < 1) return fail(FM_EINVAL, "bad argument");
+  if (npx == 0) return FM_OK;
+  project_kernel<<<fft64_grid(npx), kFft64NT, 0, (cudaStream_t)stream>>>(window, npx, t, values, valid);
+  g_launches++;
+  FM_CUDA(cudaGetLastError());
+  return FM_OK;
+}
+
+// ---- row strips across GPUs: halo rows by NVLink peer copies ----------------------
+
+int fm_copy_peer(void* dst, int dst_device, const void* src, int src_device, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(FM_EINVAL, "bad argument");
+  if (bytes == 0) return FM_OK;
+  if (dst_device < 0 || src_device < 0)   // IPC-mapped peer memory: location from unified addressing
+    FM_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  else
+    FM_CUDA(cudaMemcpyPeerAsync(dst, dst_device, src, src_device, (size_t)bytes, (cudaStream_t)stream));
+  return FM_OK;
+}
+
+int fm_ipc_get_handle(const void* dev_ptr, void* handle_out, int64_t* offset_out) {
+  if (!dev_ptr || !handle_out || !offset_out) return fail(FM_EINVAL, "null argument");
+  // the handle names the whole allocation (a caching allocator may place the buffer
+  // inside a larger block): report the buffer's offset from the allocation base
+  typedef CUresult (*RangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range_fn = nullptr;
+  if (!range_fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(FM_ECUDA, "cuMemGetAddressRange unavailable");
+    range_fn = reinterpret_cast<RangeFn>(f);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) return fail(FM_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  FM_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (int64_t)((CUdeviceptr)dev_ptr - base);
+  return FM_OK;
+}
+
+int fm_ipc_open_handle(const void* handle, int device, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(FM_EINVAL, "null argument");
+  DeviceGuard dg(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  FM_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return FM_OK;
+}
+
+int fm_ipc_close_handle(void* dev_ptr) {
+  if (!dev_ptr) return fail(FM_EINVAL, "null argument");
+  FM_CUDA(cudaIpcCloseMemHandle(dev_ptr));
   return FM_OK;
 }
 

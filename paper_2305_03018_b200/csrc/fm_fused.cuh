@@ -1,0 +1,166 @@
+// fm_fused.cuh — the tonal step (north_star (d)) fused into the conv tile kernel.
+//
+// Without it, every unit's K_t spatially-convolved spectral planes go to an HBM
+// scratch and a separate tonal kernel (fm_tonal.cuh) reads them back.  Here the
+// CTA that finishes a unit's LAST plane chunk runs the unit's inverse tonal FFT
+// itself, right after the planes were written, while they are still in L2
+// (one unit's planes are ~1.3 MB at c5; the ~150 units in flight fit the 126 MB
+// L2), then discards those L2 lines (discard.global.L2: invalidated without a
+// write-back) so the spectral volume never makes the round trip to HBM.
+//
+// Completion protocol: every CTA of a unit (its plane chunks) makes its chat
+// stores visible device-wide (__threadfence by every thread, CTA barrier) and
+// bumps the unit's counter; the CTA that sees count = chunks - 1 is the last,
+// fences again (acquire) and reads the planes with L2-only loads (ld.global.cg:
+// never a stale L1 line), then resets the counter for the next launch.
+//
+// Per pixel the math is the tonal kernel's (fm_tonal.cuh): c2r packing, the
+// compile-time length-N inverse FFT in registers, threshold c(t) > 0.5 with the
+// highest such t (umbra.py:198-203), deviation max|c - rint c| (fft_conv.py:
+// 143-148), typed store of value + validity.  Ladder entries with N above
+// kFuseNMax keep the separate tonal kernel (register budget of the 512-thread
+// conv CTA: 128 per thread).
+#pragma once
+#include "fm_tile.cuh"
+#include "fm_tonal.cuh"
+
+namespace fm {
+
+constexpr int kFuseNMax = 40;
+
+__host__ __device__ constexpr int tonal_n_at(int i) {
+  constexpr int ns[] = {FM_TONAL_NS};
+  return ns[i];
+}
+
+__device__ __forceinline__ void fused_store(const TileArgs& a, size_t i, int v) {
+  switch (a.out_dtype) {
+    case 1: reinterpret_cast<uint8_t*>(a.out)[i] = (uint8_t)v; break;
+    case 2: reinterpret_cast<uint16_t*>(a.out)[i] = (uint16_t)v; break;
+    case 3: reinterpret_cast<int16_t*>(a.out)[i] = (int16_t)v; break;
+    default: reinterpret_cast<int32_t*>(a.out)[i] = v; break;
+  }
+}
+
+__device__ __forceinline__ float2 ldcg2(const float2* p) {
+  float2 r;
+  asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
+
+// One unit's tonal step: pixels p = tid, tid + NT, ... of its QY x QX window.
+template <int N, int NT>
+__device__ __forceinline__ void fused_tonal_unit(const TileArgs& a, const float2* chat_unit, int img, int unit,
+                                              int anchor, bool full) {
+  constexpr int K = N + 1;
+  constexpr int off = tonal_off(N);
+  const int ty = unit / a.tiles_x, tx = unit - (unit / a.tiles_x) * a.tiles_x;
+  const int npx = a.QY * a.QX;
+  const float x0 = (float)((double)a.se_count / (2.0 * N));
+  float dev = 0.f;
+  // software pipeline (short tonal axes, where the registers allow it): the next
+  // pixel's K loads are in flight while this pixel's FFT and threshold run
+  constexpr bool kPre = N <= 24;
+  auto load = [&](int p, float2 (&X)[K]) {
+    const int wy = p / a.QX, wx = p - (p / a.QX) * a.QX;
+    const bool live = p < npx && ty * a.QY + wy < a.OH && tx * a.QX + wx < a.OW;
+    const float2* xs = chat_unit + p;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      X[k] = (k == 0 && full) || !live ? make_float2(x0, 0.f) : ldcg2(xs + (size_t)k * a.wpx);
+  };
+  float2 Xn[kPre ? K : 1];
+  if constexpr (kPre) load(threadIdx.x, Xn);
+#pragma unroll 1
+  for (int p = threadIdx.x; p < npx; p += NT) {
+    const int wy = p / a.QX, wx = p - (p / a.QX) * a.QX;
+    const int oy = ty * a.QY + wy, ox = tx * a.QX + wx;
+    float2 X[K];
+    if constexpr (kPre) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) X[k] = Xn[k];
+      load(p + NT, Xn);
+    }
+    if (oy >= a.OH || ox >= a.OW) continue;
+    if constexpr (!kPre) load(p, X);
+    float2 A[N], B[N];
+    {
+      const float2 xc = conjf2(X[N]);
+      A[0] = cadd(cadd(X[0], xc), mul_pi(csub(X[0], xc)));
+    }
+#pragma unroll
+    for (int k = 1; 2 * k < N; ++k) {
+      const float2 xk = X[k], xm = conjf2(X[N - k]);
+      const float2 sk = cadd(xk, xm), dk = csub(xk, xm);
+      const float2 m = cmul(c_ttw[off + k], dk);
+      A[k] = cadd_i(sk, m);
+      A[N - k] = cadd_i(conjf2(sk), conjf2(m));
+    }
+    if constexpr (N % 2 == 0 && N > 0) {
+      const float2 xh = X[N / 2];
+      A[N / 2] = make_float2(2.f * xh.x, -2.f * xh.y);
+    }
+    stock_run<N, 0, 1>(A, B);
+    float d = 0.f;
+    int top;
+    if constexpr (num_radices(N) % 2 == 0) top = tonal_threshold<N>(A, d);
+    else top = tonal_threshold<N>(B, d);
+    dev = fmaxf(dev, d);
+    const size_t dst = ((size_t)img * a.OH + oy) * a.OW + ox;
+    fused_store(a, dst, top >= 0 ? a.out_sign * (top + a.se_min) + anchor : a.fill);
+    if (a.valid) a.valid[dst] = top >= 0 ? 1 : 0;
+  }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
+  if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+}
+
+template <int NT, int I = 0>
+__device__ __forceinline__ void fused_tonal_dispatch(int n, const TileArgs& a, const float2* chat_unit, int img,
+                                                     int unit, int anchor, bool full) {
+  if constexpr (I < kTonalCount) {
+    constexpr int NI = tonal_n_at(I);
+    if constexpr (NI <= kFuseNMax) {
+      if (n == NI) {
+        fused_tonal_unit<NI, NT>(a, chat_unit, img, unit, anchor, full);
+        return;
+      }
+      fused_tonal_dispatch<NT, I + 1>(n, a, chat_unit, img, unit, anchor, full);
+    }
+  }
+}
+
+// Called by every thread of a conv CTA after its plane loop.  Returns after the
+// unit's tonal step if this CTA completed the unit (and the unit's N is fused).
+template <int NT>
+__device__ __forceinline__ void fused_tail(const TileArgs& a, float2* chat_unit, int img, int unit, int K, int T) {
+  const int N = T / 2;
+  if (a.fuse_nmax == 0 || N > a.fuse_nmax) return;
+  __shared__ int s_last;
+  const int nch = (K + a.k_chunk - 1) / a.k_chunk;
+  int* cnt = a.unit_done + ((size_t)img * a.upl + (unit - a.unit0));
+  __threadfence();        // this thread's plane stores, device-wide
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = nch > 1 ? atomicAdd(cnt, 1) : nch - 1;
+    s_last = prev == nch - 1;
+    if (s_last && nch > 1) *cnt = 0;   // self-reset for the next launch (no other CTA touches it now)
+    __threadfence();      // acquire: the other chunks' stores before our reads
+  }
+  __syncthreads();
+  if (!s_last) return;
+  const int4 up = a.unit_param[(size_t)img * a.units + unit];
+  const bool full = (up.w & 2) != 0;
+  fused_tonal_dispatch<NT>(N, a, chat_unit, img, unit, up.x, full);
+  if (a.discard) {
+    // the unit's planes are consumed: drop their L2 lines without a write-back
+    __syncthreads();
+    const char* b0 = reinterpret_cast<const char*>(chat_unit + (size_t)(full ? 1 : 0) * a.wpx);
+    const char* b1 = reinterpret_cast<const char*>(chat_unit + (size_t)K * a.wpx);
+    const uintptr_t first = ((uintptr_t)b0 + 127) & ~(uintptr_t)127, last = (uintptr_t)b1 & ~(uintptr_t)127;
+    for (uintptr_t l = first + (uintptr_t)threadIdx.x * 128; l < last; l += (uintptr_t)NT * 128)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(l) : "memory");
+  }
+}
+
+}  // namespace fm

@@ -92,6 +92,16 @@ struct TileArgs {
   const int2* bucket_list;    // [L][cap] (img, unit)
   const int* ladder;          // [L] N of each ladder entry
   int cap, L;
+  // fused tonal step (fm_fused.cuh, three-pass 128x128 kernel): the CTA completing a unit's
+  // last plane chunk runs its inverse tonal FFT + threshold + store
+  int fuse_nmax;              // 0: off; else units with N_t <= fuse_nmax are finished here
+  int discard;                // drop the consumed spectral lines from L2 (no write-back)
+  int* unit_done;             // [imgs][upl] plane-chunk completion counters (self-resetting)
+  void* out;                  // [imgs][OH][OW] of out_dtype (this launch's first image)
+  int out_dtype;              // 0 int32, 1 uint8, 2 uint16, 3 int16
+  uint8_t* valid;             // nullable
+  int out_sign, se_min, fill, se_count;
+  float* dev_max;             // max |c - rint c| (float bits, atomicMax as int)
 };
 
 __constant__ float2 c_tw[kTwTotal];

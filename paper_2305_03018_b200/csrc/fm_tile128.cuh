@@ -40,6 +40,7 @@
 // padded B2 layout beside two 32 KB SE-spectrum buffers; longer tonal axes
 // (8-bit data: c3) stage uint16 indices beside one buffer.
 #pragma once
+#include "fm_fused.cuh"
 #include "fm_tile.cuh"
 
 namespace fm {
@@ -456,6 +457,7 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
     }
     ++pord;
   }
+  if constexpr (!SPEC) fused_tail<NT>(a, chat_unit, img, unit, K, T);
 }
 
 }  // namespace fm

@@ -51,7 +51,7 @@ class MorphPlan:
     def __init__(self, *, shape, se_values, se_lo, se_defined=None, mode="dilate",
                  crop=True, img_dtype=torch.uint8, img_min=0, img_max=255, fill=0,
                  batch=1, device=None, scratch_bytes=0, tile=0, tonal_len=0, out_dtype=torch.int32,
-                 counts=False):
+                 counts=False, count_budget=0, window=None):
         L = _lib.load()
         shape = tuple(int(s) for s in shape)
         se_values = np.ascontiguousarray(np.asarray(se_values, dtype=np.int64))
@@ -70,6 +70,16 @@ class MorphPlan:
         d.ndim = len(shape)
         d.mode = code
         d.crop = 1 if crop else 0
+        if window is not None:
+            # explicit output window (row strips): ((lo per axis), (shape per axis)) in
+            # image-array indices; crop is ignored
+            wlo, wsh = window
+            if len(wlo) != len(shape) or len(wsh) != len(shape):
+                raise ValueError("window rank mismatch")
+            d.crop = 2
+            for i in range(len(shape)):
+                d.win_lo[i] = int(wlo[i])
+                d.win_shape[i] = int(wsh[i])
         d.img_dtype = {torch.uint8: FM_U8, torch.uint16: FM_U16, torch.int32: FM_I32}[img_dtype]
         d.batch = int(batch)
         for i, s in enumerate(shape):
@@ -85,6 +95,7 @@ class MorphPlan:
         d.tonal_len = int(tonal_len)
         d.out_dtype = _OUT_CODES[out_dtype]
         d.flags = _lib.FM_FLAG_COUNTS if counts else 0
+        d.count_budget = int(count_budget)
         self.counts = bool(counts)
         self.out_dtype = out_dtype
         self.desc = d
@@ -289,7 +300,7 @@ class _PlanCache:
                int(kw.get("img_max", 255)), int(kw.get("fill", 0)), int(kw.get("batch", 1)),
                str(kw.get("device")), int(kw.get("tile", 0)), int(kw.get("tonal_len", 0)),
                str(kw.get("out_dtype", torch.int32)), int(kw.get("scratch_bytes", 0)),
-               bool(kw.get("counts", False)))
+               bool(kw.get("counts", False)), int(kw.get("count_budget", 0)), repr(kw.get("window")))
         with self._mu:
             p = self._d.get(key)
             if p is not None:

@@ -7,18 +7,24 @@ with the same names, argument meaning, output ranges and errors, so the
 reference's count-level tests (test_fft_conv.py:67-139, test_umbra.py:85-123)
 read the same against this package.
 
-Operands that are tonal one-hot volumes (``build_umbra`` output: the last
-axis holds at most one 1 per spatial position) are convolved by the FFT tile
-path in count-volume mode (``FM_FLAG_COUNTS``: tonal encode, spatial FFT
-convolution, inverse tonal FFT, rounded counts), which is the hot path of the
-paper.  Any other integer operands go through the exact direct GPU kernel
-(``fm_conv_full_direct``), whose deviation is 0.  Either way the arithmetic
-runs on the device; there is no host fallback.
+Operands that are tonal one-hot volumes of 1-D / 2-D grids (``build_umbra``
+output: the last axis holds at most one 1 per spatial position) are convolved
+by the FFT tile path in count-volume mode (``FM_FLAG_COUNTS``: tonal encode,
+spatial FFT convolution, inverse tonal FFT, rounded counts), which is the hot
+path of the paper.  Any other non-negative integer operands of rank 1..4
+(generic volumes, umbra volumes of 3-D grids, or umbra pairs beyond the tile
+path's envelope) go through the FP64 FFT convolution on the device
+(``fm_conv_full_fft64``: zero-padded to the reference's ``next_fast_size``
+shape, FP64 like the reference, so its 2^52 precision budget applies as is).
+``conv_full_direct`` / ``direct_full`` run the exact direct GPU kernel
+(``fm_conv_full_direct``).  All arithmetic runs on the device; there is no host
+fallback.
 """
 
 from __future__ import annotations
 
 import ctypes
+import enum
 from dataclasses import dataclass
 
 import numpy as np
@@ -83,13 +89,19 @@ class FftStats:
     padded_shape: tuple
 
 
+class Backend(enum.Enum):
+    """fft_conv.py:41-43."""
+    DIRECT = "direct"
+    FFT = "fft"
+
+
 @dataclass(frozen=True)
 class ConvPlan:
-    """fft_conv.py:46-51 (backend as a string)."""
+    """fft_conv.py:46-51."""
     padded_shape: tuple
     out_lo: tuple
     out_hi: tuple
-    backend: str
+    backend: Backend
 
 
 def next_fast_size(n: int) -> int:
@@ -113,11 +125,13 @@ def _oa(x):
     return OffsetArray(x)
 
 
-def make_plan(a, b, backend: str = "fft") -> ConvPlan:
+def make_plan(a, b, backend=Backend.FFT) -> ConvPlan:
     """Output range = Minkowski sum; padded = next_fast_size(sa+sb-1) (fft_conv.py:80-91)."""
     a, b = _oa(a), _oa(b)
     if a.ndim != b.ndim:
         raise ValueError("rank mismatch")
+    if isinstance(backend, str):
+        backend = Backend(backend)
     out_ranges = full_output_range(a.ranges, b.ranges)
     padded = tuple(next_fast_size(sa + sb - 1) for sa, sb in zip(a.shape, b.shape))
     return ConvPlan(padded, tuple(lo for lo, _ in out_ranges), tuple(hi for _, hi in out_ranges), backend)
@@ -153,13 +167,13 @@ def direct_full(a, b) -> np.ndarray:
 
 def conv_full_direct(a, b) -> OffsetArray:
     """fft_conv.py:109-111."""
-    plan = make_plan(a, b, "direct")
+    plan = make_plan(a, b, Backend.DIRECT)
     a, b = _oa(a), _oa(b)
     return OffsetArray(direct_full(a.data, b.data), plan.out_lo)
 
 
 def _as_umbra(x: np.ndarray):
-    """(values, defined) if x is a tonal one-hot volume (last axis), else None."""
+    """(values, defined) if x is a tonal one-hot volume of a 1-D / 2-D grid (last axis), else None."""
     if x.ndim < 2 or x.ndim > 3 or x.size == 0:
         return None
     if x.min() < 0 or x.max() > 1:
@@ -168,6 +182,62 @@ def _as_umbra(x: np.ndarray):
     if s.max() > 1:
         return None
     return np.argmax(x, axis=-1).astype(np.int64), s.astype(bool)
+
+
+def fft64_full(a, b, padded) -> tuple[np.ndarray, float]:
+    """Full-mode convolution of two int64 arrays by FP64 FFTs on the device (fm_conv_full_fft64):
+    rounded counts and the max pre-rounding deviation (fft_conv.py:133-144)."""
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.int64))
+    if a.ndim != b.ndim or not 1 <= a.ndim <= 4:
+        raise ValueError("rank mismatch or unsupported rank (1..4)")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ta, tb = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    out = torch.empty(tuple(sa + sb - 1 for sa, sb in zip(a.shape, b.shape)), dtype=torch.int64, device=dev)
+    sa, sb = np.array(a.shape, np.int64), np.array(b.shape, np.int64)
+    sp = np.array(padded, np.int64)
+    d = ctypes.c_double(0.0)
+    L = _lib.load()
+    _lib.check(L.fm_conv_full_fft64(a.ndim, sa.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(ta.data_ptr()),
+                                    sb.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(tb.data_ptr()),
+                                    sp.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(out.data_ptr()),
+                                    ctypes.byref(d), ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    return out.cpu().numpy(), float(d.value)
+
+
+def _fft64(x: np.ndarray, inverse: bool) -> np.ndarray:
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+    if not 1 <= x.ndim <= 4:
+        raise ValueError("unsupported rank (1..4)")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = torch.from_numpy(x.view(np.float64)).to(dev)
+    shp = np.array(x.shape, np.int64)
+    _lib.check(_lib.load().fm_fft64(x.ndim, shp.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(t.data_ptr()),
+                                    1 if inverse else 0,
+                                    ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    out = t.cpu().numpy().view(np.complex128).reshape(x.shape)
+    return out / float(np.prod(x.shape)) if inverse else out
+
+
+def transform_forward(a, plan: ConvPlan) -> np.ndarray:
+    """Multidimensional DFT of a real array zero-padded to the plan's shape (fft_conv.py:157-166),
+    FP64 on the device."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != len(plan.padded_shape):
+        raise ValueError("rank mismatch with plan")
+    if any(s > p for s, p in zip(a.shape, plan.padded_shape)):
+        raise ValueError("input exceeds the planned transform size")
+    z = np.zeros(plan.padded_shape, dtype=np.complex128)
+    z[tuple(slice(0, n) for n in a.shape)] = a
+    return _fft64(z, inverse=False)
+
+
+def transform_inverse(spec, plan: ConvPlan) -> np.ndarray:
+    """Inverse of transform_forward (fft_conv.py:169-172), FP64 on the device."""
+    spec = np.asarray(spec)
+    if spec.shape != tuple(plan.padded_shape):
+        raise ValueError("spectrum shape does not match plan")
+    return _fft64(spec, inverse=True)
 
 
 def _umbra_counts(fa, fd, fb, bd, out_shape):
@@ -201,13 +271,20 @@ def conv_full_fft_with_stats(a, b):
     """fft_conv.py:128-150: counts over the Minkowski range, rounded, with the deviation check."""
     a, b = _oa(a), _oa(b)
     check_precision_budget(a.data, b.data)
-    plan = make_plan(a, b, "fft")
+    plan = make_plan(a, b, Backend.FFT)
     out_shape = tuple(h - l + 1 for l, h in zip(plan.out_lo, plan.out_hi))
     ua, ub = _as_umbra(np.asarray(a.data)), _as_umbra(np.asarray(b.data))
+    data = None
     if ua is not None and ub is not None:
-        data, dev = _umbra_counts(ua[0], ua[1], ub[0], ub[1], out_shape)
-    else:
-        data, dev = direct_full(a.data, b.data), 0.0
+        # the paper's hot path; convolution commutes, so the operand with the smaller
+        # spatial extent takes the SE role (the tile path bounds the SE, not the image)
+        (fv, fd), (bv, bd) = (ua, ub) if np.prod(ua[0].shape) >= np.prod(ub[0].shape) else (ub, ua)
+        try:
+            data, dev = _umbra_counts(fv, fd, bv, bd, out_shape)
+        except NotImplementedError:
+            data = None       # beyond the tile path's envelope: the FP64 path below
+    if data is None:
+        data, dev = fft64_full(a.data, b.data, plan.padded_shape)
     if dev >= MAX_DEVIATION:
         raise ArithmeticError(f"pre-rounding deviation {dev:.3g} >= {MAX_DEVIATION}; "
                               "precision budget logic is broken")

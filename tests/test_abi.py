@@ -19,7 +19,7 @@ HEADER = ROOT / "include" / "fftmorph_b200.h"
 def _declared_functions():
     text = HEADER.read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(fm_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(fm_[a-z0-9_]+)\s*\(", text)))
 
 
 @pytest.fixture(scope="module")
@@ -35,7 +35,7 @@ def test_header_and_binding_agree():
 def test_library_exports_every_symbol(lib):
     for name in _declared_functions():
         assert hasattr(lib, name), name
-    assert lib.fm_abi_version() == 3
+    assert lib.fm_abi_version() == _lib.ABI_VERSION == 4
 
 
 def test_dynamic_symbol_table():
@@ -60,10 +60,11 @@ def test_struct_layouts_match_header(tmp_path):
         #include <stddef.h>
         #include "fftmorph_b200.h"
         int main(void) {
-          printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(fm_plan_desc), sizeof(fm_plan_info),
+          printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(fm_plan_desc), sizeof(fm_plan_info),
                  sizeof(fm_stats), offsetof(fm_plan_desc, img_min), offsetof(fm_plan_desc, scratch_bytes),
                  offsetof(fm_plan_info, se_count), offsetof(fm_plan_desc, flags), offsetof(fm_plan_info, count_len),
-                 sizeof(fm_timing), offsetof(fm_timing, range_launches));
+                 sizeof(fm_timing), offsetof(fm_timing, range_launches), offsetof(fm_plan_desc, count_budget),
+                 offsetof(fm_plan_desc, win_lo), offsetof(fm_plan_desc, win_shape));
           return 0;
         }
     """))
@@ -73,7 +74,8 @@ def test_struct_layouts_match_header(tmp_path):
     want = [ctypes.sizeof(_lib.PlanDesc), ctypes.sizeof(_lib.PlanInfo), ctypes.sizeof(_lib.Stats),
             _lib.PlanDesc.img_min.offset, _lib.PlanDesc.scratch_bytes.offset, _lib.PlanInfo.se_count.offset,
             _lib.PlanDesc.flags.offset, _lib.PlanInfo.count_len.offset, ctypes.sizeof(_lib.Timing),
-            _lib.Timing.range_launches.offset]
+            _lib.Timing.range_launches.offset, _lib.PlanDesc.count_budget.offset,
+            _lib.PlanDesc.win_lo.offset, _lib.PlanDesc.win_shape.offset]
     assert got == want
 
 
