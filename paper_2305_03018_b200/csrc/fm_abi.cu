@@ -390,6 +390,12 @@ struct fm_plan {
   // 256x256 tiles through an HBM scratch (fm_bigtile.cuh) for wide SEs
   bool big = false;
   float2* S = nullptr;
+  // composite plan (SE wider than one tile, fm_plan_create): dilation by B = U B_i is the
+  // max over the parts' dilations (erosion: min), validity OR-ed
+  std::vector<fm_plan*> parts;
+  void* part_out = nullptr;               // [batch][OH][OW] of out_dtype
+  uint8_t* part_valid = nullptr;          // [batch][OH][OW]
+  uint8_t* acc_valid = nullptr;           // [batch][OH][OW] when the caller passes no validity
   // fused tonal step (fm_fused.cuh): ladder entries with N <= fuse_nmax finish in the conv kernel
   int fuse_nmax = 0;
   int* unit_done = nullptr;               // [ipc][upl] plane-chunk completion counters
@@ -403,9 +409,14 @@ namespace {
 
 void free_plan(fm_plan* p) {
   if (!p) return;
+  for (fm_plan* q : p->parts) free_plan(q);
+  p->parts.clear();
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(p->device);
+  cudaFree(p->part_out);
+  cudaFree(p->part_valid);
+  cudaFree(p->acc_valid);
   cudaFree(p->spec);
   cudaFree(p->twN);
   cudaFree(p->wT);
@@ -483,6 +494,135 @@ int validate_common(const fm_plan_desc* d) {
 
 }  // namespace
 
+// validity-aware max (dilation) / min (erosion) of a part into the accumulated result
+template <typename T>
+__global__ void combine_kernel(T* __restrict__ out, uint8_t* __restrict__ valid, const T* __restrict__ part,
+                               const uint8_t* __restrict__ pvalid, int64_t n, int erode) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!pvalid[i]) continue;
+    const T v = part[i];
+    if (!valid[i]) {
+      out[i] = v;
+      valid[i] = 1;
+    } else {
+      const T o = out[i];
+      out[i] = erode ? (v < o ? v : o) : (v > o ? v : o);
+    }
+  }
+}
+
+int out_elem_size(int od) { return od == FM_OUT_U8 ? 1 : (od == FM_OUT_U16 || od == FM_OUT_I16) ? 2 : 4; }
+
+// Largest SE extent per axis served by one plan (the 256x256 tile path); wider SEs are
+// split into blocks of at most kSplitEdge (so each block keeps a useful 256-tile window).
+constexpr int kMaxSeEdge = 256;
+constexpr int kSplitEdge = 128;
+
+extern "C" int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* se_values,
+                              const uint8_t* se_defined);
+
+// Composite plan: the SE is cut into blocks B_i (each with its own lo), one plan per non-empty
+// block, all writing the parent's output window (crop = 2); exact because a dilation by a
+// union of SEs is the max of the dilations (erosion: the min), a pixel being valid if any
+// part has a pair there (morphology.py:65-113 semantics per part).
+int create_composite(fm_plan** out_plan, const fm_plan_desc& d, const int32_t* se_values, const uint8_t* se_defined) {
+  const bool two_d = d.ndim == 2;
+  const int64_t my = two_d ? d.se_shape[0] : 1, mx = two_d ? d.se_shape[1] : d.se_shape[0];
+  const int64_t H = two_d ? d.shape[0] : 1, W = two_d ? d.shape[1] : d.shape[0];
+  const int64_t lo_y = two_d ? d.se_lo[0] : 0, lo_x = two_d ? d.se_lo[1] : d.se_lo[0];
+  // the parent's output window, as a single plan would place it (crop / Minkowski range)
+  int64_t wy = 0, wx = 0, oh = H, ow = W;
+  if (d.crop == 2) {
+    wy = two_d ? d.win_lo[0] : 0;
+    wx = two_d ? d.win_lo[1] : d.win_lo[0];
+    oh = two_d ? d.win_shape[0] : 1;
+    ow = two_d ? d.win_shape[1] : d.win_shape[0];
+  } else if (!d.crop) {
+    const bool er = d.mode == FM_ERODE;
+    wy = two_d ? (er ? -(lo_y + my - 1) : lo_y) : 0;
+    wx = er ? -(lo_x + mx - 1) : lo_x;
+    oh = two_d ? H + my - 1 : 1;
+    ow = W + mx - 1;
+  }
+  const int64_t ny = (my + kSplitEdge - 1) / kSplitEdge, nx = (mx + kSplitEdge - 1) / kSplitEdge;
+  const int64_t by = (my + ny - 1) / ny, bx = (mx + nx - 1) / nx;
+  fm_plan* p = new fm_plan();
+  p->d = d;
+  p->device = d.device;
+  p->two_d = two_d;
+  p->batch = d.batch;
+  p->H = H;
+  p->W = W;
+  p->my = (int)my;
+  p->mx = (int)mx;
+  p->OH = oh;
+  p->OW = ow;
+  p->off_y = wy;
+  p->off_x = wx;
+  int smin = INT32_MAX, smax = INT32_MIN, cnt = 0;
+  for (int64_t i = 0; i < my * mx; ++i)
+    if (!se_defined || se_defined[i]) {
+      smin = std::min(smin, se_values[i]);
+      smax = std::max(smax, se_values[i]);
+      ++cnt;
+    }
+  if (cnt == 0) { delete p; return fail(FM_EINVAL, "grid needs at least one defined pixel"); }
+  p->se_min = smin;
+  p->se_max = smax;
+  p->se_count = cnt;
+  for (int64_t y0 = 0; y0 < my; y0 += by)
+    for (int64_t x0 = 0; x0 < mx; x0 += bx) {
+      const int64_t sh = std::min(by, my - y0), sw = std::min(bx, mx - x0);
+      std::vector<int32_t> v((size_t)(sh * sw));
+      std::vector<uint8_t> m((size_t)(sh * sw));
+      bool any = false;
+      for (int64_t yy = 0; yy < sh; ++yy)
+        for (int64_t xx = 0; xx < sw; ++xx) {
+          const int64_t src = (y0 + yy) * mx + (x0 + xx);
+          v[(size_t)(yy * sw + xx)] = se_values[src];
+          m[(size_t)(yy * sw + xx)] = se_defined ? (se_defined[src] ? 1 : 0) : 1;
+          any = any || m[(size_t)(yy * sw + xx)];
+        }
+      if (!any) continue;
+      fm_plan_desc c = d;
+      c.crop = 2;
+      if (two_d) {
+        c.se_shape[0] = sh;
+        c.se_shape[1] = sw;
+        c.se_lo[0] = lo_y + y0;
+        c.se_lo[1] = lo_x + x0;
+        c.win_lo[0] = wy;
+        c.win_lo[1] = wx;
+        c.win_shape[0] = oh;
+        c.win_shape[1] = ow;
+      } else {
+        c.se_shape[0] = sw;
+        c.se_lo[0] = lo_x + x0;
+        c.win_lo[0] = wx;
+        c.win_shape[0] = ow;
+      }
+      fm_plan* q = nullptr;
+      const int rc = fm_plan_create(&q, &c, v.data(), m.data());
+      if (rc) {
+        const std::string msg = g_err;
+        free_plan(p);
+        return fail(rc, "SE block plan: " + msg);
+      }
+      p->parts.push_back(q);
+    }
+  DeviceGuard dg(p->device);
+  const size_t n = (size_t)p->batch * oh * ow;
+  cudaError_t e = cudaMalloc(&p->part_out, n * out_elem_size(d.out_dtype));
+  if (e == cudaSuccess) e = cudaMalloc(&p->part_valid, n);
+  if (e == cudaSuccess) e = cudaMalloc(&p->acc_valid, n);
+  if (e != cudaSuccess) {
+    free_plan(p);
+    return fail(FM_ENOMEM, std::string("composite buffers: ") + cudaGetErrorString(e));
+  }
+  *out_plan = p;
+  return FM_OK;
+}
+
 extern "C" {
 
 int fm_abi_version(void) { return FM_ABI_VERSION; }
@@ -507,6 +647,13 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     for (int i = 0; i < d.ndim; ++i)
       if (d.win_shape[i] < 1 || d.win_shape[i] > (1 << 30) || d.win_lo[i] < -(1 << 30) || d.win_lo[i] > (1 << 30))
         return fail(FM_EINVAL, "crop=2 needs a non-empty output window within +-2^30");
+  {
+    const bool wide = d.ndim == 2 ? (d.se_shape[0] > kMaxSeEdge || d.se_shape[1] > kMaxSeEdge)
+                                  : d.se_shape[0] > kMaxSeEdge;
+    if (wide && (d.flags & FM_FLAG_COUNTS))
+      return fail(FM_EUNSUPPORTED, "count volumes need an SE within one tile (<= 256 per axis)");
+    if (wide) return create_composite(out_plan, d, se_values, se_defined);
+  }
   fm_plan* p = new fm_plan();
   p->d = d;
   p->counts = (d.flags & FM_FLAG_COUNTS) != 0;
@@ -717,7 +864,8 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   // generic tonal kernel (N beyond the compiled set): geometry for N_global
   p->tonal_stride = (p->N + 1) | 1;
   int nt = 128;
-  while (nt > 32 && (size_t)(2 * p->N + 2 * (size_t)nt * p->tonal_stride) * 8 > 200 * 1024) nt -= 32;
+  // long tonal axes (10-11-bit data): fewer pixels per CTA, down to 8 (T up to ~3200)
+  while (nt > 8 && (size_t)(2 * p->N + 2 * (size_t)nt * p->tonal_stride) * 8 > 200 * 1024) nt = nt > 32 ? nt - 32 : nt / 2;
   p->tonal_threads = nt;
   p->tonal_smem = (size_t)(2 * p->N + 2 * (size_t)nt * p->tonal_stride) * 8;
   if (!p->ladder_var.back() && p->tonal_smem > kSmemLimit) {
@@ -1009,6 +1157,29 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
 
 int fm_plan_query(const fm_plan* p, fm_plan_info* info) {
   if (!p || !info) return fail(FM_EINVAL, "null argument");
+  if (!p->parts.empty()) {
+    // composite: geometry of the first block, output / SE facts of the whole plan
+    int rc = fm_plan_query(p->parts[0], info);
+    if (rc) return rc;
+    int64_t scratch = 0;
+    for (const fm_plan* q : p->parts) {
+      fm_plan_info qi;
+      fm_plan_query(q, &qi);
+      scratch += qi.scratch_bytes;
+      info->tonal_len = std::max(info->tonal_len, qi.tonal_len);
+      info->planes = std::max(info->planes, qi.planes);
+      info->l_r = std::max(info->l_r, qi.l_r);
+    }
+    info->out_shape[0] = p->two_d ? p->OH : p->OW;
+    info->out_shape[1] = p->two_d ? p->OW : 0;
+    info->out_lo_offset[0] = p->two_d ? p->off_y : p->off_x;
+    info->out_lo_offset[1] = p->two_d ? p->off_x : 0;
+    info->scratch_bytes = scratch + (int64_t)p->batch * p->OH * p->OW * (out_elem_size(p->d.out_dtype) + 2);
+    info->se_min = p->se_min;
+    info->se_max = p->se_max;
+    info->se_count = p->se_count;
+    return FM_OK;
+  }
   std::memset(info, 0, sizeof(*info));
   info->tonal_len = p->T;
   info->planes = p->K;
@@ -1036,6 +1207,11 @@ int fm_plan_query(const fm_plan* p, fm_plan_info* info) {
 
 int fm_reset_stats(fm_plan* p, void* stream) {
   if (!p) return fail(FM_EINVAL, "null plan");
+  for (fm_plan* q : p->parts) {
+    int rc = fm_reset_stats(q, stream);
+    if (rc) return rc;
+  }
+  if (!p->parts.empty()) return FM_OK;
   DeviceGuard dg(p->device);
   FM_CUDA(cudaMemsetAsync(p->stats, 0, sizeof(int) * 4, (cudaStream_t)stream));
   return FM_OK;
@@ -1458,10 +1634,47 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
   return FM_OK;
 }
 
+static int execute_composite(fm_plan* p, const void* img, const uint8_t* img_defined, void* out, uint8_t* valid,
+                      cudaStream_t s) {
+  p->last_stream = s;
+  uint8_t* acc = valid ? valid : p->acc_valid;
+  const int64_t n = p->batch * p->OH * p->OW;
+  for (size_t i = 0; i < p->parts.size(); ++i) {
+    fm_plan* q = p->parts[i];
+    if (i == 0) {
+      const int rc = run_images(q, img, img_defined, out, acc, s, 0, q->batch);
+      if (rc) return rc;
+      continue;
+    }
+    int rc = run_images(q, img, img_defined, p->part_out, p->part_valid, s, 0, q->batch);
+    if (rc) return rc;
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)g_num_sms * 8));
+    const int er = p->d.mode == FM_ERODE ? 1 : 0;
+    switch (p->d.out_dtype) {
+      case FM_OUT_U8:
+        combine_kernel<uint8_t><<<g, 256, 0, s>>>((uint8_t*)out, acc, (const uint8_t*)p->part_out, p->part_valid, n, er);
+        break;
+      case FM_OUT_U16:
+        combine_kernel<uint16_t><<<g, 256, 0, s>>>((uint16_t*)out, acc, (const uint16_t*)p->part_out, p->part_valid, n, er);
+        break;
+      case FM_OUT_I16:
+        combine_kernel<int16_t><<<g, 256, 0, s>>>((int16_t*)out, acc, (const int16_t*)p->part_out, p->part_valid, n, er);
+        break;
+      default:
+        combine_kernel<int32_t><<<g, 256, 0, s>>>((int32_t*)out, acc, (const int32_t*)p->part_out, p->part_valid, n, er);
+        break;
+    }
+    g_launches++;
+    FM_CUDA(cudaGetLastError());
+  }
+  return FM_OK;
+}
+
 int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, void* out, uint8_t* valid,
                void* stream) {
   if (!p || !img || !out) return fail(FM_EINVAL, "null argument");
   DeviceGuard dg(p->device);
+  if (!p->parts.empty()) return execute_composite(p, img, img_defined, out, valid, (cudaStream_t)stream);
   if (p->counts)
     FM_CUDA(cudaMemsetAsync(out, 0, (size_t)p->batch * p->OH * p->OW * (size_t)(p->lr + 1) * sizeof(int32_t),
                             (cudaStream_t)stream));
@@ -1470,12 +1683,32 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, void* ou
 
 int fm_set_timing(fm_plan* p, int enable) {
   if (!p) return fail(FM_EINVAL, "null plan");
+  for (fm_plan* q : p->parts) fm_set_timing(q, enable);
   p->timing = enable != 0;
   return FM_OK;
 }
 
 int fm_get_timing(fm_plan* p, fm_timing* out, int reset) {
   if (!p) return fail(FM_EINVAL, "null plan");
+  if (!p->parts.empty()) {
+    fm_timing sum{};
+    for (fm_plan* q : p->parts) {
+      fm_timing t{};
+      int rc = fm_get_timing(q, &t, reset);
+      if (rc) return rc;
+      sum.conv_ms += t.conv_ms;
+      sum.tonal_ms += t.tonal_ms;
+      sum.conv_launches += t.conv_launches;
+      sum.tonal_launches += t.tonal_launches;
+      sum.conv_bytes += t.conv_bytes;
+      sum.tonal_bytes += t.tonal_bytes;
+      sum.conv_flops += t.conv_flops;
+      sum.range_ms += t.range_ms;
+      sum.range_launches += t.range_launches;
+    }
+    if (out) *out = sum;
+    return FM_OK;
+  }
   DeviceGuard dg(p->device);
   FM_CUDA(cudaStreamSynchronize(p->last_stream));
   FM_CUDA(cudaDeviceSynchronize());
@@ -1508,6 +1741,23 @@ int fm_get_timing(fm_plan* p, fm_timing* out, int reset) {
 
 int fm_read_stats(fm_plan* p, fm_stats* st) {
   if (!p) return fail(FM_EINVAL, "null plan");
+  if (!p->parts.empty()) {
+    fm_stats acc{0.0, 0};
+    int worst = FM_OK;
+    std::string msg;
+    for (fm_plan* q : p->parts) {
+      fm_stats qs{};
+      const int rc = fm_read_stats(q, &qs);
+      acc.max_abs_deviation = std::max(acc.max_abs_deviation, qs.max_abs_deviation);
+      acc.value_error |= qs.value_error;
+      if (rc && !worst) {
+        worst = rc;
+        msg = g_err;
+      }
+    }
+    if (st) *st = acc;
+    return worst ? fail(worst, msg) : FM_OK;
+  }
   DeviceGuard dg(p->device);
   FM_CUDA(cudaStreamSynchronize(p->last_stream));
   int h[2] = {0, 0};
@@ -1533,6 +1783,28 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, v
   if (p->counts) return fail(FM_EUNSUPPORTED, "count-volume plans run on device buffers (fm_execute)");
   DeviceGuard dg(p->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (!p->parts.empty()) {
+    // composite plan: one staged round trip (no chunk pipeline)
+    const size_t in_b = (size_t)p->batch * p->H * p->W * dtype_size(p->d.img_dtype);
+    const size_t n = (size_t)p->batch * p->OH * p->OW, ob = n * out_elem_size(p->d.out_dtype);
+    char* buf = nullptr;
+    FM_CUDA(cudaMallocAsync(&buf, in_b + (def_host ? (size_t)p->batch * p->H * p->W : 0) + ob + n, s));
+    char* di = buf;
+    uint8_t* dd = def_host ? reinterpret_cast<uint8_t*>(buf + in_b) : nullptr;
+    char* dout = buf + in_b + (def_host ? (size_t)p->batch * p->H * p->W : 0);
+    uint8_t* dv = reinterpret_cast<uint8_t*>(dout + ob);
+    int rc = FM_OK;
+    cudaError_t e = cudaMemcpyAsync(di, img_host, in_b, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && dd) e = cudaMemcpyAsync(dd, def_host, (size_t)p->batch * p->H * p->W, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) rc = execute_composite(p, di, dd, dout, dv, s);
+    if (e == cudaSuccess && !rc) e = cudaMemcpyAsync(out_host_v, dout, ob, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && !rc && valid_host) e = cudaMemcpyAsync(valid_host, dv, n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && !rc) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(buf, s);
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(FM_ECUDA, std::string("composite host path: ") + cudaGetErrorString(e));
+    return FM_OK;
+  }
   const size_t in_n = (size_t)p->batch * p->H * p->W;
   const size_t out_n = (size_t)p->batch * p->OH * p->OW;
   const size_t dsz = dtype_size(p->d.img_dtype);

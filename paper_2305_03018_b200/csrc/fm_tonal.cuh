@@ -486,9 +486,13 @@ __global__ void __launch_bounds__(128) tonal_kernel(const TonalArgs a) {
     if (!crow) store_out(a, pp.dst, top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill);
     if (a.valid) a.valid[pp.dst] = top >= 0 ? 1 : 0;
   }
+  if (blockDim.x >= 32) {
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, off));
-  if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+    for (int off = 16; off > 0; off >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, off));
+    if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+  } else if (dev > 0.f) {   // partial-warp CTAs (very long tonal axes): no full-warp shuffle
+    atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+  }
 }
 
 }  // namespace fm

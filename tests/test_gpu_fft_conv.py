@@ -164,7 +164,7 @@ def test_transforms_zero_roundtrip_theorem():
     a = rng.integers(0, 1 << 20, (7, 9)).astype(np.float64)
     plan = m.make_plan(m.OffsetArray(a.astype(np.int64)), m.OffsetArray(np.ones((3, 3), np.int64)), m.Backend.FFT)
     spec = m.transform_forward(a, plan)
-    assert np.allclose(spec, np.fft.fftn(a, s=plan.padded_shape), rtol=1e-12, atol=1e-6)
+    assert np.allclose(spec, np.fft.fftn(a, s=plan.padded_shape, axes=(0, 1)), rtol=1e-12, atol=1e-6)
     back = m.transform_inverse(spec, plan)
     sl = tuple(slice(0, n) for n in a.shape)
     assert np.abs(back[sl].real - a).max() / a.max() < 1e-9
