@@ -355,14 +355,18 @@ def run_ours(args, rank, world, local_rank):
     # parity of exactly what was timed: every image of the rank, every pixel
     par_d = verify_outputs(out, valid, idx, "dilate") if args.verify else None
 
-    # e2e: same metric through the public API with HOST buffers (pinned), copies inside
+    # e2e: same metric through the public API with HOST buffers (pinned), copies inside.  The
+    # host-facing output uses the narrowest type holding every possible value, as the drop-in
+    # dilate_fft does (c5: 0..78 -> uint8); --e2e-out-dtype overrides it.
+    e2e_dt = {"narrow": torch.uint8, "u8": torch.uint8, "i16": torch.int16, "i32": torch.int32}[args.e2e_out_dtype]
+    eplan = plan if e2e_dt == out_dt else MorphPlan(mode="dilate", fill=0, out_dtype=e2e_dt, **common)
     pin_in = torch.from_numpy(imgs).pin_memory()
-    pin_out = torch.empty((nloc, EDGE, EDGE), dtype=out_dt).pin_memory()
+    pin_out = torch.empty((nloc, EDGE, EDGE), dtype=e2e_dt).pin_memory()
     pin_valid = torch.empty((nloc, EDGE, EDGE), dtype=torch.uint8).pin_memory()
-    plan.execute_host(pin_in, out=pin_out, valid=pin_valid, stream=stream)   # warm (staging alloc)
+    eplan.execute_host(pin_in, out=pin_out, valid=pin_valid, stream=stream)   # warm (staging alloc)
     e2e_steps = max(1, min(args.steps, 3))
     t0 = time.perf_counter()
-    e2e_ms = _timed(lambda: plan.execute_host(pin_in, out=pin_out, valid=pin_valid, stream=stream),
+    e2e_ms = _timed(lambda: eplan.execute_host(pin_in, out=pin_out, valid=pin_valid, stream=stream),
                     e2e_steps, stream, world) / e2e_steps
     wall_ms = (time.perf_counter() - t0) * 1000.0 / e2e_steps
     e2e_t = torch.tensor([max(e2e_ms, wall_ms)], dtype=torch.float64, device=dev)
@@ -370,7 +374,10 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_val = mpx / (float(e2e_t.item()) / 1000.0)
     par_e2e = verify_outputs(pin_out, pin_valid, idx, "dilate") if args.verify else None
+    e2e_osz = pin_out.element_size()
     del pin_in, pin_out, pin_valid
+    if eplan is not plan:
+        eplan.close()
 
     # erosion of the same batch (erode_fft semantics, l = tonal_max = 63), same timing rules
     ero = None
@@ -466,7 +473,8 @@ def run_ours(args, rank, world, local_rank):
                      # tonal length moves less than the floor's minimal-extent volume
                      "method_floor_effective": method_floor(value, hbm, osz)},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(imgs.nbytes),
-                "d2h_bytes_per_step": int(nloc * EDGE * EDGE * (osz + 1))},
+                "d2h_bytes_per_step": int(nloc * EDGE * EDGE * (e2e_osz + 1)),
+                "out_dtype": str(e2e_dt).split(".")[-1], "api": "fm_execute_host (pinned host buffers)"},
         "gpu_launches": int(launches),
         "max_abs_deviation": dev_max,
         "parity": parity,
@@ -626,6 +634,9 @@ def main():
     ap.add_argument("--scratch-gib", type=int, default=16)
     ap.add_argument("--out-dtype", choices=["u8", "i16", "i32"], default="i32",
                     help="output value type (int32 as SURVEY §8(d); the c5 dilation range 0..78 also fits u8)")
+    ap.add_argument("--e2e-out-dtype", choices=["narrow", "u8", "i16", "i32"], default="narrow",
+                    help="host output type of the e2e run (narrow: the narrowest type holding every value, "
+                         "as the drop-in API picks)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-verify", dest="verify", action="store_false",
                     help="skip the post-timing bit-exact check of every output image")

@@ -269,6 +269,8 @@ const int g_tonal_occ_cap = std::getenv("FM_TONAL_OCC") ? std::atoi(std::getenv(
 const bool g_fuse = std::getenv("FM_FUSE") && std::getenv("FM_FUSE")[0] == '1';
 const int g_fuse_kch = std::getenv("FM_FUSE_KCH") ? std::atoi(std::getenv("FM_FUSE_KCH")) : 0;
 const bool g_discard = !(std::getenv("FM_DISCARD") && std::getenv("FM_DISCARD")[0] == '0');
+// FM_DEVDISPATCH=0: small launches also wait on the host for the per-ladder counts (A/B)
+const bool g_devdispatch = !(std::getenv("FM_DEVDISPATCH") && std::getenv("FM_DEVDISPATCH")[0] == '0');
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
@@ -791,7 +793,13 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   p->DY = p->two_d ? (int)DY : 0;
   p->DX = (int)DX;
 
-  // tile choice: minimise tiles * P^2 * (log2 P^2 + 2) over the built variants
+  // tile choice: minimise the estimated time over the built variants.  Per (tile, plane) a
+  // CTA costs c(P) = P^2 (log2 P^2 + 2) + overhead; a launch of J such jobs with `occ` CTAs
+  // per SM takes ceil(J / (SMs occ)) waves of occ * c(P): the throughput form J c(P) / SMs
+  // for large batches (c5, c3), and for small images (latency bound: fewer jobs than the
+  // GPU holds) the per-CTA latency, where smaller tiles win.  Planes per tile after the
+  // clamp are not known yet: estimated as K / 3.
+  const double kest = std::max(1.0, std::ceil((double)p->K / 3.0));
   double best = 1e300;
   const Variant* bv = nullptr;
   // FM_TILE3=0 disables the three-pass 128x128 kernel (A/B measurements)
@@ -806,7 +814,11 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     const int qx = P - p->mx + 1, qy = p->two_d ? P - p->my + 1 : 1;
     const double tx = std::ceil((double)p->OW / qx), ty = p->two_d ? std::ceil((double)p->OH / qy) : 1.0;
     const double pts = p->two_d ? (double)P * P : (double)P;
-    const double cost = tx * ty * pts * (std::log2(pts) + 2.0) + tx * ty * 2048.0;
+    const double occ = std::max(1, std::min(kSmemLimit / (v.smem_fixed + 1024), 2048 / v.nt));
+    const double units = p->two_d ? tx * ty : std::ceil(tx / v.py);   // 1-D: py tiles per CTA
+    const double jobs = units * (double)p->batch * kest;
+    const double per = (p->two_d ? 1.0 : (double)v.py) * (pts * (std::log2(pts) + 2.0) + 2048.0);
+    const double cost = std::ceil(jobs / ((double)g_num_sms * occ)) * occ * per;
     if (cost < best) {
       best = cost;
       bv = &v;
@@ -817,7 +829,8 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     const int q = kBig - p->mx + 1, qy = kBig - p->my + 1;
     const double tx = std::ceil((double)p->OW / q), ty = std::ceil((double)p->OH / qy);
     const double pts = (double)kBig * kBig;
-    const double cost = 1.7 * tx * ty * pts * (std::log2(pts) + 2.0) + tx * ty * 2048.0;
+    const double cost = 1.7 * tx * ty * (double)p->batch * kest * (pts * (std::log2(pts) + 2.0) + 2048.0) /
+                        (double)g_num_sms;
     if (cost < best || d.tile == kBig) {
       best = cost;
       p->big = true;
@@ -1263,6 +1276,14 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
   // range kernels run one step ahead on a low-priority stream (double-buffered
   // outputs): they fill the conv tail and overlap the tonal kernels
   cudaStream_t rs = p->range_stream;
+  // Device dispatch (small launches, latency bound): the conv grid and the tonal pass are
+  // sized on the device from the range kernel's per-ladder counts (decode_job with
+  // k_chunk = 0, tonal_kernel_dispatch), so the call never waits on the host for them.
+  const int64_t conv_target_all = (int64_t)g_num_sms * p->conv_occ * 2;
+  auto devdisp = [&](const Step& st) {
+    return g_devdispatch && !p->big && !p->counts && p->fuse_nmax == 0 && p->N <= kDispatchNMax &&
+           (int64_t)st.nu * st.n < conv_target_all;
+  };
   FM_CUDA(cudaEventRecord(p->entry_ev, s));          // inputs / prior work on s
   FM_CUDA(cudaStreamWaitEvent(rs, p->entry_ev, 0));
   auto launch_range = [&](const Step& st, int buf) -> int {
@@ -1341,9 +1362,11 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     // the counts reach the host through a kernel store to mapped memory, not a
     // copy-engine D2H: a D2H copy would queue behind any large D2H transfer in
     // flight on the device (e.g. the previous chunk's outputs)
-    publish_counts<<<1, 64, 0, rs>>>(p->bucket_count[buf], p->h_counts_dev[buf], L);
-    g_launches++;
-    FM_CUDA(cudaGetLastError());
+    if (!devdisp(st) || p->timing) {   // (timing mode accounts the planes on the host)
+      publish_counts<<<1, 64, 0, rs>>>(p->bucket_count[buf], p->h_counts_dev[buf], L);
+      g_launches++;
+      FM_CUDA(cudaGetLastError());
+    }
     FM_CUDA(cudaEventRecord(p->count_ev[buf], rs));
 
     return FM_OK;
@@ -1476,6 +1499,82 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       }
       return FM_OK;
     };
+    if (devdisp(steps[si])) {
+      // ---- device-dispatched small launch: no host round trip
+      a.k_chunk = 0;
+      a.conv_target = (int)conv_target;
+      int rc = launch_conv((unsigned)(conv_target + (int64_t)nu * n));
+      if (rc) return rc;
+      TonalArgs t{};
+      t.chat = p->chat;
+      t.K_max = p->K;
+      t.unit_param = p->unit_param[buf];
+      t.units = p->units;
+      t.unit0 = u0;
+      t.upl = p->upl;
+      t.wpx = p->wpx;
+      t.npx = p->npx;
+      t.qx_magic = p->QX > 1 ? (uint32_t)((0x100000000ull + p->QX - 1) / p->QX) : 0u;
+      t.tx_magic = p->tiles_x > 1 ? (uint32_t)((0x100000000ull + p->tiles_x - 1) / p->tiles_x) : 0u;
+      t.two_d = p->two_d ? 1 : 0;
+      t.QY = p->QY;
+      t.QX = p->QX;
+      t.OH = (int)p->OH;
+      t.OW = (int)p->OW;
+      t.tiles_x = p->tiles_x;
+      t.unit_step_x = p->unit_step_x;
+      t.out = reinterpret_cast<char*>(out) + (size_t)c0 * npix * out_size(p->d.out_dtype);
+      t.out_dtype = p->d.out_dtype;
+      t.valid = valid ? valid + (size_t)c0 * npix : nullptr;
+      t.out_sign = p->out_sign;
+      t.se_min = p->se_min;
+      t.fill = p->d.fill;
+      t.dev_max = reinterpret_cast<float*>(p->stats);
+      t.bucket_count = p->bucket_count[buf];
+      t.ladder = p->d_ladder;
+      t.lists = p->bucket_list[buf];
+      t.L = L;
+      t.cap = (int)cap;
+      t.se_count = p->se_count;
+      constexpr int kDispNT = 128;
+      const int64_t blocks = (int64_t)nu * n * ((p->npx + kDispNT - 1) / kDispNT);
+      int e1 = -1;
+      if (p->timing) { e1 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
+      tonal_kernel_dispatch<kDispNT><<<(unsigned)blocks, kDispNT, 0, s>>>(t);
+      g_launches++;
+      FM_CUDA(cudaGetLastError());
+      if (p->timing) {
+        FM_CUDA(cudaEventRecord(next_event(p), s));
+        p->pending_tonal.push_back({e1, e1 + 1});
+      }
+      p->units_done += (int64_t)n * nu;
+      if (p->timing) {
+        // measurement mode: the per-ladder counts (published for it) give the planes
+        FM_CUDA(cudaEventSynchronize(p->count_ev[buf]));
+        double planes = 0, tonal_b = 0;
+        for (int li = 0; li < L; ++li) {
+          const int cnt = reinterpret_cast<volatile int*>(p->h_counts[buf])[li];
+          planes += (double)cnt * (p->ladder[li] + 1);
+          tonal_b += (double)cnt * ((p->ladder[li] + 1) * (double)p->npx * 8.0 +
+                                    (double)p->npx * (out_size(p->d.out_dtype) + (valid ? 1.0 : 0.0)));
+        }
+        if (!g_no_skip0 && img_defined == nullptr) {
+          const double skipped = (double)n * (double)(p->full_prefix[u0 + nu] - p->full_prefix[u0]);
+          planes -= skipped;
+          tonal_b -= skipped * (double)p->npx * 8.0;
+        }
+        p->planes_done += (int64_t)planes;
+        p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->npx * 8.0;
+        p->acc.conv_flops += planes * p->conv_flops_per_plane;
+        p->acc.tonal_bytes += tonal_b;
+      }
+      FM_CUDA(cudaEventRecord(p->free_ev[buf], s));
+      if (after_chunk && u0 + nu >= p->units) {
+        int rc2 = after_chunk(steps[si].chunk, c0, n);
+        if (rc2) return rc2;
+      }
+      continue;
+    }
     if (p->big) {
     } else if (!dyn) {
       // plan-time chunking (one chunk per unit for large launches); CTAs past

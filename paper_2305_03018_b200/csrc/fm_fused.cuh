@@ -11,8 +11,8 @@
 // Completion protocol: every CTA of a unit (its plane chunks) makes its chat
 // stores visible device-wide (__threadfence by every thread, CTA barrier) and
 // bumps the unit's counter; the CTA that sees count = chunks - 1 is the last,
-// fences again (acquire) and reads the planes with L2-only loads (ld.global.cg:
-// never a stale L1 line), then resets the counter for the next launch.
+// fences again (acquire) and streams the planes through shared memory with bulk
+// async copies (served by L2), then resets the counter for the next launch.
 //
 // Per pixel the math is the tonal kernel's (fm_tonal.cuh): c2r packing, the
 // compile-time length-N inverse FFT in registers, threshold c(t) > 0.5 with the
@@ -48,41 +48,55 @@ __device__ __forceinline__ float2 ldcg2(const float2* p) {
   return r;
 }
 
-// One unit's tonal step: pixels p = tid, tid + NT, ... of its QY x QX window.
+// One unit's tonal step: pixels p = tid + NT b, b = 0, 1, ... of its QY x QX window.
+// The K planes of each pixel block stream from L2 into shared memory by bulk async copies
+// (one per plane, issued by thread 0, completion on an mbarrier) one or two blocks ahead
+// of the block being computed -- the conv kernel's tile buffers are free by now.
 template <int N, int NT>
 __device__ __forceinline__ void fused_tonal_unit(const TileArgs& a, const float2* chat_unit, int img, int unit,
-                                              int anchor, bool full) {
+                                                 int anchor, bool full, float2* stg, int stg_slots,
+                                                 uint64_t* bars) {
   constexpr int K = N + 1;
   constexpr int off = tonal_off(N);
+  const int tid = threadIdx.x;
   const int ty = unit / a.tiles_x, tx = unit - (unit / a.tiles_x) * a.tiles_x;
   const int npx = a.QY * a.QX;
+  const int nblk = (npx + NT - 1) / NT;
+  const int k0 = full ? 1 : 0;
+  const int ST = 2 * K * NT <= stg_slots ? 2 : 1;
   const float x0 = (float)((double)a.se_count / (2.0 * N));
-  float dev = 0.f;
-  // software pipeline (short tonal axes, where the registers allow it): the next
-  // pixel's K loads are in flight while this pixel's FFT and threshold run
-  constexpr bool kPre = N <= 24;
-  auto load = [&](int p, float2 (&X)[K]) {
-    const int wy = p / a.QX, wx = p - (p / a.QX) * a.QX;
-    const bool live = p < npx && ty * a.QY + wy < a.OH && tx * a.QX + wx < a.OW;
-    const float2* xs = chat_unit + p;
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      X[k] = (k == 0 && full) || !live ? make_float2(x0, 0.f) : ldcg2(xs + (size_t)k * a.wpx);
+  auto issue = [&](int blk, int st) {   // thread 0: the block's planes k0..K-1 into stage st
+    const int p0 = blk * NT;
+    const uint32_t bytes = (uint32_t)min(NT, a.wpx - p0) * 8u;   // wpx even: 16-byte multiples
+    mbar_expect_tx(&bars[st], bytes * (uint32_t)(K - k0));
+    for (int k = k0; k < K; ++k)
+      bulk_g2s_nohint(stg + (size_t)(st * K + k) * NT, chat_unit + (size_t)k * a.wpx + p0, bytes, &bars[st]);
   };
-  float2 Xn[kPre ? K : 1];
-  if constexpr (kPre) load(threadIdx.x, Xn);
+  if (tid == 0) {
+    // the conv passes last wrote these bytes through the generic proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue(0, 0);
+    if (ST == 2 && nblk > 1) issue(1, 1);
+  }
+  float dev = 0.f;
 #pragma unroll 1
-  for (int p = threadIdx.x; p < npx; p += NT) {
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int st = ST == 2 ? (blk & 1) : 0;
+    const uint32_t par = (uint32_t)((ST == 2 ? (blk >> 1) : blk) & 1);
+    mbar_wait(&bars[st], par);
+    float2 X[K];
+    const float2* xs = stg + (size_t)st * K * NT + tid;
+#pragma unroll
+    for (int k = 0; k < K; ++k) X[k] = (k == 0 && full) ? make_float2(x0, 0.f) : xs[(size_t)k * NT];
+    __syncthreads();   // every thread has read the stage
+    if (tid == 0 && blk + ST < nblk) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(blk + ST, st);
+    }
+    const int p = blk * NT + tid;
     const int wy = p / a.QX, wx = p - (p / a.QX) * a.QX;
     const int oy = ty * a.QY + wy, ox = tx * a.QX + wx;
-    float2 X[K];
-    if constexpr (kPre) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) X[k] = Xn[k];
-      load(p + NT, Xn);
-    }
-    if (oy >= a.OH || ox >= a.OW) continue;
-    if constexpr (!kPre) load(p, X);
+    if (p >= npx || oy >= a.OH || ox >= a.OW) continue;
     float2 A[N], B[N];
     {
       const float2 xc = conjf2(X[N]);
@@ -112,20 +126,21 @@ __device__ __forceinline__ void fused_tonal_unit(const TileArgs& a, const float2
   }
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
-  if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+  if ((tid & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
 }
 
 template <int NT, int I = 0>
 __device__ __forceinline__ void fused_tonal_dispatch(int n, const TileArgs& a, const float2* chat_unit, int img,
-                                                     int unit, int anchor, bool full) {
+                                                     int unit, int anchor, bool full, float2* stg, int stg_slots,
+                                                     uint64_t* bars) {
   if constexpr (I < kTonalCount) {
     constexpr int NI = tonal_n_at(I);
     if constexpr (NI <= kFuseNMax) {
       if (n == NI) {
-        fused_tonal_unit<NI, NT>(a, chat_unit, img, unit, anchor, full);
+        fused_tonal_unit<NI, NT>(a, chat_unit, img, unit, anchor, full, stg, stg_slots, bars);
         return;
       }
-      fused_tonal_dispatch<NT, I + 1>(n, a, chat_unit, img, unit, anchor, full);
+      fused_tonal_dispatch<NT, I + 1>(n, a, chat_unit, img, unit, anchor, full, stg, stg_slots, bars);
     }
   }
 }
@@ -133,11 +148,13 @@ __device__ __forceinline__ void fused_tonal_dispatch(int n, const TileArgs& a, c
 // Called by every thread of a conv CTA after its plane loop.  Returns after the
 // unit's tonal step if this CTA completed the unit (and the unit's N is fused).
 template <int NT>
-__device__ __forceinline__ void fused_tail(const TileArgs& a, float2* chat_unit, int img, int unit, int K, int T) {
+__device__ __forceinline__ void fused_tail(const TileArgs& a, float2* chat_unit, int img, int unit, int K, int T,
+                                           int k_chunk, float2* stg, int stg_slots) {
   const int N = T / 2;
   if (a.fuse_nmax == 0 || N > a.fuse_nmax) return;
   __shared__ int s_last;
-  const int nch = (K + a.k_chunk - 1) / a.k_chunk;
+  __shared__ __align__(8) uint64_t s_tbar[2];
+  const int nch = (K + k_chunk - 1) / k_chunk;
   int* cnt = a.unit_done + ((size_t)img * a.upl + (unit - a.unit0));
   __threadfence();        // this thread's plane stores, device-wide
   __syncthreads();
@@ -151,7 +168,13 @@ __device__ __forceinline__ void fused_tail(const TileArgs& a, float2* chat_unit,
   if (!s_last) return;
   const int4 up = a.unit_param[(size_t)img * a.units + unit];
   const bool full = (up.w & 2) != 0;
-  fused_tonal_dispatch<NT>(N, a, chat_unit, img, unit, up.x, full);
+  if (threadIdx.x == 0) {
+    mbar_init(&s_tbar[0], 1);
+    mbar_init(&s_tbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  fused_tonal_dispatch<NT>(N, a, chat_unit, img, unit, up.x, full, stg, stg_slots, s_tbar);
   if (a.discard) {
     // the unit's planes are consumed: drop their L2 lines without a write-back
     __syncthreads();

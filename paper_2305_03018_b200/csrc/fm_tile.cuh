@@ -70,7 +70,8 @@ struct TileArgs {
   int tiles_x, tiles_total;   // tile grid (1-D: tiles_total = number of 1-D tiles)
   int T, K;                   // tonal length and planes (T/2+1)
   uint32_t magicT;            // floor(2^32 / T)
-  int k_chunk;
+  int k_chunk;                // planes per CTA; 0: chosen on the device (fills conv_target CTAs)
+  int conv_target;
   int enc_sign, enc_bias;     // v = enc_sign * f + enc_bias (CONV) / v = b - se_min (SPEC)
   const float4* spec;         // [K][thread order] SE spectrum, pairs (CONV reads)
   float4* spec_out;           // SPEC writes
@@ -183,6 +184,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // stragglers).  Every thread calls it (it contains a CTA barrier); false = no work.
 struct UnitJob {
   int img, unit, kchunk;
+  int k_chunk;                // planes per CTA (device-chosen when the launch is sized on the device)
   int T, K, enc_bias, unit_li;
   uint32_t magicT;
   bool skip0;                 // CONV unit whose plane 0 is a known constant (fm_range.cuh "full")
@@ -194,6 +196,7 @@ __device__ __forceinline__ bool decode_job(const TileArgs& a, UnitJob& j) {
   j.img = 0;
   j.unit = a.unit0 + blockIdx.x;
   j.kchunk = blockIdx.y;
+  j.k_chunk = a.k_chunk;
   j.T = a.T;
   j.K = a.K;
   j.enc_bias = a.enc_bias;
@@ -203,12 +206,22 @@ __device__ __forceinline__ bool decode_job(const TileArgs& a, UnitJob& j) {
   j.spec_base = a.spec;
   if constexpr (!SPEC) {
     const int lane = threadIdx.x & 31;
-    __shared__ int s_job[3];
+    __shared__ int s_job[4];
     if (threadIdx.x < 32) {
+      // k_chunk = 0: the launch was sized on the device (no host round trip for the
+      // per-ladder counts): planes per CTA so that the jobs fill a.conv_target CTAs
+      int kc = a.k_chunk;
+      if (kc <= 0) {
+        int planes = 0;
+        for (int li = lane; li < a.L; li += 32) planes += a.bucket_count[li] * (a.ladder[li] + 1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) planes += __shfl_xor_sync(0xffffffffu, planes, o);
+        kc = max(1, (planes + a.conv_target - 1) / a.conv_target);
+      }
       int rem = (int)blockIdx.x, found = -1, fch = 1;
       for (int top = a.L - 1; top >= 0 && found < 0; top -= 32) {
         const int li = top - lane;
-        const int ch = li >= 0 ? (a.ladder[li] + a.k_chunk) / a.k_chunk : 1;   // ceil((N+1)/k_chunk)
+        const int ch = li >= 0 ? (a.ladder[li] + kc) / kc : 1;   // ceil((N+1)/k_chunk)
         const int c = li >= 0 ? a.bucket_count[li] * ch : 0;
         int incl = c;
 #pragma unroll
@@ -236,6 +249,7 @@ __device__ __forceinline__ bool decode_job(const TileArgs& a, UnitJob& j) {
           s_job[1] = job.y & ~kJobFull;
           s_job[2] = rem - u * fch;   // plane chunk of the unit
         }
+        s_job[3] = kc;
       }
     }
     __syncthreads();
@@ -243,9 +257,10 @@ __device__ __forceinline__ bool decode_job(const TileArgs& a, UnitJob& j) {
     j.img = s_job[0];
     j.unit = s_job[1];
     j.kchunk = s_job[2];
+    j.k_chunk = s_job[3];
     const int4 up = a.unit_param[(size_t)j.img * a.units + j.unit];
     j.K = up.y + 1;
-    if (j.kchunk * a.k_chunk >= j.K) return false;   // this k-chunk is beyond the unit's planes
+    if (j.kchunk * j.k_chunk >= j.K) return false;   // this k-chunk is beyond the unit's planes
     j.T = 2 * up.y;
     j.magicT = (uint32_t)(0x100000000ull / (uint64_t)j.T);
     j.unit_li = up.z;
@@ -381,7 +396,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   __shared__ __align__(8) uint64_t s_full[2];   // spectrum ring (C::kBulkSpec)
   __shared__ int s_rel[2];                       // warps that released the buffer's chunk
   {
-    const int k_first = kchunk_idx * a.k_chunk + ((skip0 && kchunk_idx == 0) ? 1 : 0);
+    const int k_first = kchunk_idx * job.k_chunk + ((skip0 && kchunk_idx == 0) ? 1 : 0);
     if (mtab) build_mtab(k_first);
     if constexpr (!SPEC && C::kBulkSpec) {
       if (tid == 0) {
@@ -390,7 +405,7 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
         s_rel[0] = 0;
         s_rel[1] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (k_first < min(K, kchunk_idx * a.k_chunk + a.k_chunk)) {
+        if (k_first < min(K, kchunk_idx * job.k_chunk + job.k_chunk)) {
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
             mbar_expect_tx(&s_full[g], C::kChunkBytes);
@@ -404,11 +419,11 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
   __syncthreads();
   const int ty = (TWO_D && !SPEC) ? unit / a.tiles_x : 0;
   const int tx = (TWO_D && !SPEC) ? unit - ty * a.tiles_x : 0;
-  const int k_begin = kchunk_idx * a.k_chunk;
+  const int k_begin = kchunk_idx * job.k_chunk;
   // the plane loop bound lives in shared memory: under the kernel's register
   // pressure a register copy gets spilled and reloaded from local memory
   __shared__ int s_kend;
-  if (tid == 0) s_kend = min(K, k_begin + a.k_chunk);
+  if (tid == 0) s_kend = min(K, k_begin + job.k_chunk);
   __syncthreads();
   const volatile int* kend_s = &s_kend;
   // window-local output planes of this unit (slot = launch-local unit index)

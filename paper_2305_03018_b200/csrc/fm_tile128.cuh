@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
     }
   }
   if (tid < 128) twt[tid] = c_tw[TwOff<128>::v + (tid & 15) * (tid >> 4)];
-  const int k_begin = kchunk_idx * a.k_chunk;
+  const int k_begin = kchunk_idx * job.k_chunk;
   const int k_first = k_begin + ((skip0 && kchunk_idx == 0) ? 1 : 0);
   // with a trimmed window (QX <= 96) the inverse-y warps of column block 3 have
   // no output columns: they build the encode table two planes ahead while the
@@ -172,19 +172,19 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
   // plane k's F1 barrier
   const bool tab_in_i1 = !SPEC && a.QX <= 96;
   build_mtab(k_first);
-  if (tab_in_i1 && k_first + 1 < min(K, k_begin + a.k_chunk)) build_mtab(k_first + 1);
+  if (tab_in_i1 && k_first + 1 < min(K, k_begin + job.k_chunk)) build_mtab(k_first + 1);
   __shared__ __align__(8) uint64_t s_full[2];   // spectrum buffers: bulk-copy completion
   __shared__ int s_rel[2];                       // warps that released the buffer
   __shared__ int s_kend;
   if (tid == 0) {
-    s_kend = min(K, k_begin + a.k_chunk);
+    s_kend = min(K, k_begin + job.k_chunk);
     if constexpr (!SPEC) {
 #pragma unroll
       for (int b = 0; b < C::kNSB; ++b) mbar_init(&s_full[b], 1);
       s_rel[0] = 0;
       s_rel[1] = 0;
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      if (k_first < min(K, k_begin + a.k_chunk)) {
+      if (k_first < min(K, k_begin + job.k_chunk)) {
 #pragma unroll
         for (int b = 0; b < C::kNSB; ++b) {
           mbar_expect_tx(&s_full[b], C::kChunkBytes);
@@ -457,7 +457,9 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
     }
     ++pord;
   }
-  if constexpr (!SPEC) fused_tail<NT>(a, chat_unit, img, unit, K, T);
+  if constexpr (!SPEC)
+    fused_tail<NT>(a, chat_unit, img, unit, K, T, job.k_chunk, reinterpret_cast<float2*>(smem_raw),
+                   (C::kBufBytes + C::kSpecBytes) / 8);
 }
 
 }  // namespace fm

@@ -47,6 +47,11 @@ struct TonalArgs {
   // have plane 0 = (defined SE entries) / T everywhere; the conv kernel skips it
   float x0_full;
   int use_tma;            // pipelined kernel: stages by 2-D tensor copies (maps passed beside the args)
+  // device-dispatched kernel (small launches): every ladder entry in one launch
+  const int* bucket_count;   // [L] units per ladder entry
+  const int* ladder;         // [L] N of each entry
+  const int2* lists;         // [L][cap] work lists
+  int L, cap, se_count;
 };
 
 __device__ __forceinline__ void store_out(const TonalArgs& a, size_t i, int v) {
@@ -285,6 +290,101 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
     store_out(a, pp.dst, top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill);
     if (a.valid) a.valid[pp.dst] = top >= 0 ? 1 : 0;
   }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
+  if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+}
+
+// ---------------------------------------------------------------------------
+// Device-dispatched tonal pass for small launches (one small image: latency bound).
+// One CTA per (unit, pixel block) of ANY ladder entry: the entry, the unit and the
+// block are decoded from the device per-ladder counts (walked in ladder order), and
+// the compile-time inverse FFT of that entry's N is picked by a switch -- so the
+// whole call needs no host round trip for the counts (the host-sized launches of
+// tonal_kernel_pipe / tonal_kernel_t need them).  Register variants (N <= 40).
+constexpr int kDispatchNMax = 40;
+
+__host__ __device__ constexpr int tonal_ns_at(int i) {
+  constexpr int ns[] = {FM_TONAL_NS};
+  return ns[i];
+}
+
+template <int N>
+__device__ __forceinline__ void tonal_pixel_reg(const TonalArgs& a, const TonalPix& pp, float& dev) {
+  constexpr int off = tonal_off(N);
+  const float2* src = a.chat + pp.src;
+  const float x0 = (float)((double)a.se_count / (2.0 * N));
+  float2 X[N + 1];
+#pragma unroll
+  for (int k = 0; k <= N; ++k) X[k] = (k == 0 && pp.full) ? make_float2(x0, 0.f) : __ldcs(src + (size_t)k * a.wpx);
+  float2 A[N], B[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const float2 xk = X[k], xc = conjf2(X[N - k]);
+    A[k] = cadd(cadd(xk, xc), mul_pi(cmul(c_ttw[off + k], csub(xk, xc))));
+  }
+  stock_run<N, 0, 1>(A, B);
+  float d = 0.f;
+  int top;
+  if constexpr (num_radices(N) % 2 == 0) top = tonal_threshold<N>(A, d);
+  else top = tonal_threshold<N>(B, d);
+  dev = fmaxf(dev, d);
+  store_out(a, pp.dst, top >= 0 ? a.out_sign * (top + a.se_min) + pp.anchor : a.fill);
+  if (a.valid) a.valid[pp.dst] = top >= 0 ? 1 : 0;
+}
+
+template <int I = 0>
+__device__ __forceinline__ void tonal_pixel_dispatch(int n, const TonalArgs& a, const TonalPix& pp, float& dev) {
+  if constexpr (I < kTonalCount) {
+    constexpr int NI = tonal_ns_at(I);
+    if constexpr (NI <= kDispatchNMax) {
+      if (n == NI) {
+        tonal_pixel_reg<NI>(a, pp, dev);
+        return;
+      }
+      tonal_pixel_dispatch<I + 1>(n, a, pp, dev);
+    }
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) tonal_kernel_dispatch(const TonalArgs a) {
+  __shared__ int s_li, s_rem;
+  const int bpj = (a.npx + NT - 1) / NT;
+  if (threadIdx.x < 32) {
+    // warp-parallel walk of the per-ladder item counts (one load per lane, prefix by shuffles)
+    const int lane = threadIdx.x;
+    int rem = (int)blockIdx.x, found = -1;
+    for (int base = 0; base < a.L && found < 0; base += 32) {
+      const int l = base + lane;
+      const int c = l < a.L ? a.bucket_count[l] * bpj : 0;
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int nb = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += nb;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, l < a.L && rem < incl);
+      if (m) {
+        const int l0 = __ffs(m) - 1;
+        rem -= __shfl_sync(0xffffffffu, incl - c, l0);
+        found = base + l0;
+      } else {
+        rem -= __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    if (lane == 0) {
+      s_li = found;
+      s_rem = rem;
+    }
+  }
+  __syncthreads();
+  const int li = s_li;
+  if (li < 0) return;   // grid sized for every unit of the launch; past the jobs
+  const int j = s_rem / bpj, blk = s_rem - (s_rem / bpj) * bpj;
+  const TonalPix pp = tonal_pixel_job(a, a.lists[(size_t)li * a.cap + j], blk * NT + threadIdx.x);
+  float dev = 0.f;
+  if (pp.live) tonal_pixel_dispatch(a.ladder[li], a, pp, dev);
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
   if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
