@@ -277,6 +277,20 @@ def verify_outputs(out, valid, idx, op):
     return {"images": len(idx), "ok": not bad, "mismatched": bad}
 
 
+def over_ranks(value, op, world, device, dtype=None):
+    """Reduce one number over the ranks (the bench's only collectives besides the barriers):
+    'max' for times (the slowest rank sets the step), 'min' for parity flags, 'sum' for
+    counts.  World 1: the value itself."""
+    import torch
+    import torch.distributed as dist
+    if world <= 1:
+        return value
+    t = torch.tensor([value], dtype=dtype or (torch.float64 if isinstance(value, float) else torch.int64),
+                     device=device)
+    dist.all_reduce(t, op={"max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN, "sum": dist.ReduceOp.SUM}[op])
+    return t.item()
+
+
 def _timed(fn, steps, stream, world):
     """CUDA-event time of `steps` calls of fn on `stream`, barrier + synchronize on both
     sides, max over ranks (ms)."""
@@ -294,10 +308,8 @@ def _timed(fn, steps, stream, world):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    return float(ms.item())
+    return float(over_ranks(float(a.elapsed_time(b)), "max", world,
+                            torch.device("cuda", torch.cuda.current_device())))
 
 
 def run_ours(args, rank, world, local_rank):
@@ -330,6 +342,13 @@ def run_ours(args, rank, world, local_rank):
 
     def step():
         plan.execute(x, out=out, valid=valid, stream=stream)
+
+    if args.profile_step:
+        # exactly one step of the hot path (for an ncu launch list / DRAM-bytes pass)
+        step()
+        torch.cuda.synchronize()
+        print(json.dumps({"profile_step": True, "images": nloc}), flush=True)
+        return
 
     # the clock sampler runs from before the warm-up (all of it under load) to the end
     # of the timed region
@@ -369,10 +388,7 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = _timed(lambda: eplan.execute_host(pin_in, out=pin_out, valid=pin_valid, stream=stream),
                     e2e_steps, stream, world) / e2e_steps
     wall_ms = (time.perf_counter() - t0) * 1000.0 / e2e_steps
-    e2e_t = torch.tensor([max(e2e_ms, wall_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_val = mpx / (float(e2e_t.item()) / 1000.0)
+    e2e_val = mpx / (float(over_ranks(float(max(e2e_ms, wall_ms)), "max", world, dev)) / 1000.0)
     par_e2e = verify_outputs(pin_out, pin_valid, idx, "dilate") if args.verify else None
     e2e_osz = pin_out.element_size()
     del pin_in, pin_out, pin_valid
@@ -399,12 +415,9 @@ def run_ours(args, rank, world, local_rank):
     parity = None
     if args.verify:
         flags = [par_d["ok"], par_e2e["ok"]] + ([ero["parity"]["ok"]] if ero else [])
-        ok_t = torch.tensor([1 if all(flags) else 0], dtype=torch.int32, device=dev)
-        n_t = torch.tensor([nloc], dtype=torch.int64, device=dev)
-        if world > 1:
-            dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
-            dist.all_reduce(n_t)
-        parity = {"images": int(n_t.item()), "ok": bool(ok_t.item()),
+        ok_all = over_ranks(1 if all(flags) else 0, "min", world, dev)
+        n_all = over_ranks(nloc, "sum", world, dev)
+        parity = {"images": int(n_all), "ok": bool(ok_all),
                   "dilate": par_d, "e2e_dilate": par_e2e, "erode": ero["parity"] if ero else None,
                   "checker": "sha256(int32 values || uint8 validity) per image vs tests/golden/c5_all_digests.json "
                              "(oracle/naive.c restatement of dilate_naive/erode_naive, pinned to the reference "
@@ -575,10 +588,7 @@ def run_strips(args, rank, world, local_rank):
     t0 = time.perf_counter()
     e2e_ms = _timed(e2e_step, args.steps, stream, world) / args.steps
     wall_ms = (time.perf_counter() - t0) * 1000.0 / args.steps
-    e2e_t = torch.tensor([max(e2e_ms, wall_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_val = mpx / (float(e2e_t.item()) / 1000.0)
+    e2e_val = mpx / (float(over_ranks(float(max(e2e_ms, wall_ms)), "max", world, dev)) / 1000.0)
     # parity: the stitched image against the reference's own output digest
     parts = [None] * world
     mine = (r0, pin_out.numpy().copy(), pin_valid.numpy().copy())
@@ -641,6 +651,8 @@ def main():
     ap.add_argument("--no-verify", dest="verify", action="store_false",
                     help="skip the post-timing bit-exact check of every output image")
     ap.add_argument("--no-erode", dest="erode", action="store_false", help="skip the erosion measurement")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="run exactly one untimed step and exit (for profilers)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -88,6 +88,7 @@ def main():
         summary["images_per_launch"] = int(sys.argv[sys.argv.index("--images-per-launch") + 1])
     if launches:
         per = defaultdict(list)
+        step_bytes = [0.0]
         with open(launches) as fh:
             lines = [l for l in fh if l.startswith('"')]
         rd = list(csv.reader(lines))
@@ -96,8 +97,18 @@ def main():
             dd = dict(zip(h, r))
             if dd.get("Metric Name") == "gpu__time_duration.sum":
                 per[dd["Kernel Name"].split("(")[0]].append(to_float(dd["Metric Value"]))
+            elif dd.get("Metric Name") in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                # one hot-path step (bench --profile-step); the SE-spectrum launches at plan
+                # creation (tile kernels with SPEC = 1) are not part of it
+                if not dd["Kernel Name"].rstrip().endswith("1>(TileArgs)"):
+                    sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(dd.get("Metric Unit"), 1)
+                    step_bytes[0] += (to_float(dd["Metric Value"]) or 0.0) * sc
         summary["launch_list"] = {k: {"launches": len(v), "total": sum(x for x in v if x), "mean": sum(x for x in v if x) / max(len(v), 1)}
                                   for k, v in per.items()}
+        if step_bytes[0] > 0 and "--step-images" in sys.argv:
+            n_img = int(sys.argv[sys.argv.index("--step-images") + 1])
+            summary["dram_bytes_per_step"] = step_bytes[0]
+            summary["dram_bytes_per_image"] = step_bytes[0] / n_img
         tot = sum(s["total"] for s in summary["launch_list"].values())
         for s in summary["launch_list"].values():
             s["share"] = s["total"] / tot if tot else None

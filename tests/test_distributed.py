@@ -83,3 +83,109 @@ def test_row_strip_halo_exchange_bit_exact(world, mode):
         assert p.exitcode == 0
     assert q.get(timeout=10) is True
     assert q.get(timeout=10) is True
+
+
+def _window_worker(rank, world, port, mode, q):
+    """Each rank computes ITS strip exactly as the product's per-strip plan does
+    (strips.strip_plan_kwargs: image = the strip's input rows, output window = its owned
+    rows): here the window is cut out of the oracle's full-range result on the strip
+    rows, at the plan's window offset.  Stitched, it must equal the one-image result."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        from pathlib import Path
+        sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+        from oracle import cnaive
+        from paper_2305_03018_b200 import sharding, strips as S
+        rng = np.random.default_rng(321)
+        H, W = 61, 37
+        img = rng.integers(0, 40, (H, W)).astype(np.int32)
+        se = rng.integers(0, 5, (11, 4))
+        sd = rng.random((11, 4)) > 0.3
+        sd[5, 1] = True
+        lo = (-7, -1)       # SE not centred: asymmetric halos
+        my, mx = se.shape
+        plan = sharding.strips(H, world, lo[0], my, mode)
+        me = plan[rank]
+        local = torch.from_numpy(img[me.out0:me.out1].copy())
+        window = sharding.exchange_halos(local, plan, rank).numpy()
+        kw = S.strip_plan_kwargs(me, W)
+        assert kw["shape"] == window.shape
+        (wy, wx), (wh, ww) = kw["window"]
+        erode = mode == "erode"
+        fill = 99 if erode else 0
+        full, fvalid = cnaive.naive(window, None, se, sd, lo, erode=erode, crop=False, fill=fill, threads=1)
+        off_y = -(lo[0] + my - 1) if erode else lo[0]
+        off_x = -(lo[1] + mx - 1) if erode else lo[1]
+        mine = np.full((wh, ww), fill, np.int32)
+        for y in range(wh):
+            fy = wy + y - off_y
+            if 0 <= fy < full.shape[0]:
+                xs = np.arange(ww) + wx - off_x
+                ok = (xs >= 0) & (xs < full.shape[1])
+                mine[y, ok] = full[fy, xs[ok]]
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (me.out0, mine))
+        if rank == 0:
+            stitched = np.concatenate([g[1] for g in sorted(gathered, key=lambda t: t[0])])
+            ref, _ = cnaive.naive(img, None, se, sd, lo, erode=erode, crop=True, fill=fill)
+            q.put(bool(np.array_equal(stitched, ref)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("mode", ["dilate", "erode"])
+def test_row_strip_plan_windows_bit_exact(world, mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_window_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True
+
+
+def _bench_worker(rank, world, port, q):
+    """bench.py's multi-rank orchestration on CPU (gloo): rank-safe build, image shards,
+    max-over-ranks timing, parity and image-count reductions."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        from pathlib import Path
+        sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+        import bench
+        from paper_2305_03018_b200 import build as B
+        from paper_2305_03018_b200.sharding import shard_range
+        B.build_rank_safe(rank, world)
+        i0, i1 = shard_range(bench.N_IMAGES, rank, world)
+        cpu = torch.device("cpu")
+        ms = bench.over_ranks(10.0 + rank, "max", world, cpu)
+        ok = bench.over_ranks(0 if rank == world - 1 else 1, "min", world, cpu)
+        n = bench.over_ranks(i1 - i0, "sum", world, cpu)
+        q.put((rank, ms, ok, n))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_orchestration_gloo():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    for rank, ms, ok, n in res:
+        assert ms == 10.0 + world - 1 and ok == 0 and n == 64

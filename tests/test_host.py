@@ -196,7 +196,7 @@ def test_committed_bench_line_contract():
     import json
     from pathlib import Path
     prof = Path(__file__).resolve().parents[1] / "profiles"
-    lines = sorted(prof.glob("r1*_bench_line.json"), key=lambda f: (len(f.stem), f.stem))
+    lines = sorted(prof.glob("r*_bench_line.json"), key=lambda f: (f.stem[:2], len(f.stem), f.stem))
     assert lines, "no committed bench line"
     d = json.loads(lines[-1].read_text())
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
@@ -213,3 +213,7 @@ def test_committed_bench_line_contract():
         assert key in d["cpu_baseline"], key
     assert d["gpu_launches"] > 0 and d["steps"] >= 1 and d["warmup"] >= 3
     assert not set(d["clocks"].get("reasons", [])) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    if lines[-1].name.startswith("r2"):
+        # round 2: the timed output is parity-checked image by image, erosion measured too
+        assert d["parity"]["ok"] and d["parity"]["images"] == 64
+        assert d["erode"]["parity"]["ok"] and r["bound"] == "fp32"
