@@ -195,7 +195,8 @@ struct Variant {
 const Variant kVariants[] = {
     FM_VARIANT128(uint8_t), FM_VARIANT128(uint16_t),
     FM_VARIANT(true, 16, 16, 32),   FM_VARIANT(true, 32, 32, 64),   FM_VARIANT(true, 64, 64, 256),
-    FM_VARIANT(true, 128, 128, 512), FM_VARIANT(false, 32, 16, 64),  FM_VARIANT(false, 32, 32, 64),
+    FM_VARIANT(true, 128, 128, 512), FM_VARIANT(false, 8, 256, 64), FM_VARIANT(false, 16, 256, 128),
+    FM_VARIANT(false, 32, 16, 64),  FM_VARIANT(false, 32, 32, 64),
     FM_VARIANT(false, 32, 64, 128),  FM_VARIANT(false, 32, 128, 128), FM_VARIANT(false, 32, 256, 256),
 };
 
@@ -271,6 +272,7 @@ const int g_fuse_kch = std::getenv("FM_FUSE_KCH") ? std::atoi(std::getenv("FM_FU
 const bool g_discard = !(std::getenv("FM_DISCARD") && std::getenv("FM_DISCARD")[0] == '0');
 // FM_DEVDISPATCH=0: small launches also wait on the host for the per-ladder counts (A/B)
 const bool g_devdispatch = !(std::getenv("FM_DEVDISPATCH") && std::getenv("FM_DEVDISPATCH")[0] == '0');
+const int g_big_steps = std::getenv("FM_BIG_STEPS") ? std::atoi(std::getenv("FM_BIG_STEPS")) : 1;
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
@@ -818,7 +820,9 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     const double units = p->two_d ? tx * ty : std::ceil(tx / v.py);   // 1-D: py tiles per CTA
     const double jobs = units * (double)p->batch * kest;
     const double per = (p->two_d ? 1.0 : (double)v.py) * (pts * (std::log2(pts) + 2.0) + 2048.0);
-    const double cost = std::ceil(jobs / ((double)g_num_sms * occ)) * occ * per;
+    // CTAs actually sharing an SM in a wave (a lone CTA gets the SM to itself)
+    const double resident = std::min(occ, std::ceil(jobs / (double)g_num_sms));
+    const double cost = std::ceil(jobs / ((double)g_num_sms * occ)) * resident * per;
     if (cost < best) {
       best = cost;
       bv = &v;
@@ -843,6 +847,10 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   }
   if (p->big) bv = nullptr;
   p->var = bv;
+  if (std::getenv("FM_PLAN_DEBUG"))
+    std::fprintf(stderr, "[fm plan] %s %lldx%lld se %dx%d T=%d K=%d tile %s%dx%d nt=%d batch=%lld\n",
+                 p->two_d ? "2-D" : "1-D", (long long)p->H, (long long)p->W, p->my, p->mx, p->T, p->K,
+                 p->big ? "big " : "", bv ? bv->py : kBig, bv ? bv->px : kBig, bv ? bv->nt : 0, (long long)p->batch);
   p->PY = p->big ? kBig : bv->py;
   p->PX = p->big ? kBig : bv->px;
   p->QX = p->PX - p->mx + 1;
@@ -949,6 +957,11 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   // default budget 16 GiB: large launches keep the per-launch tail small (B200: 180 GB HBM)
   const int64_t budget = d.scratch_bytes > 0 ? d.scratch_bytes : (int64_t)16 << 30;
   p->upl = (int)std::max<int64_t>(1, std::min<int64_t>(p->units, budget / std::max<int64_t>(per_unit, 1)));
+  // one image on the 256^2 path: split its units into a few launch steps so the range
+  // kernel of step i+1 (its own low-priority stream) overlaps the conv / tonal of step i
+  // instead of preceding them (FM_BIG_STEPS=<n>, default 3; 1 = one step)
+  if (p->big && d.batch == 1 && g_big_steps > 1 && p->units >= 4 * g_big_steps)
+    p->upl = std::min(p->upl, (p->units + g_big_steps - 1) / g_big_steps);
   if (p->upl < p->units) {
     p->ipc = 1;
   } else {

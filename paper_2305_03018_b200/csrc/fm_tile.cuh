@@ -40,6 +40,7 @@ namespace fm {
 constexpr uint16_t kSent = 0xFFFFu;  // "no one-hot entry": gap or outside the grid
 
 template <int P> struct Split;
+template <> struct Split<8> { static constexpr int R1 = 4, R2 = 2; };     // (1-D CTAs of 8 rows: y unused)
 template <> struct Split<16> { static constexpr int R1 = 4, R2 = 4; };
 template <> struct Split<32> { static constexpr int R1 = 8, R2 = 4; };
 template <> struct Split<64> { static constexpr int R1 = 8, R2 = 8; };
@@ -327,7 +328,10 @@ __global__ void __launch_bounds__(NT, 1) tile_conv_kernel(const TileArgs a) {
         const int sy = TWO_D ? py : 0;
         if (sy < a.my && px < a.mx) {
           const int si = sy * a.mx + px;
-          if (a.se_def == nullptr || a.se_def[si]) t = (uint16_t)(a.se_vals[si] + a.enc_bias);
+          // ladder entries shorter than the SE's own value range are never used by a
+          // unit (a unit's T exceeds max b - min b); reduce so their (unused) spectra
+          // stay finite and the per-plane table (T + 1 entries) is never overrun
+          if (a.se_def == nullptr || a.se_def[si]) t = (uint16_t)((a.se_vals[si] + a.enc_bias) % T);
         }
         tv[p] = t;
       }

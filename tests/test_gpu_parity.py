@@ -306,6 +306,26 @@ def test_tile_and_tonal_length_invariance():
         assert np.array_equal(v[0], ref), T
 
 
+@pytest.mark.parametrize("tile", [16, 32, 64, 128, 256])
+def test_se_value_range_wider_than_short_ladder_entries(tile):
+    """8-bit data with an SE whose own value range (up to 230) exceeds the shortest ladder
+    entries: their (never used) SE spectra must stay in bounds for every tile engine
+    (regression: the four-pass kernels indexed a per-plane table of T + 1 entries with
+    unreduced SE values)."""
+    from paper_2305_03018_b200 import workloads as W
+    rng = np.random.default_rng(230 + tile)
+    edge = max(tile - 2, 12)
+    img = rng.integers(0, 256, (1, edge, edge + 5)).astype(np.uint8)
+    se = rng.integers(0, 231, (3, 3))
+    se[0, 0], se[2, 2] = 0, 230
+    w = W.Workload("x", img, se, np.ones((3, 3), bool), (-1, -1), 255, 8)
+    for mode in ("dilate", "erode"):
+        v, valid, dev, plan = _plan_run(w, mode, tile=tile)
+        ref, refv = cnaive.naive(img[0], None, se, None, (-1, -1), erode=(mode == "erode"), crop=True,
+                                 fill=0 if mode == "dilate" else 255)
+        assert np.array_equal(v[0], ref) and np.array_equal(valid[0].astype(bool), refv), (tile, mode)
+
+
 def test_wide_se_big_tiles():
     """SEs wider than the 128 SMEM tile run on 256x256 tiles through HBM (fm_bigtile.cuh)."""
     from paper_2305_03018_b200 import workloads as W
