@@ -139,3 +139,69 @@ def test_stage_reuse_race_regression():
         junk = torch.full((int(1e9) // 4,), float(r) + 0.5, dtype=torch.float32, device="cuda")
         del junk
         test_fuzz_engine_vs_oracle(124)
+
+
+def _wide_case(seed):
+    """Round-2 envelope: SE value ranges up to 255 (wider than the short ladder entries),
+    8..11-bit data, every tile engine forced, SEs wider than one tile (split and combined),
+    output windows (crop = 2) and device-dispatched small launches."""
+    rng = np.random.default_rng(seed)
+    shape = (int(rng.integers(3, 300)), int(rng.integers(3, 300)))
+    big_se = rng.random() < 0.15
+    se_shape = tuple(int(rng.integers(100, 330)) if big_se else int(rng.integers(1, 40)) for _ in range(2))
+    levels = int(rng.choice([16, 256, 1024, 2048]))
+    img = rng.integers(0, levels, shape)
+    se_top = int(rng.choice([1, 64, 200, 255]))
+    se = rng.integers(0, se_top + 1, se_shape)
+    se_def = rng.random(se_shape) > (0.97 if big_se else 0.4)
+    se_def.flat[int(rng.integers(0, se_def.size))] = True
+    se_lo = tuple(int(-(s // 2) + rng.integers(-3, 4)) for s in se_shape)
+    mode = "erode" if rng.random() < 0.4 else "dilate"
+    window = None
+    if rng.random() < 0.25:
+        window = ((int(rng.integers(-5, shape[0])), int(rng.integers(-5, shape[1]))),
+                  (int(rng.integers(1, shape[0] + 5)), int(rng.integers(1, shape[1] + 5))))
+    tile = 0 if big_se else int(rng.choice([0, 0, 16, 32, 64, 128, 256]))
+    if tile and max(se_shape) > tile:
+        tile = 0
+    return dict(shape=shape, img=img, se=se, se_def=se_def, se_lo=se_lo, mode=mode, window=window, tile=tile,
+                levels=levels)
+
+
+@pytest.mark.parametrize("seed", list(range(60)))
+def test_fuzz_wide_ranges_vs_oracle(seed):
+    import torch
+    from paper_2305_03018_b200.engine import MorphPlan
+    c = _wide_case(zlib.crc32(f"fuzz-wide/{seed}".encode()))
+    vmax = c["levels"] - 1
+    fill = 0 if c["mode"] == "dilate" else vmax
+    dt, npdt = (torch.uint8, np.uint8) if vmax <= 255 else (torch.uint16, np.uint16)
+    try:
+        plan = MorphPlan(shape=c["shape"], se_values=c["se"], se_defined=c["se_def"], se_lo=c["se_lo"],
+                         mode=c["mode"], crop=True, img_dtype=dt, img_min=0, img_max=vmax, fill=fill,
+                         tile=c["tile"], window=c["window"])
+    except NotImplementedError:
+        pytest.skip("configuration outside the FFT path's limits")
+    out, valid = plan.execute(torch.from_numpy(c["img"].astype(npdt)).cuda().unsqueeze(0))
+    assert plan.read_stats() < 0.25
+    out, valid = out[0].cpu().numpy(), valid[0].cpu().numpy().astype(bool)
+    erode = c["mode"] == "erode"
+    if c["window"] is None:
+        ref, rvalid = cnaive.naive(c["img"], None, c["se"], c["se_def"], c["se_lo"], erode=erode, crop=True, fill=fill)
+    else:
+        full, fvalid = cnaive.naive(c["img"], None, c["se"], c["se_def"], c["se_lo"], erode=erode, crop=False,
+                                    fill=fill)
+        my, mx = c["se"].shape
+        lo = c["se_lo"]
+        off = (-(lo[0] + my - 1), -(lo[1] + mx - 1)) if erode else lo
+        (wy, wx), (wh, ww) = c["window"]
+        ref = np.full((wh, ww), fill, np.int64)
+        rvalid = np.zeros((wh, ww), bool)
+        ys = np.arange(wh) + wy - off[0]
+        xs = np.arange(ww) + wx - off[1]
+        oky = (ys >= 0) & (ys < full.shape[0])
+        okx = (xs >= 0) & (xs < full.shape[1])
+        ref[np.ix_(oky, okx)] = full[np.ix_(ys[oky], xs[okx])]
+        rvalid[np.ix_(oky, okx)] = fvalid[np.ix_(ys[oky], xs[okx])]
+    assert np.array_equal(valid, rvalid.astype(bool)), seed
+    assert np.array_equal(out.astype(np.int64), ref.astype(np.int64)), seed
