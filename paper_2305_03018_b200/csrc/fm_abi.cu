@@ -52,6 +52,7 @@ int fail(int code, const std::string& msg) {
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr int64_t kFp32CountBudget = 1 << 17;   // fm_plan_desc.count_budget default
+constexpr int kChat16MaxCount = 2048;            // 16-bit spectral planes up to this many SE entries
 
 int set_all_smem_attrs();
 
@@ -73,14 +74,16 @@ EncodeTiledFn encode_tiled_fn() {
   return fn;
 }
 // [rows][wpx] float2 spectral scratch as a 2-D tensor of 8-byte elements; box {bx, by}
-bool encode_chat_map(CUtensorMap* m, void* chat, int64_t wpx, int64_t rows, int bx, int by) {
+bool encode_chat_map(CUtensorMap* m, void* chat, int64_t wpx, int64_t rows, int bx, int by, int esz = 8) {
   EncodeTiledFn fn = encode_tiled_fn();
   if (!fn || bx < 1 || by < 1 || bx > 256 || by > 256) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)wpx, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)wpx * 8};
+  const cuuint64_t strides[1] = {(cuuint64_t)wpx * esz};
   const cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by};
   const cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, chat, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  // 8-byte complex64 elements, or 4-byte int16 pairs (16-bit planes): the map only moves bytes
+  return fn(m, esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, chat, dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -273,6 +276,11 @@ const bool g_discard = !(std::getenv("FM_DISCARD") && std::getenv("FM_DISCARD")[
 // FM_DEVDISPATCH=0: small launches also wait on the host for the per-ladder counts (A/B)
 const bool g_devdispatch = !(std::getenv("FM_DEVDISPATCH") && std::getenv("FM_DEVDISPATCH")[0] == '0');
 const int g_big_steps = std::getenv("FM_BIG_STEPS") ? std::atoi(std::getenv("FM_BIG_STEPS")) : 1;
+// 256^2 path: L2 budget (MiB) of one unit batch's scratch items (FM_BIG_L2_MB; default 0 = one
+// batch: measured slower at 96 / 48 / 24 MiB, the passes are latency bound, not HBM bound)
+const int g_big_l2_mb = std::getenv("FM_BIG_L2_MB") ? std::atoi(std::getenv("FM_BIG_L2_MB")) : 0;
+// FM_CHAT16=0 keeps complex64 spectral planes (A/B)
+const bool g_chat16 = !(std::getenv("FM_CHAT16") && std::getenv("FM_CHAT16")[0] == '0');
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
@@ -400,6 +408,9 @@ struct fm_plan {
   void* part_out = nullptr;               // [batch][OH][OW] of out_dtype
   uint8_t* part_valid = nullptr;          // [batch][OH][OW]
   uint8_t* acc_valid = nullptr;           // [batch][OH][OW] when the caller passes no validity
+  // 16-bit spectral planes (chat16): int16 pairs at scale q = chat_q_T * T (see fm_plan_create)
+  bool chat16 = false;
+  float chat_q_T = 0.f, chat_invq_T = 0.f;
   // fused tonal step (fm_fused.cuh): ladder entries with N <= fuse_nmax finish in the conv kernel
   int fuse_nmax = 0;
   int* unit_done = nullptr;               // [ipc][upl] plane-chunk completion counters
@@ -908,7 +919,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     p->unit_step_x = p->PY * p->QX;
   }
 
-  p->wpx = (p->npx + 1) & ~1;  // even plane stride: 16-byte aligned bulk copies of pixel blocks
+  p->wpx = (p->npx + 3) & ~3;  // plane stride a multiple of 4 pixels: 16-byte aligned bulk / TMA copies of pixel blocks for both element sizes (8 B, and 4 B with 16-bit planes)
   // units whose input window lies inside the image (the "full" test of fm_range.cuh)
   p->full_prefix.assign(p->units + 1, 0);
   for (int u = 0; u < p->units; ++u) {
@@ -999,6 +1010,20 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   if (g_fuse && !p->counts && !p->big && p->two_d && bv && bv->tmax < (1 << 30)) {
     p->fuse_nmax = kFuseNMax;
     if (g_fuse_kch > 0) p->k_chunk = std::min(p->K, g_fuse_kch);
+  }
+  // 16-bit spectral planes.  A plane value is X_k = (1/T) sum_t c(t) w^{kt} with
+  // sum_t c(t) <= C = defined SE entries, so |Re X_k|, |Im X_k| <= C / T: stored as int16
+  // at q = 32000 T / C the rounding error is <= C / (64000 T) per component, and the
+  // inverse tonal transform (2N terms, |weights| <= 1 after the c2r packing) recovers
+  // every count within sqrt(2) C / 64000 (C = 961 at c5: 0.021; the reference aborts at
+  // 0.25).  Enabled for C <= 2048 (bound <= 0.045) on the three-pass 128^2 kernels;
+  // the measured deviation (fm_read_stats) includes it.  Halves the spectral volume's
+  // bytes (conv writes, tonal reads).
+  if (g_chat16 && !p->counts && !p->big && p->fuse_nmax == 0 && p->two_d && bv && bv->tmax < (1 << 30) &&
+      p->se_count <= kChat16MaxCount) {
+    p->chat16 = true;
+    p->chat_q_T = (float)(32000.0 / (double)p->se_count);
+    p->chat_invq_T = (float)((double)p->se_count / 32000.0);
   }
   p->kchunks = (p->K + p->k_chunk - 1) / p->k_chunk;
   p->conv_occ = occ;
@@ -1094,7 +1119,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     if ((e = cudaMalloc(&p->unit_done, sizeof(int) * (size_t)slots)) != cudaSuccess) return cfail(e, "counter alloc");
     cudaMemset(p->unit_done, 0, sizeof(int) * (size_t)slots);
   }
-  if ((e = cudaMalloc(&p->chat, (size_t)slots * p->K * p->wpx * 8)) != cudaSuccess) {
+  if ((e = cudaMalloc(&p->chat, (size_t)slots * p->K * p->wpx * (p->chat16 ? 4 : 8))) != cudaSuccess) {
     free_plan(p);
     return fail(FM_ENOMEM, std::string("spectral scratch alloc: ") + cudaGetErrorString(e));
   }
@@ -1107,8 +1132,9 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
       const TonalVariant* tv = p->ladder_var[li];
       const int K = p->ladder[li] + 1;
       const int bx = tv ? tv->pipe_nt : 128;
-      ok = encode_chat_map(&maps[2 * li], p->chat, p->wpx, slots * p->K, bx, K) &&
-           encode_chat_map(&maps[2 * li + 1], p->chat, p->wpx, slots * p->K, bx, std::max(1, K - 1));
+      const int esz = p->chat16 ? 4 : 8;
+      ok = encode_chat_map(&maps[2 * li], p->chat, p->wpx, slots * p->K, bx, K, esz) &&
+           encode_chat_map(&maps[2 * li + 1], p->chat, p->wpx, slots * p->K, bx, std::max(1, K - 1), esz);
     }
     if (ok) p->tmaps = std::move(maps);
   }
@@ -1140,6 +1166,8 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     b.enc_sign = 1;
     b.enc_bias = -smin;
     b.units = 1;
+    b.nu = 1;
+    b.nub = 1;
     b.K_max = b.K;
     b.S = p->S + (size_t)slots * p->K * kBig * kBig;   // spare slab after the batch scratch
     b.spec = p->spec + p->spec_off[li];
@@ -1436,6 +1464,8 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     a.enc_off = p->d_enc_off;
     a.cap = (int)cap;
     a.L = L;
+    a.chat16 = p->chat16 ? 1 : 0;
+    a.chat_q_T = p->chat_q_T;
     if (p->fuse_nmax > 0) {
       a.fuse_nmax = p->fuse_nmax;
       a.discard = g_discard ? 1 : 0;
@@ -1499,13 +1529,24 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       b.chat = p->chat;
       b.wpx = p->wpx;
       b.err = p->stats + 1;
-      const unsigned z = (unsigned)(nu * n);
       const unsigned inv_blocks = (unsigned)((kBig - (p->my - 1) + kBigRows - 1) / kBigRows);
-      big_rows_kernel<true, false><<<dim3(kBig / kBigRows, kmax, z), kBigNT, kBigRowsSmem, s>>>(b);
-      big_cols_kernel<false><<<dim3(kBig / kBigCols, kmax, z), kBigColsNT, kBigColsSmem, s>>>(b);
-      big_rows_kernel<false, false><<<dim3(inv_blocks, kmax, z), kBigNT, kBigRowsSmem, s>>>(b);
-      g_launches += 3;
-      FM_CUDA(cudaGetLastError());
+      // units in batches whose 256^2 scratch items (written and re-read by the three
+      // kernels) fit in L2, so the passes read back from L2 instead of HBM
+      int ub = nu;
+      if (g_big_l2_mb > 0) {
+        const int64_t item = (int64_t)kBig * kBig * 8 * kmax * n;
+        ub = (int)std::max<int64_t>(1, std::min<int64_t>(nu, ((int64_t)g_big_l2_mb << 20) / item));
+      }
+      for (int b0 = 0; b0 < nu; b0 += ub) {
+        b.lu0 = b0;
+        b.nub = std::min(ub, nu - b0);
+        const unsigned z = (unsigned)(b.nub * n);
+        big_rows_kernel<true, false><<<dim3(kBig / kBigRows, kmax, z), kBigNT, kBigRowsSmem, s>>>(b);
+        big_cols_kernel<false><<<dim3(kBig / kBigCols, kmax, z), kBigColsNT, kBigColsSmem, s>>>(b);
+        big_rows_kernel<false, false><<<dim3(inv_blocks, kmax, z), kBigNT, kBigRowsSmem, s>>>(b);
+        g_launches += 3;
+        FM_CUDA(cudaGetLastError());
+      }
       if (p->timing) {
         FM_CUDA(cudaEventRecord(next_event(p), s));
         p->pending_conv.push_back({e0, e0 + 1});
@@ -1543,6 +1584,8 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       t.se_min = p->se_min;
       t.fill = p->d.fill;
       t.dev_max = reinterpret_cast<float*>(p->stats);
+      t.chat16 = p->chat16 ? 1 : 0;
+      t.chat_invq_T = p->chat_invq_T;
       t.bucket_count = p->bucket_count[buf];
       t.ladder = p->d_ladder;
       t.lists = p->bucket_list[buf];
@@ -1568,16 +1611,16 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         for (int li = 0; li < L; ++li) {
           const int cnt = reinterpret_cast<volatile int*>(p->h_counts[buf])[li];
           planes += (double)cnt * (p->ladder[li] + 1);
-          tonal_b += (double)cnt * ((p->ladder[li] + 1) * (double)p->npx * 8.0 +
+          tonal_b += (double)cnt * ((p->ladder[li] + 1) * (double)p->npx * (p->chat16 ? 4.0 : 8.0) +
                                     (double)p->npx * (out_size(p->d.out_dtype) + (valid ? 1.0 : 0.0)));
         }
         if (!g_no_skip0 && img_defined == nullptr) {
           const double skipped = (double)n * (double)(p->full_prefix[u0 + nu] - p->full_prefix[u0]);
           planes -= skipped;
-          tonal_b -= skipped * (double)p->npx * 8.0;
+          tonal_b -= skipped * (double)p->npx * (p->chat16 ? 4.0 : 8.0);
         }
         p->planes_done += (int64_t)planes;
-        p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->npx * 8.0;
+        p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->npx * (p->chat16 ? 4.0 : 8.0);
         p->acc.conv_flops += planes * p->conv_flops_per_plane;
         p->acc.tonal_bytes += tonal_b;
       }
@@ -1648,6 +1691,8 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     t.se_min = p->se_min;
     t.fill = p->d.fill;
     t.dev_max = reinterpret_cast<float*>(p->stats);
+    t.chat16 = p->chat16 ? 1 : 0;
+    t.chat_invq_T = p->chat_invq_T;
     if (p->counts) {
       t.counts = reinterpret_cast<int32_t*>(out) + (size_t)c0 * npix * (size_t)(p->lr + 1);
       t.count_len = p->lr + 1;
@@ -1666,7 +1711,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       if (p->ladder[li] <= p->fuse_nmax) {
         const int N = p->ladder[li];
         planes += (double)cnt * (N + 1);
-        fused_b += (double)cnt * ((N + 1) * (double)p->npx * 8.0 +
+        fused_b += (double)cnt * ((N + 1) * (double)p->npx * (p->chat16 ? 4.0 : 8.0) +
                                   (double)p->npx * (out_size(p->d.out_dtype) + (valid ? 1.0 : 0.0)));
         continue;
       }
@@ -1712,7 +1757,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       g_launches++;
       FM_CUDA(cudaGetLastError());
       planes += (double)cnt * (N + 1);
-      tonal_b += (double)cnt * ((N + 1) * (double)p->npx * 8.0 +
+      tonal_b += (double)cnt * ((N + 1) * (double)p->npx * (p->chat16 ? 4.0 : 8.0) +
                                 (double)p->npx * (out_size(p->d.out_dtype) + (valid ? 1.0 : 0.0)));
     }
     for (int i = 0; i < nstreams - 1; ++i) {
@@ -1725,15 +1770,15 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       planes -= skipped;
       // (per-ladder counts of full units are not known here: with the fused step the
       // skipped planes are charged to it, else to the tonal kernels)
-      if (p->fuse_nmax > 0) fused_b -= skipped * (double)p->npx * 8.0;
-      else tonal_b -= skipped * (double)p->npx * 8.0;
+      if (p->fuse_nmax > 0) fused_b -= skipped * (double)p->npx * (p->chat16 ? 4.0 : 8.0);
+      else tonal_b -= skipped * (double)p->npx * (p->chat16 ? 4.0 : 8.0);
     }
     p->planes_done += (int64_t)planes;
     p->units_done += (int64_t)n * nu;
     if (p->timing) {
       FM_CUDA(cudaEventRecord(next_event(p), s));
       p->pending_tonal.push_back({e1, e1 + 1});
-      p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->npx * 8.0 + fused_b;
+      p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->npx * (p->chat16 ? 4.0 : 8.0) + fused_b;
       p->acc.conv_flops += planes * p->conv_flops_per_plane;
       p->acc.tonal_bytes += tonal_b;
     }

@@ -36,7 +36,8 @@ struct BigArgs {
   int T, K;                   // SPEC launch: the ladder entry
   const int4* unit_param;     // CONV: [imgs][units]
   int units;
-  int unit0, upl, nu;         // first unit, slots per image, units in this launch (grid z = imgs * nu)
+  int unit0, upl, nu;         // first unit, slots per image, units in this launch
+  int lu0, nub;               // this launch's unit batch: launch-local units [lu0, lu0 + nub), grid z = imgs * nub
   int K_max;
   float2* S;                  // [imgs][units][K_max][256][256] (CONV) or [K][256][256] (SPEC)
   const float4* spec;         // CONV: ladder base; SPEC: output
@@ -61,9 +62,9 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = blockIdx.y;
-  const int lu = SPEC ? 0 : (int)(blockIdx.z % a.nu);
+  const int lu = SPEC ? 0 : a.lu0 + (int)(blockIdx.z % a.nub);
   const int unit = SPEC ? 0 : a.unit0 + lu;
-  const int img = SPEC ? 0 : (int)(blockIdx.z / a.nu);
+  const int img = SPEC ? 0 : (int)(blockIdx.z / a.nub);
   int T = a.T, K = a.K, enc_bias = a.enc_bias;
   if constexpr (!SPEC) {
     const int4 up = a.unit_param[(size_t)img * a.units + unit];
@@ -272,9 +273,9 @@ __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a
 
   const int tid = threadIdx.x;
   const int cb = blockIdx.x, k = blockIdx.y;
-  const int lu = SPEC ? 0 : (int)(blockIdx.z % a.nu);
+  const int lu = SPEC ? 0 : a.lu0 + (int)(blockIdx.z % a.nub);
   const int unit = SPEC ? 0 : a.unit0 + lu;
-  const int img = SPEC ? 0 : (int)(blockIdx.z / a.nu);
+  const int img = SPEC ? 0 : (int)(blockIdx.z / a.nub);
   int K = a.K;
   const float4* spec_plane = nullptr;
   if constexpr (!SPEC) {

@@ -96,6 +96,8 @@ struct TileArgs {
   int cap, L;
   // fused tonal step (fm_fused.cuh, three-pass 128x128 kernel): the CTA completing a unit's
   // last plane chunk runs its inverse tonal FFT + threshold + store
+  int chat16;                 // spectral planes stored as int16 pairs, value * (chat_q_T * T) (fm_abi.cu)
+  float chat_q_T;
   int fuse_nmax;              // 0: off; else units with N_t <= fuse_nmax are finished here
   int discard;                // drop the consumed spectral lines from L2 (no write-back)
   int* unit_done;             // [imgs][upl] plane-chunk completion counters (self-resetting)
@@ -163,6 +165,14 @@ __device__ __forceinline__ int load_img(const void* img, int dtype, int64_t i) {
   if (dtype == 0) return (int)__ldg(reinterpret_cast<const uint8_t*>(img) + i);
   if (dtype == 1) return (int)__ldg(reinterpret_cast<const uint16_t*>(img) + i);
   return __ldg(reinterpret_cast<const int32_t*>(img) + i);
+}
+
+// complex value -> two int16 fixed-point numbers (round to nearest, saturating)
+__device__ __forceinline__ uint32_t pack16(float2 v, float q) {
+  unsigned short re, im;
+  asm("cvt.rni.sat.s16.f32 %0, %1;" : "=h"(re) : "f"(v.x * q));
+  asm("cvt.rni.sat.s16.f32 %0, %1;" : "=h"(im) : "f"(v.y * q));
+  return (uint32_t)re | ((uint32_t)im << 16);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -197,7 +197,11 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
   __syncthreads();
   // the plane loop bound lives in shared memory (a register copy would be spilled)
   const volatile int* kend_s = &s_kend;
-  float2* chat_unit = SPEC ? nullptr : a.chat + ((size_t)img * a.upl + (unit - a.unit0)) * a.K_max * (size_t)a.wpx;
+  // the unit's planes (8-byte complex64 elements, or 4-byte int16 pairs with chat16)
+  float2* chat_unit = SPEC ? nullptr
+                           : reinterpret_cast<float2*>(reinterpret_cast<char*>(a.chat) +
+                                                       ((size_t)img * a.upl + (unit - a.unit0)) * a.K_max *
+                                                           (size_t)a.wpx * (a.chat16 ? 4 : 8));
 
   // thread roles
   // F1 / I1: column x = (c + mx - 1) mod 128 for c = 32 (warp>>2) + lane, so the
@@ -435,7 +439,20 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
         const int hi = min(32, (max(0, y_end - f_n2) + 3) >> 2);
         const uint32_t below_hi = hi >= 32 ? 0xFFFFFFFFu : ((1u << hi) - 1u);
         const uint32_t rows = hi > lo ? below_hi & ~((1u << lo) - 1u) : 0u;
-        float2* dst = chat_unit + ((ptrdiff_t)k * a.wpx + (ptrdiff_t)(f_n2 - (a.my - 1)) * a.QX + f_c);
+        const ptrdiff_t e0 = (ptrdiff_t)k * a.wpx + (ptrdiff_t)(f_n2 - (a.my - 1)) * a.QX + f_c;
+        if (a.chat16) {
+          // 16-bit planes: int16 pairs at the unit's fixed-point scale (half the bytes)
+          const float q = a.chat_q_T * (float)T;
+          uint64_t pa = reinterpret_cast<uint64_t>(reinterpret_cast<uint32_t*>(chat_unit) + e0);
+          const uint64_t step_b = (uint64_t)(4 * a.QX) * sizeof(uint32_t);
+#pragma unroll
+          for (int n1 = 0; n1 < 32; ++n1) {
+            if ((rows >> n1) & 1u)
+              asm volatile("st.global.b32 [%0], %1;" ::"l"(pa), "r"(pack16(v[n1], q)) : "memory");
+            asm("add.s64 %0, %0, %1;" : "+l"(pa) : "l"(step_b));
+          }
+        } else {
+        float2* dst = chat_unit + e0;
         // the running row address is kept in a register by inline PTX (left to
         // itself the compiler re-derives it from the kernel parameter every row)
         uint64_t pa = reinterpret_cast<uint64_t>(dst);
@@ -445,6 +462,7 @@ __global__ void __launch_bounds__(512, 1) tile128_kernel(const TileArgs a) {
           if ((rows >> n1) & 1u)
             asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(pa), "f"(v[n1].x), "f"(v[n1].y) : "memory");
           asm("add.s64 %0, %0, %1;" : "+l"(pa) : "l"(step_b));
+        }
         }
       }
       // no barrier: the next plane's F1 writes exactly the slots this thread read

@@ -52,7 +52,24 @@ struct TonalArgs {
   const int* ladder;         // [L] N of each entry
   const int2* lists;         // [L][cap] work lists
   int L, cap, se_count;
+  // 16-bit spectral planes (plan chat16): each complex value stored as two int16
+  // fixed-point numbers; value = stored * chat_invq_T / T (see fm_abi.cu)
+  int chat16;
+  float chat_invq_T;
 };
+
+// One spectral value of pixel index `idx` (elements of the window-local planes):
+// complex64, or a pair of int16 fixed-point numbers scaled by `invq` (16-bit planes).
+__device__ __forceinline__ float2 unpack16(uint32_t w, float invq) {
+  float re, im;
+  asm("cvt.rn.f32.s16 %0, %1;" : "=f"(re) : "h"((unsigned short)(w & 0xFFFFu)));
+  asm("cvt.rn.f32.s16 %0, %1;" : "=f"(im) : "h"((unsigned short)(w >> 16)));
+  return make_float2(re * invq, im * invq);
+}
+__device__ __forceinline__ float2 chat_ld(const TonalArgs& a, size_t idx, float invq) {
+  if (a.chat16) return unpack16(__ldcs(reinterpret_cast<const unsigned int*>(a.chat) + idx), invq);
+  return __ldcs(a.chat + idx);
+}
 
 __device__ __forceinline__ void store_out(const TonalArgs& a, size_t i, int v) {
   switch (a.out_dtype) {
@@ -255,12 +272,13 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
   const size_t plane = a.wpx;
   float dev = 0.f;
   if (pp.live) {
-    const float2* src = a.chat + pp.src;
+    const float invq = a.chat_invq_T / (float)(2 * N);
     int top;
     if constexpr (!SM) {
       float2 X[N + 1];
 #pragma unroll
-      for (int k = 0; k <= N; ++k) X[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : __ldcs(src + (size_t)k * plane);
+      for (int k = 0; k <= N; ++k)
+        X[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : chat_ld(a, pp.src + (size_t)k * plane, invq);
       float2 A[N], B[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
@@ -275,8 +293,9 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
       SmemArr<NT> A{tsm_t + threadIdx.x}, B{tsm_t + (size_t)N * NT + threadIdx.x};
       // X[0..N-1] -> B, X[N] stays in a register
 #pragma unroll 8
-      for (int k = 0; k < N; ++k) B[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : __ldcs(src + (size_t)k * plane);
-      const float2 xN = __ldcs(src + (size_t)N * plane);
+      for (int k = 0; k < N; ++k)
+        B[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : chat_ld(a, pp.src + (size_t)k * plane, invq);
+      const float2 xN = chat_ld(a, pp.src + (size_t)N * plane, invq);
 #pragma unroll 4
       for (int k = 0; k < N; ++k) {
         const float2 xk = B[k];
@@ -312,11 +331,12 @@ __host__ __device__ constexpr int tonal_ns_at(int i) {
 template <int N>
 __device__ __forceinline__ void tonal_pixel_reg(const TonalArgs& a, const TonalPix& pp, float& dev) {
   constexpr int off = tonal_off(N);
-  const float2* src = a.chat + pp.src;
   const float x0 = (float)((double)a.se_count / (2.0 * N));
+  const float invq = a.chat_invq_T / (float)(2 * N);
   float2 X[N + 1];
 #pragma unroll
-  for (int k = 0; k <= N; ++k) X[k] = (k == 0 && pp.full) ? make_float2(x0, 0.f) : __ldcs(src + (size_t)k * a.wpx);
+  for (int k = 0; k <= N; ++k)
+    X[k] = (k == 0 && pp.full) ? make_float2(x0, 0.f) : chat_ld(a, pp.src + (size_t)k * a.wpx, invq);
   float2 A[N], B[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) {
@@ -417,7 +437,10 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a, 
   constexpr int K = N + 1;
   constexpr int off = tonal_off(N);
   constexpr int NCW = NT / 32;
-  extern __shared__ __align__(128) float2 tstg[];   // [ST][K][NT]
+  extern __shared__ __align__(128) float2 tstg[];   // [ST][K][NT] of complex64 (or int16 pairs: chat16)
+  unsigned char* stg_b = reinterpret_cast<unsigned char*>(tstg);
+  const size_t esz = a.chat16 ? 4 : 8;               // bytes per stored spectral value
+  const float invq = a.chat_invq_T / (float)(2 * N);
   __shared__ __align__(8) uint64_t full[ST], empty[ST];
   __shared__ int stage_k0[ST];   // 1: the stage's unit has a known plane 0 (not copied)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -455,19 +478,21 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a, 
         const int k0 = (job.y & kJobFull) ? 1 : 0;   // plane 0 known (not copied)
         if (a.use_tma) {
           stage_k0[st] = k0;   // published to the consumers by the arrive below
-          mbar_expect_tx(&full[st], (uint32_t)(NT * 8 * (K - k0)));
+          mbar_expect_tx(&full[st], (uint32_t)(NT * esz * (K - k0)));
           const int row = ((job.x * a.upl + ((job.y & ~kJobFull) - a.unit0)) * a.K_max) + k0;
-          tma_load_2d(tstg + (size_t)st * K * NT + k0 * NT, k0 ? &tm1 : &tm, blk * NT, row, &full[st], pol);
+          tma_load_2d(stg_b + ((size_t)st * K * NT + k0 * NT) * esz, k0 ? &tm1 : &tm, blk * NT, row, &full[st], pol);
           continue;
         }
-        const float2* src = a.chat + ((size_t)job.x * a.upl + ((job.y & ~kJobFull) - a.unit0)) * a.K_max * (size_t)a.wpx +
-                            (size_t)blk * NT;
-        const uint32_t bytes = (uint32_t)min(NT, a.wpx - blk * NT) * 8u;
+        const char* src = reinterpret_cast<const char*>(a.chat) +
+                          (((size_t)job.x * a.upl + ((job.y & ~kJobFull) - a.unit0)) * a.K_max * (size_t)a.wpx +
+                           (size_t)blk * NT) * esz;
+        const uint32_t bytes = (uint32_t)min(NT, a.wpx - blk * NT) * (uint32_t)esz;
         stage_k0[st] = k0;   // published to the consumers by the arrive below
         mbar_expect_tx(&full[st], bytes * (K - k0));
-        float2* dst = tstg + (size_t)st * K * NT;
+        unsigned char* dst = stg_b + (size_t)st * K * NT * esz;
 #pragma unroll 1
-        for (int k = k0; k < K; ++k) bulk_g2s(dst + k * NT, src + (size_t)k * a.wpx, bytes, &full[st], pol);
+        for (int k = k0; k < K; ++k)
+          bulk_g2s(dst + (size_t)k * NT * esz, src + (size_t)k * a.wpx * esz, bytes, &full[st], pol);
       }
     }
     return;
@@ -480,26 +505,28 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a, 
     mbar_wait(&full[st], (uint32_t)((i / ST) & 1));
     const int j = item / bpj, blk = item - j * bpj;
     const TonalPix pp = tonal_pixel_job(a, a.list[j], blk * NT + tid);
-    const float2* xs = tstg + (size_t)st * K * NT + tid;
+    const float2* xs8 = tstg + (size_t)st * K * NT + tid;
+    const uint32_t* xs4 = reinterpret_cast<const uint32_t*>(tstg) + (size_t)st * K * NT + tid;
+    auto xs = [&](int i) -> float2 { return a.chat16 ? unpack16(xs4[i], invq) : xs8[i]; };
     float2 A[N], B[N];
     // c2r packing Z[k] = s_k + i w_k d_k, s_k = X[k] + X[N-k]^*, d_k = X[k] - X[N-k]^*,
     // w_k = exp(+2 pi i k / T); the partner N-k reuses s, d and m = w_k d_k:
     // Z[N-k] = s^* + i m^*  (w_{N-k} = -w_k^*, d_{N-k} = -d_k^*)
     {
-      const float2 x0 = stage_k0[st] ? make_float2(a.x0_full, 0.f) : xs[0];
-      const float2 xc = conjf2(xs[N * NT]);
+      const float2 x0 = stage_k0[st] ? make_float2(a.x0_full, 0.f) : xs(0);
+      const float2 xc = conjf2(xs(N * NT));
       A[0] = cadd(cadd(x0, xc), mul_pi(csub(x0, xc)));
     }
 #pragma unroll
     for (int k = 1; 2 * k < N; ++k) {
-      const float2 xk = xs[k * NT], xm = conjf2(xs[(N - k) * NT]);
+      const float2 xk = xs(k * NT), xm = conjf2(xs((N - k) * NT));
       const float2 sk = cadd(xk, xm), dk = csub(xk, xm);
       const float2 m = cmul(c_ttw[off + k], dk);
       A[k] = cadd_i(sk, m);                       // s + i m
       A[N - k] = cadd_i(conjf2(sk), conjf2(m));   // s^* + i m^*
     }
     if constexpr (N % 2 == 0 && N > 0) {
-      const float2 xh = xs[(N / 2) * NT];
+      const float2 xh = xs((N / 2) * NT);
       A[N / 2] = make_float2(2.f * xh.x, -2.f * xh.y);
     }
     __syncwarp();
@@ -538,10 +565,11 @@ __global__ void __launch_bounds__(128) tonal_kernel(const TonalArgs a) {
   const size_t plane = a.wpx;
   float dev = 0.f;
   if (pp.live) {
-    const float2* src = a.chat + pp.src;
+    const float invq = a.chat_invq_T / (float)(2 * N);
     float2* A = bufA + (size_t)threadIdx.x * a.stride;
     float2* B = bufB + (size_t)threadIdx.x * a.stride;
-    for (int k = 0; k <= N; ++k) A[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : __ldcs(src + (size_t)k * plane);
+    for (int k = 0; k <= N; ++k)
+      A[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : chat_ld(a, pp.src + (size_t)k * plane, invq);
     // c2r packing: Z[k] = (X[k] + X[N-k]^*) + i w_T^{-k}... so that the
     // unnormalised length-N inverse DFT of Z gives z[n] = c(2n) + i c(2n+1).
     for (int k = 0; k < N; ++k) {
