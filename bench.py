@@ -449,8 +449,10 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32",
-        "dtype_note": "FFT arithmetic in FP32 (the reference uses f64); exact integer results: worst "
-                      f"pre-rounding deviation {dev_max:.2e}, margin {0.5 / max(dev_max, 1e-30):.0f}x to 0.5",
+        "dtype_note": "FFT arithmetic in FP32 (the reference uses f64); spectral planes between the passes stored "
+                      "as int16 pairs at a per-tile fixed-point scale (analytic count error <= sqrt(2) C/64000, "
+                      f"C = defined SE entries); exact integer results: worst pre-rounding deviation {dev_max:.2e}, "
+                      f"margin {0.5 / max(dev_max, 1e-30):.0f}x to 0.5",
         "data": "synthetic (SURVEY §8(d) c5 recipe, seeded PCG64)",
         "config": {"workload": WORKLOAD, "images": args.images, "images_per_gpu": nloc,
                    "out_dtype": args.out_dtype, "tonal_len": info["tonal_len"],

@@ -1,4 +1,4 @@
-TAG=r2a
+TAG=r2b
 mkdir -p gpurun_out
 python -c "from paper_2305_03018_b200 import build; build.build()" > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:"tile128_kernelIhLb0E|tonal_kernel_pipeILi18E|range_kernelILi0E" -c 3 -o gpurun_out/prof_$TAG \
