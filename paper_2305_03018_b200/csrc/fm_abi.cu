@@ -281,6 +281,8 @@ const int g_big_steps = std::getenv("FM_BIG_STEPS") ? std::atoi(std::getenv("FM_
 const int g_big_l2_mb = std::getenv("FM_BIG_L2_MB") ? std::atoi(std::getenv("FM_BIG_L2_MB")) : 0;
 // FM_CHAT16=0 keeps complex64 spectral planes (A/B)
 const bool g_chat16 = !(std::getenv("FM_CHAT16") && std::getenv("FM_CHAT16")[0] == '0');
+// FM_OVERLAP=0: the tonal pass of a launch step and the next step's conv stay serialised (A/B)
+const bool g_overlap = !(std::getenv("FM_OVERLAP") && std::getenv("FM_OVERLAP")[0] == '0');
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
@@ -408,6 +410,12 @@ struct fm_plan {
   void* part_out = nullptr;               // [batch][OH][OW] of out_dtype
   uint8_t* part_valid = nullptr;          // [batch][OH][OW]
   uint8_t* acc_valid = nullptr;           // [batch][OH][OW] when the caller passes no validity
+  // conv of launch step i+1 overlapping the tonal pass of step i: two spectral buffer sets
+  // (chat16 keeps their sum within the scratch budget), the tonal passes on their own stream
+  bool overlap = false;
+  size_t chat_set_bytes = 0;
+  cudaStream_t tstream = nullptr;
+  cudaEvent_t conv_ev[2] = {}, tjoin_ev = nullptr;
   // 16-bit spectral planes (chat16): int16 pairs at scale q = chat_q_T * T (see fm_plan_create)
   bool chat16 = false;
   float chat_q_T = 0.f, chat_invq_T = 0.f;
@@ -460,6 +468,10 @@ void free_plan(fm_plan* p) {
   cudaFree(p->enc_tab);
   cudaFree(p->d_enc_off);
   cudaFree(p->unit_done);
+  if (p->tstream) cudaStreamDestroy(p->tstream);
+  for (int b = 0; b < 2; ++b)
+    if (p->conv_ev[b]) cudaEventDestroy(p->conv_ev[b]);
+  if (p->tjoin_ev) cudaEventDestroy(p->tjoin_ev);
   cudaFree(p->S);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
@@ -1119,7 +1131,15 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     if ((e = cudaMalloc(&p->unit_done, sizeof(int) * (size_t)slots)) != cudaSuccess) return cfail(e, "counter alloc");
     cudaMemset(p->unit_done, 0, sizeof(int) * (size_t)slots);
   }
-  if ((e = cudaMalloc(&p->chat, (size_t)slots * p->K * p->wpx * (p->chat16 ? 4 : 8))) != cudaSuccess) {
+  p->chat_set_bytes = (size_t)slots * p->K * p->wpx * (p->chat16 ? 4 : 8);
+  p->overlap = g_overlap && p->chat16 && !p->counts && !p->big && p->fuse_nmax == 0;
+  if (p->overlap) {
+    if ((e = cudaStreamCreateWithFlags(&p->tstream, cudaStreamNonBlocking)) != cudaSuccess) return cfail(e, "stream");
+    for (int b = 0; b < 2; ++b)
+      if ((e = cudaEventCreateWithFlags(&p->conv_ev[b], cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+    if ((e = cudaEventCreateWithFlags(&p->tjoin_ev, cudaEventDisableTiming)) != cudaSuccess) return cfail(e, "event");
+  }
+  if ((e = cudaMalloc(&p->chat, p->chat_set_bytes * (p->overlap ? 2 : 1))) != cudaSuccess) {
     free_plan(p);
     return fail(FM_ENOMEM, std::string("spectral scratch alloc: ") + cudaGetErrorString(e));
   }
@@ -1133,8 +1153,9 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
       const int K = p->ladder[li] + 1;
       const int bx = tv ? tv->pipe_nt : 128;
       const int esz = p->chat16 ? 4 : 8;
-      ok = encode_chat_map(&maps[2 * li], p->chat, p->wpx, slots * p->K, bx, K, esz) &&
-           encode_chat_map(&maps[2 * li + 1], p->chat, p->wpx, slots * p->K, bx, std::max(1, K - 1), esz);
+      const int64_t rows = slots * p->K * (p->overlap ? 2 : 1);
+      ok = encode_chat_map(&maps[2 * li], p->chat, p->wpx, rows, bx, K, esz) &&
+           encode_chat_map(&maps[2 * li + 1], p->chat, p->wpx, rows, bx, std::max(1, K - 1), esz);
     }
     if (ok) p->tmaps = std::move(maps);
   }
@@ -1283,7 +1304,7 @@ static int out_size(int od) { return od == FM_OUT_U8 ? 1 : (od == FM_OUT_U16 || 
 static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, void* out, uint8_t* valid,
                       cudaStream_t s, int64_t cbeg, int64_t cend,
                       const std::vector<std::pair<int64_t, int>>* chunks = nullptr, const cudaEvent_t* in_ready = nullptr,
-                      const std::function<int(size_t, int64_t, int)>& after_chunk = nullptr) {
+                      const std::function<int(size_t, int64_t, int, cudaStream_t)>& after_chunk = nullptr) {
   p->last_stream = s;
   const int64_t npix = p->OH * p->OW;
   const int64_t img_elems = p->H * p->W;
@@ -1425,6 +1446,11 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     const int64_t c0 = steps[si].c0;
     const int n = steps[si].n, u0 = steps[si].u0, nu = steps[si].nu;
     FM_CUDA(cudaStreamWaitEvent(s, p->count_ev[buf], 0));
+    // this step's spectral buffer set (two sets alternate when the tonal pass of a step
+    // overlaps the next step's conv)
+    float2* chat_set = reinterpret_cast<float2*>(reinterpret_cast<char*>(p->chat) +
+                                                 (p->overlap ? (size_t)buf * p->chat_set_bytes : 0));
+    cudaStream_t tsm = p->overlap ? p->tstream : s;   // where this step's tonal pass runs
     TileArgs a{};
     a.img = reinterpret_cast<const char*>(img) + (size_t)c0 * img_elems * dsz;
     a.img_def = img_defined ? img_defined + (size_t)c0 * img_elems : nullptr;
@@ -1448,7 +1474,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     a.enc_sign = p->enc_sign;
     a.enc_bias = p->enc_bias;
     a.spec = p->spec;
-    a.chat = p->chat;
+    a.chat = chat_set;
     a.err = p->stats + 1;
     a.unit_param = p->unit_param[buf];
     a.spec_off = p->d_spec_off;
@@ -1560,7 +1586,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       int rc = launch_conv((unsigned)(conv_target + (int64_t)nu * n));
       if (rc) return rc;
       TonalArgs t{};
-      t.chat = p->chat;
+      t.chat = chat_set;
       t.K_max = p->K;
       t.unit_param = p->unit_param[buf];
       t.units = p->units;
@@ -1626,7 +1652,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       }
       FM_CUDA(cudaEventRecord(p->free_ev[buf], s));
       if (after_chunk && u0 + nu >= p->units) {
-        int rc2 = after_chunk(steps[si].chunk, c0, n);
+        int rc2 = after_chunk(steps[si].chunk, c0, n, s);
         if (rc2) return rc2;
       }
       continue;
@@ -1667,7 +1693,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       }
     }
     TonalArgs t{};
-    t.chat = p->chat;
+    t.chat = chat_set;
     t.K_max = p->K;
     t.unit_param = p->unit_param[buf];
     t.units = p->units;
@@ -1698,8 +1724,14 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       t.count_len = p->lr + 1;
       t.count_base = p->d.img_min;
     }
+    // the tonal pass runs on tsm after this step's conv (with overlap, beside the next
+    // step's conv on s)
+    if (p->overlap) {
+      FM_CUDA(cudaEventRecord(p->conv_ev[buf], s));
+      FM_CUDA(cudaStreamWaitEvent(tsm, p->conv_ev[buf], 0));
+    }
     int e1 = -1;
-    if (p->timing) { e1 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
+    if (p->timing) { e1 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), tsm)); }
     double planes = 0, tonal_b = 0;
     // one launch per ladder entry in use, spread over the aux streams so the
     // small ones (few units each) run side by side; joined back into s
@@ -1719,7 +1751,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     }
     const int nstreams = std::min(nlaunch, 1 + kAuxStreams);
     if (nstreams > 1) {
-      FM_CUDA(cudaEventRecord(p->ev_fork, s));
+      FM_CUDA(cudaEventRecord(p->ev_fork, tsm));
       for (int i = 0; i < nstreams - 1; ++i) FM_CUDA(cudaStreamWaitEvent(p->aux[i], p->ev_fork, 0));
     }
     int launch_i = 0;
@@ -1728,7 +1760,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       if (cnt <= 0 || p->ladder[li] <= p->fuse_nmax) continue;
       const int N = p->ladder[li];
       const int si = launch_i++ % nstreams;
-      cudaStream_t ts = si == 0 ? s : p->aux[si - 1];
+      cudaStream_t ts = si == 0 ? tsm : p->aux[si - 1];
       t.N = N;
       t.T = 2 * N;
       t.x0_full = (float)((double)p->se_count / (2.0 * N));
@@ -1741,6 +1773,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         const int grid = (int)std::min<int64_t>(items, (int64_t)g_num_sms * std::min(occ, g_tonal_occ_cap));
         static const CUtensorMap kNoMap[2] = {};
         t.use_tma = p->tmaps.empty() ? 0 : 1;
+        t.tma_row0 = p->overlap ? buf * (int)(cap * p->K) : 0;
         tv->pipe_fn(dim3((unsigned)grid), tv->pipe_nt, tv->pipe_smem, ts, t, t.use_tma ? &p->tmaps[2 * li] : kNoMap);
       } else if (tv) {
         const int nt = tv->nt;
@@ -1762,7 +1795,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     }
     for (int i = 0; i < nstreams - 1; ++i) {
       FM_CUDA(cudaEventRecord(p->ev_join[i], p->aux[i]));
-      FM_CUDA(cudaStreamWaitEvent(s, p->ev_join[i], 0));
+      FM_CUDA(cudaStreamWaitEvent(tsm, p->ev_join[i], 0));
     }
     // full units (fm_range.cuh) skip plane 0: fewer planes computed, stored and read
     if (!g_no_skip0 && img_defined == nullptr) {
@@ -1776,17 +1809,21 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     p->planes_done += (int64_t)planes;
     p->units_done += (int64_t)n * nu;
     if (p->timing) {
-      FM_CUDA(cudaEventRecord(next_event(p), s));
+      FM_CUDA(cudaEventRecord(next_event(p), tsm));
       p->pending_tonal.push_back({e1, e1 + 1});
       p->acc.conv_bytes += (double)n * img_elems * dsz * nu / p->units + planes * (double)p->npx * (p->chat16 ? 4.0 : 8.0) + fused_b;
       p->acc.conv_flops += planes * p->conv_flops_per_plane;
       p->acc.tonal_bytes += tonal_b;
     }
-    FM_CUDA(cudaEventRecord(p->free_ev[buf], s));
+    FM_CUDA(cudaEventRecord(p->free_ev[buf], tsm));
     if (after_chunk && u0 + nu >= p->units) {
-      int rc = after_chunk(steps[si].chunk, c0, n);
+      int rc = after_chunk(steps[si].chunk, c0, n, tsm);
       if (rc) return rc;
     }
+  }
+  if (p->overlap) {   // the caller's stream sees every step's outputs
+    FM_CUDA(cudaEventRecord(p->tjoin_ev, p->tstream));
+    FM_CUDA(cudaStreamWaitEvent(s, p->tjoin_ev, 0));
   }
   return FM_OK;
 }
@@ -2056,8 +2093,8 @@ int fm_execute_host(fm_plan* p, const void* img_host, const uint8_t* def_host, v
     FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci], hs));
     in_ev[ci] = p->ev_chunks[2 * ci];
   }
-  auto after = [&](size_t ci, int64_t c0, int n) -> int {
-    FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci + 1], s));
+  auto after = [&](size_t ci, int64_t c0, int n, cudaStream_t done) -> int {
+    FM_CUDA(cudaEventRecord(p->ev_chunks[2 * ci + 1], done));   // the chunk's outputs are written on `done`
     FM_CUDA(cudaStreamWaitEvent(ds, p->ev_chunks[2 * ci + 1], 0));
     FM_CUDA(cudaMemcpyAsync(out_host + c0 * out_e * osz, reinterpret_cast<char*>(p->h_out) + c0 * out_e * osz,
                             n * out_e * osz, cudaMemcpyDeviceToHost, ds));

@@ -47,6 +47,7 @@ struct TonalArgs {
   // have plane 0 = (defined SE entries) / T everywhere; the conv kernel skips it
   float x0_full;
   int use_tma;            // pipelined kernel: stages by 2-D tensor copies (maps passed beside the args)
+  int tma_row0;           // first map row of this launch's spectral buffer set (double-buffered plans)
   // device-dispatched kernel (small launches): every ladder entry in one launch
   const int* bucket_count;   // [L] units per ladder entry
   const int* ladder;         // [L] N of each entry
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(NT + 32) tonal_kernel_pipe(const TonalArgs a, 
         if (a.use_tma) {
           stage_k0[st] = k0;   // published to the consumers by the arrive below
           mbar_expect_tx(&full[st], (uint32_t)(NT * esz * (K - k0)));
-          const int row = ((job.x * a.upl + ((job.y & ~kJobFull) - a.unit0)) * a.K_max) + k0;
+          const int row = a.tma_row0 + ((job.x * a.upl + ((job.y & ~kJobFull) - a.unit0)) * a.K_max) + k0;
           tma_load_2d(stg_b + ((size_t)st * K * NT + k0 * NT) * esz, k0 ? &tm1 : &tm, blk * NT, row, &full[st], pol);
           continue;
         }
