@@ -1031,7 +1031,7 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
   // 0.25).  Enabled for C <= 2048 (bound <= 0.045) on the three-pass 128^2 kernels;
   // the measured deviation (fm_read_stats) includes it.  Halves the spectral volume's
   // bytes (conv writes, tonal reads).
-  if (g_chat16 && !p->counts && !p->big && p->fuse_nmax == 0 && p->two_d && bv && bv->tmax < (1 << 30) &&
+  if (g_chat16 && !p->counts && !p->big && p->two_d && bv && bv->tmax < (1 << 30) &&
       p->se_count <= kChat16MaxCount) {
     p->chat16 = true;
     p->chat_q_T = (float)(32000.0 / (double)p->se_count);

@@ -22,7 +22,7 @@
 // conv CTA: 128 per thread).
 #pragma once
 #include "fm_tile.cuh"
-#include "fm_tonal.cuh"
+#include "fm_tonal.cuh"   // (unpack16: 16-bit planes)
 
 namespace fm {
 
@@ -65,12 +65,17 @@ __device__ __forceinline__ void fused_tonal_unit(const TileArgs& a, const float2
   const int k0 = full ? 1 : 0;
   const int ST = 2 * K * NT <= stg_slots ? 2 : 1;
   const float x0 = (float)((double)a.se_count / (2.0 * N));
+  // element size of the stored planes: complex64, or int16 pairs (16-bit planes)
+  const int esz = a.chat16 ? 4 : 8;
+  const float invq = a.chat16 ? 1.0f / (a.chat_q_T * (float)(2 * N)) : 1.f;
+  const char* cu = reinterpret_cast<const char*>(chat_unit);
+  unsigned char* sb = reinterpret_cast<unsigned char*>(stg);
   auto issue = [&](int blk, int st) {   // thread 0: the block's planes k0..K-1 into stage st
     const int p0 = blk * NT;
-    const uint32_t bytes = (uint32_t)min(NT, a.wpx - p0) * 8u;   // wpx even: 16-byte multiples
+    const uint32_t bytes = (uint32_t)min(NT, a.wpx - p0) * (uint32_t)esz;   // wpx a multiple of 4: 16-byte multiples
     mbar_expect_tx(&bars[st], bytes * (uint32_t)(K - k0));
     for (int k = k0; k < K; ++k)
-      bulk_g2s_nohint(stg + (size_t)(st * K + k) * NT, chat_unit + (size_t)k * a.wpx + p0, bytes, &bars[st]);
+      bulk_g2s_nohint(sb + (size_t)(st * K + k) * NT * esz, cu + ((size_t)k * a.wpx + p0) * esz, bytes, &bars[st]);
   };
   if (tid == 0) {
     // the conv passes last wrote these bytes through the generic proxy
@@ -86,8 +91,10 @@ __device__ __forceinline__ void fused_tonal_unit(const TileArgs& a, const float2
     mbar_wait(&bars[st], par);
     float2 X[K];
     const float2* xs = stg + (size_t)st * K * NT + tid;
+    const uint32_t* xs4 = reinterpret_cast<const uint32_t*>(stg) + (size_t)st * K * NT + tid;
 #pragma unroll
-    for (int k = 0; k < K; ++k) X[k] = (k == 0 && full) ? make_float2(x0, 0.f) : xs[(size_t)k * NT];
+    for (int k = 0; k < K; ++k)
+      X[k] = (k == 0 && full) ? make_float2(x0, 0.f) : (a.chat16 ? unpack16(xs4[(size_t)k * NT], invq) : xs[(size_t)k * NT]);
     __syncthreads();   // every thread has read the stage
     if (tid == 0 && blk + ST < nblk) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -178,8 +185,9 @@ __device__ __forceinline__ void fused_tail(const TileArgs& a, float2* chat_unit,
   if (a.discard) {
     // the unit's planes are consumed: drop their L2 lines without a write-back
     __syncthreads();
-    const char* b0 = reinterpret_cast<const char*>(chat_unit + (size_t)(full ? 1 : 0) * a.wpx);
-    const char* b1 = reinterpret_cast<const char*>(chat_unit + (size_t)K * a.wpx);
+    const size_t esz = a.chat16 ? 4 : 8;
+    const char* b0 = reinterpret_cast<const char*>(chat_unit) + (size_t)(full ? 1 : 0) * a.wpx * esz;
+    const char* b1 = reinterpret_cast<const char*>(chat_unit) + (size_t)K * a.wpx * esz;
     const uintptr_t first = ((uintptr_t)b0 + 127) & ~(uintptr_t)127, last = (uintptr_t)b1 & ~(uintptr_t)127;
     for (uintptr_t l = first + (uintptr_t)threadIdx.x * 128; l < last; l += (uintptr_t)NT * 128)
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(l) : "memory");

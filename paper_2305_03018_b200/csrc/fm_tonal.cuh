@@ -277,9 +277,16 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
     int top;
     if constexpr (!SM) {
       float2 X[N + 1];
+      if (a.chat16) {   // (two loops: the element format is uniform per launch)
+        const unsigned int* src = reinterpret_cast<const unsigned int*>(a.chat) + pp.src;
 #pragma unroll
-      for (int k = 0; k <= N; ++k)
-        X[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : chat_ld(a, pp.src + (size_t)k * plane, invq);
+        for (int k = 0; k <= N; ++k) X[k] = unpack16(__ldcs(src + (size_t)k * plane), invq);
+      } else {
+        const float2* src = a.chat + pp.src;
+#pragma unroll
+        for (int k = 0; k <= N; ++k) X[k] = __ldcs(src + (size_t)k * plane);
+      }
+      if (pp.full) X[0] = make_float2(a.x0_full, 0.f);
       float2 A[N], B[N];
 #pragma unroll
       for (int k = 0; k < N; ++k) {
@@ -293,9 +300,16 @@ __global__ void __launch_bounds__(NT) tonal_kernel_t(const TonalArgs a) {
       extern __shared__ __align__(16) float2 tsm_t[];
       SmemArr<NT> A{tsm_t + threadIdx.x}, B{tsm_t + (size_t)N * NT + threadIdx.x};
       // X[0..N-1] -> B, X[N] stays in a register
+      if (a.chat16) {
+        const unsigned int* src = reinterpret_cast<const unsigned int*>(a.chat) + pp.src;
 #pragma unroll 8
-      for (int k = 0; k < N; ++k)
-        B[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : chat_ld(a, pp.src + (size_t)k * plane, invq);
+        for (int k = 0; k < N; ++k) B[k] = unpack16(__ldcs(src + (size_t)k * plane), invq);
+      } else {
+        const float2* src = a.chat + pp.src;
+#pragma unroll 8
+        for (int k = 0; k < N; ++k) B[k] = __ldcs(src + (size_t)k * plane);
+      }
+      if (pp.full) B[0] = make_float2(a.x0_full, 0.f);
       const float2 xN = chat_ld(a, pp.src + (size_t)N * plane, invq);
 #pragma unroll 4
       for (int k = 0; k < N; ++k) {
@@ -569,8 +583,14 @@ __global__ void __launch_bounds__(128) tonal_kernel(const TonalArgs a) {
     const float invq = a.chat_invq_T / (float)(2 * N);
     float2* A = bufA + (size_t)threadIdx.x * a.stride;
     float2* B = bufB + (size_t)threadIdx.x * a.stride;
-    for (int k = 0; k <= N; ++k)
-      A[k] = (k == 0 && pp.full) ? make_float2(a.x0_full, 0.f) : chat_ld(a, pp.src + (size_t)k * plane, invq);
+    if (a.chat16) {
+      const unsigned int* src = reinterpret_cast<const unsigned int*>(a.chat) + pp.src;
+      for (int k = 0; k <= N; ++k) A[k] = unpack16(__ldcs(src + (size_t)k * plane), invq);
+    } else {
+      const float2* src = a.chat + pp.src;
+      for (int k = 0; k <= N; ++k) A[k] = __ldcs(src + (size_t)k * plane);
+    }
+    if (pp.full) A[0] = make_float2(a.x0_full, 0.f);
     // c2r packing: Z[k] = (X[k] + X[N-k]^*) + i w_T^{-k}... so that the
     // unnormalised length-N inverse DFT of Z gives z[n] = c(2n) + i c(2n+1).
     for (int k = 0; k < N; ++k) {
