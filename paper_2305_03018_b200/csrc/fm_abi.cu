@@ -283,6 +283,8 @@ const int g_big_l2_mb = std::getenv("FM_BIG_L2_MB") ? std::atoi(std::getenv("FM_
 const bool g_chat16 = !(std::getenv("FM_CHAT16") && std::getenv("FM_CHAT16")[0] == '0');
 // FM_OVERLAP=0: the tonal pass of a launch step and the next step's conv stay serialised (A/B)
 const bool g_overlap = !(std::getenv("FM_OVERLAP") && std::getenv("FM_OVERLAP")[0] == '0');
+// FM_GRAPH=0: small calls launch their kernels one by one instead of replaying a graph (A/B)
+const bool g_graph = !(std::getenv("FM_GRAPH") && std::getenv("FM_GRAPH")[0] == '0');
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
@@ -410,6 +412,20 @@ struct fm_plan {
   void* part_out = nullptr;               // [batch][OH][OW] of out_dtype
   uint8_t* part_valid = nullptr;          // [batch][OH][OW]
   uint8_t* acc_valid = nullptr;           // [batch][OH][OW] when the caller passes no validity
+  // one-launch-step calls sized on the device replay a captured CUDA graph (keyed on the
+  // buffers and the stream): no per-kernel host launches, smaller gaps between the kernels
+  bool graphable = false, capturing = false;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev_in = nullptr, gev_out = nullptr;
+  int gmiss = 0;                          // captures so far (new buffer sets)
+  bool gstaged = false;                   // graph on plan-owned staging buffers
+  void* g_img = nullptr;
+  uint8_t* g_def = nullptr;
+  void* g_out = nullptr;
+  uint8_t* g_valid = nullptr;
+  const void* gkey[5] = {};
+  int64_t graph_kernels = 0;
   // conv of launch step i+1 overlapping the tonal pass of step i: two spectral buffer sets
   // (chat16 keeps their sum within the scratch budget), the tonal passes on their own stream
   bool overlap = false;
@@ -468,6 +484,14 @@ void free_plan(fm_plan* p) {
   cudaFree(p->enc_tab);
   cudaFree(p->d_enc_off);
   cudaFree(p->unit_done);
+  if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  cudaFree(p->g_img);
+  cudaFree(p->g_def);
+  cudaFree(p->g_out);
+  cudaFree(p->g_valid);
+  if (p->gstream) cudaStreamDestroy(p->gstream);
+  if (p->gev_in) cudaEventDestroy(p->gev_in);
+  if (p->gev_out) cudaEventDestroy(p->gev_out);
   if (p->tstream) cudaStreamDestroy(p->tstream);
   for (int b = 0; b < 2; ++b)
     if (p->conv_ev[b]) cudaEventDestroy(p->conv_ev[b]);
@@ -1226,6 +1250,10 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     if ((e = cudaGetLastError()) != cudaSuccess) return cfail(e, "SE spectrum launch");
   }
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cfail(e, "SE spectrum");
+  // a whole call is one device-dispatched launch step (run_images' devdisp): capturable
+  p->graphable = g_graph && !p->big && !p->counts && p->fuse_nmax == 0 && p->N <= kDispatchNMax &&
+                 p->ipc >= p->batch && p->upl >= p->units &&
+                 (int64_t)p->units * p->batch < (int64_t)g_num_sms * p->conv_occ * 2 && g_devdispatch;
   *out_plan = p;
   return FM_OK;
 }
@@ -1335,6 +1363,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     for (int u0 = 0; u0 < p->units; u0 += p->upl)
       steps.push_back({plan_chunks[ci].first, plan_chunks[ci].second, u0, std::min(p->upl, p->units - u0), ci});
   if (steps.empty()) return FM_OK;
+  bool used_tstream = false;
   // range kernels run one step ahead on a low-priority stream (double-buffered
   // outputs): they fill the conv tail and overlap the tonal kernels
   cudaStream_t rs = p->range_stream;
@@ -1351,7 +1380,9 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
   auto launch_range = [&](const Step& st, int buf) -> int {
     const int64_t c0 = st.c0;
     const int n = st.n, u0 = st.u0, nu = st.nu;
-    FM_CUDA(cudaStreamWaitEvent(rs, p->free_ev[buf], 0));   // the previous user of this buffer set
+    // the previous user of this buffer set (a graph replay is ordered on its stream as a whole,
+    // and a capture may not wait on events recorded outside it)
+    if (!p->capturing) FM_CUDA(cudaStreamWaitEvent(rs, p->free_ev[buf], 0));
     if (in_ready) FM_CUDA(cudaStreamWaitEvent(rs, in_ready[st.chunk], 0));
     // ---- per-unit tonal range -> ladder entry + work lists (fm_range.cuh)
     FM_CUDA(cudaMemsetAsync(p->bucket_count[buf], 0, sizeof(int) * L, rs));
@@ -1650,7 +1681,9 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         p->acc.conv_flops += planes * p->conv_flops_per_plane;
         p->acc.tonal_bytes += tonal_b;
       }
-      FM_CUDA(cudaEventRecord(p->free_ev[buf], s));
+      // (a capture records no persistent event: one recorded inside a graph cannot be
+      // waited on by a later direct call; replays are ordered through the caller's stream)
+      if (!p->capturing) FM_CUDA(cudaEventRecord(p->free_ev[buf], s));
       if (after_chunk && u0 + nu >= p->units) {
         int rc2 = after_chunk(steps[si].chunk, c0, n, s);
         if (rc2) return rc2;
@@ -1726,6 +1759,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     }
     // the tonal pass runs on tsm after this step's conv (with overlap, beside the next
     // step's conv on s)
+    used_tstream = used_tstream || p->overlap;
     if (p->overlap) {
       FM_CUDA(cudaEventRecord(p->conv_ev[buf], s));
       FM_CUDA(cudaStreamWaitEvent(tsm, p->conv_ev[buf], 0));
@@ -1821,7 +1855,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       if (rc) return rc;
     }
   }
-  if (p->overlap) {   // the caller's stream sees every step's outputs
+  if (p->overlap && used_tstream) {   // the caller's stream sees every step's outputs
     FM_CUDA(cudaEventRecord(p->tjoin_ev, p->tstream));
     FM_CUDA(cudaStreamWaitEvent(s, p->tjoin_ev, 0));
   }
@@ -1872,7 +1906,92 @@ int fm_execute(fm_plan* p, const void* img, const uint8_t* img_defined, void* ou
   if (p->counts)
     FM_CUDA(cudaMemsetAsync(out, 0, (size_t)p->batch * p->OH * p->OW * (size_t)(p->lr + 1) * sizeof(int32_t),
                             (cudaStream_t)stream));
-  return run_images(p, img, img_defined, out, valid, (cudaStream_t)stream, 0, p->batch);
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (p->graphable && !p->timing) {
+    // the graph is captured and replayed on the plan's own stream, ordered after the
+    // caller's stream by an event and back (the legacy default stream cannot be captured)
+    if (!p->gstream) {
+      FM_CUDA(cudaStreamCreateWithFlags(&p->gstream, cudaStreamNonBlocking));
+      FM_CUDA(cudaEventCreateWithFlags(&p->gev_in, cudaEventDisableTiming));
+      FM_CUDA(cudaEventCreateWithFlags(&p->gev_out, cudaEventDisableTiming));
+    }
+    cudaStream_t s = p->gstream;
+    FM_CUDA(cudaEventRecord(p->gev_in, cs));
+    FM_CUDA(cudaStreamWaitEvent(s, p->gev_in, 0));
+    const void* key[5] = {img, img_defined, out, valid, nullptr};
+    // Callers that pass new buffers every call (the drop-in API) would force a capture per
+    // call: after the second distinct buffer set the graph runs on plan-owned staging
+    // buffers instead, with device-to-device copies in and out around each replay.
+    const bool match = p->gexec && std::memcmp(key, p->gkey, sizeof(key)) == 0;
+    const size_t in_b = (size_t)p->batch * p->H * p->W * dtype_size(p->d.img_dtype);
+    const size_t def_b = (size_t)p->batch * p->H * p->W;
+    const size_t out_b = (size_t)p->batch * p->OH * p->OW * out_size(p->d.out_dtype);
+    const size_t val_b = (size_t)p->batch * p->OH * p->OW;
+    if (!match && !p->gstaged && ++p->gmiss >= 2) {
+      FM_CUDA(cudaMalloc(&p->g_img, in_b));
+      FM_CUDA(cudaMalloc(&p->g_def, def_b));
+      FM_CUDA(cudaMalloc(&p->g_out, out_b));
+      FM_CUDA(cudaMalloc(&p->g_valid, val_b));
+      p->gstaged = true;
+    }
+    const void* gi = img;
+    const uint8_t* gd = img_defined;
+    void* go = out;
+    uint8_t* gv = valid;
+    if (p->gstaged) {
+      FM_CUDA(cudaMemcpyAsync(p->g_img, img, in_b, cudaMemcpyDeviceToDevice, s));
+      if (img_defined) FM_CUDA(cudaMemcpyAsync(p->g_def, img_defined, def_b, cudaMemcpyDeviceToDevice, s));
+      gi = p->g_img;
+      gd = img_defined ? p->g_def : nullptr;
+      go = p->g_out;
+      gv = valid ? p->g_valid : nullptr;
+      key[0] = gi;
+      key[1] = gd;
+      key[2] = go;
+      key[3] = gv;
+    }
+    if (!p->gexec || std::memcmp(key, p->gkey, sizeof(key)) != 0) {
+      // (re)capture the whole call: memset, range, conv and tonal kernels on s and the
+      // range stream, joined back into s
+      if (p->gexec) {
+        cudaGraphExecDestroy(p->gexec);
+        p->gexec = nullptr;
+      }
+      FM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      p->capturing = true;
+      const long long l0 = g_launches.load();
+      const int rc = run_images(p, gi, gd, go, gv, s, 0, p->batch);
+      p->capturing = false;
+      cudaGraph_t g = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(s, &g);
+      if (rc || ec != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();   // a failed capture leaves its error behind: not this plan's next call's
+        if (rc) return rc;
+        return fail(FM_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+      }
+      const cudaError_t ei = cudaGraphInstantiate(&p->gexec, g, 0);
+      cudaGraphDestroy(g);
+      if (ei != cudaSuccess) {
+        p->gexec = nullptr;
+        return fail(FM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+      }
+      p->graph_kernels = g_launches.load() - l0;
+      g_launches -= p->graph_kernels;   // counted when replayed
+      std::memcpy(p->gkey, key, sizeof(key));
+    }
+    FM_CUDA(cudaGraphLaunch(p->gexec, s));
+    g_launches += p->graph_kernels;
+    if (p->gstaged) {
+      FM_CUDA(cudaMemcpyAsync(out, p->g_out, out_b, cudaMemcpyDeviceToDevice, s));
+      if (valid) FM_CUDA(cudaMemcpyAsync(valid, p->g_valid, val_b, cudaMemcpyDeviceToDevice, s));
+    }
+    FM_CUDA(cudaEventRecord(p->gev_out, s));
+    FM_CUDA(cudaStreamWaitEvent(cs, p->gev_out, 0));
+    p->last_stream = s;
+    return FM_OK;
+  }
+  return run_images(p, img, img_defined, out, valid, cs, 0, p->batch);
 }
 
 int fm_set_timing(fm_plan* p, int enable) {
