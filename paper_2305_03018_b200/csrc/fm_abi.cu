@@ -28,6 +28,7 @@
 #include "fm_tile.cuh"
 #include "fm_tile128.cuh"
 #include "fm_tonal.cuh"
+#include "fm_tonal_coop.cuh"
 
 using namespace fm;
 
@@ -208,6 +209,11 @@ template <int N, bool SM, int NT>
 void launch_tonal(dim3 grid, int nt, size_t smem, cudaStream_t s, const TonalArgs& a) {
   tonal_kernel_t<N, SM, NT><<<grid, NT, smem, s>>>(a);
 }
+// long tonal axes: the cooperative kernel (fm_tonal_coop.cuh), several threads per pixel
+template <int N>
+void launch_tonal_coop(dim3 grid, int nt, size_t smem, cudaStream_t s, const TonalArgs& a) {
+  if constexpr (coop_ok(N)) tonal_kernel_coop<N><<<grid, coop_threads(N), smem, s>>>(a);
+}
 template <int N>
 constexpr bool tonal_sm() { return N > kTonalRegMax; }
 template <int N>
@@ -217,6 +223,9 @@ typedef void (*tonal_pipe_launch_fn)(dim3, int, size_t, cudaStream_t, const Tona
 struct TonalVariant {
   int n, nt, smem;
   tonal_launch_fn fn;
+  // cooperative kernel (coop_ok(n)): threads, dynamic smem, launcher; 32 pixels per CTA
+  int coop_nt, coop_smem;
+  tonal_launch_fn coop_fn;
   cudaError_t (*attr)();
   // pipelined persistent kernel (register variants): threads, dynamic smem, launcher
   int pipe_nt, pipe_smem;
@@ -248,7 +257,7 @@ cudaError_t tonal_attr() {
 #define FM_TV(N)                                                                                             \
   TonalVariant {                                                                                             \
     N, tonal_nt<N>(), tonal_sm<N>() ? 2 * N * tonal_nt<N>() * 8 : 0, &launch_tonal<N, tonal_sm<N>(), tonal_nt<N>()>, \
-        &tonal_attr<N>, tonal_pipe_nt<N>(), tonal_pipe_smem<N>(), &launch_tonal_pipe<N>, &tonal_pipe_attr<N>      \
+        coop_ok(N) ? coop_threads(N) : 0, coop_smem(N), &launch_tonal_coop<N>, &tonal_attr<N>, tonal_pipe_nt<N>(), tonal_pipe_smem<N>(), &launch_tonal_pipe<N>, &tonal_pipe_attr<N>      \
   }
 const TonalVariant kTonal[] = {
     FM_TV(1),  FM_TV(2),  FM_TV(3),  FM_TV(4),  FM_TV(5),   FM_TV(6),   FM_TV(8),   FM_TV(9),   FM_TV(10),
@@ -258,7 +267,7 @@ const TonalVariant kTonal[] = {
     FM_TV(125), FM_TV(128), FM_TV(135), FM_TV(144), FM_TV(150), FM_TV(160)};
 static_assert(sizeof(kTonal) / sizeof(TonalVariant) == kTonalCount, "tonal variant table");
 
-constexpr int kAuxStreams = 3;
+constexpr int kAuxStreams = 7;
 int g_tonal_pipe_occ[kTonalCount];   // CTAs per SM of each pipelined variant (0: not pipelined)
 int g_num_sms = 148;
 const bool g_tonal_nopipe = std::getenv("FM_TONAL_NOPIPE") != nullptr;  // A/B switch for measurements
@@ -288,6 +297,14 @@ const bool g_graph = !(std::getenv("FM_GRAPH") && std::getenv("FM_GRAPH")[0] == 
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
+// FM_TONAL_COOP=0: long tonal axes (40 < N <= 160) by the one-thread-per-pixel kernels (A/B)
+const bool g_tonal_coop = !(std::getenv("FM_TONAL_COOP") && std::getenv("FM_TONAL_COOP")[0] == '0');
+// largest number of 128-pixel items for which the N <= 40 ladder entries of a launch step go in
+// one device-dispatched launch (FM_TONAL_DISP_MAX; 0 = always one pipelined launch per entry)
+const int g_tonal_disp_max = std::getenv("FM_TONAL_DISP_MAX") ? std::atoi(std::getenv("FM_TONAL_DISP_MAX")) : 16384;
+// smallest N served by the cooperative kernel (FM_TONAL_COOP_MIN), conv grid target in CTAs per SM slot
+const int g_tonal_coop_min = std::getenv("FM_TONAL_COOP_MIN") ? std::atoi(std::getenv("FM_TONAL_COOP_MIN")) : 41;
+const int g_conv_waves = std::getenv("FM_CONV_WAVES") ? std::atoi(std::getenv("FM_CONV_WAVES")) : 4;
 const int g_tonal_pipe_max = std::getenv("FM_TONAL_PIPE_MAX") ? std::atoi(std::getenv("FM_TONAL_PIPE_MAX")) : 40;
 
 const TonalVariant* find_tonal(int n) {
@@ -1539,7 +1556,9 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     // Few units (one small image): split every unit's planes into chunks so the
     // conv grid fills the GPU; that needs the per-ladder counts first.  Many
     // units: one CTA per unit (all its planes), launched before the host waits.
-    const int64_t conv_target = (int64_t)g_num_sms * p->conv_occ * 2;
+    // (device-sized small launches: 2 CTAs per slot; host-sized ones, whose units carry many
+    // planes, split finer -- the tail of the last wave is at most one chunk long)
+    const int64_t conv_target = (int64_t)g_num_sms * p->conv_occ * (devdisp(steps[si]) ? 2 : g_conv_waves);
     const bool dyn = !p->big && (int64_t)nu * n < conv_target && p->k_chunk > 1;
     int e0 = -1;
     auto launch_conv = [&](unsigned grid) -> int {
@@ -1783,15 +1802,57 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       }
       ++nlaunch;
     }
+    // few units per ladder entry (one mid-sized image: c3): the register-kernel entries
+    // (N <= 40) go in ONE device-dispatched launch instead of one small launch each
+    int disp_nmax = 0;
+    if (!p->counts && p->fuse_nmax <= 0 && g_tonal_disp_max > 0) {
+      constexpr int kDispNT = 128;
+      const int bpj = (p->npx + kDispNT - 1) / kDispNT;
+      int64_t items = 0;
+      int entries = 0;
+      for (int li = 0; li < L && p->ladder[li] <= kDispatchNMax; ++li) {
+        const int cnt = reinterpret_cast<volatile int*>(p->h_counts[buf])[li];
+        items += (int64_t)cnt * bpj;
+        entries += cnt > 0;
+      }
+      if (entries > 1 && items <= g_tonal_disp_max) {
+        disp_nmax = kDispatchNMax;
+        nlaunch -= entries - 1;
+      }
+    }
     const int nstreams = std::min(nlaunch, 1 + kAuxStreams);
     if (nstreams > 1) {
       FM_CUDA(cudaEventRecord(p->ev_fork, tsm));
       for (int i = 0; i < nstreams - 1; ++i) FM_CUDA(cudaStreamWaitEvent(p->aux[i], p->ev_fork, 0));
     }
     int launch_i = 0;
+    if (disp_nmax > 0) {
+      constexpr int kDispNT = 128;
+      const int bpj = (p->npx + kDispNT - 1) / kDispNT;
+      int64_t items = 0;
+      for (int li = 0; li < L && p->ladder[li] <= disp_nmax; ++li) {
+        const int cnt = reinterpret_cast<volatile int*>(p->h_counts[buf])[li];
+        const int N = p->ladder[li];
+        items += (int64_t)cnt * bpj;
+        planes += (double)cnt * (N + 1);
+        tonal_b += (double)cnt * ((N + 1) * (double)p->npx * (p->chat16 ? 4.0 : 8.0) +
+                                  (double)p->npx * (out_size(p->d.out_dtype) + (valid ? 1.0 : 0.0)));
+      }
+      t.bucket_count = p->bucket_count[buf];
+      t.ladder = p->d_ladder;
+      t.lists = p->bucket_list[buf];
+      t.L = L;
+      t.cap = (int)cap;
+      t.se_count = p->se_count;
+      // the last stream of the round robin: the long entries start first on the others
+      const int si = nstreams - 1;
+      tonal_kernel_dispatch<kDispNT><<<(unsigned)items, kDispNT, 0, si == 0 ? tsm : p->aux[si - 1]>>>(t);
+      g_launches++;
+      FM_CUDA(cudaGetLastError());
+    }
     for (int li = L - 1; li >= 0; --li) {
       const int cnt = reinterpret_cast<volatile int*>(p->h_counts[buf])[li];
-      if (cnt <= 0 || p->ladder[li] <= p->fuse_nmax) continue;
+      if (cnt <= 0 || p->ladder[li] <= p->fuse_nmax || p->ladder[li] <= disp_nmax) continue;
       const int N = p->ladder[li];
       const int si = launch_i++ % nstreams;
       cudaStream_t ts = si == 0 ? tsm : p->aux[si - 1];
@@ -1809,6 +1870,8 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         t.use_tma = p->tmaps.empty() ? 0 : 1;
         t.tma_row0 = p->overlap ? buf * (int)(cap * p->K) : 0;
         tv->pipe_fn(dim3((unsigned)grid), tv->pipe_nt, tv->pipe_smem, ts, t, t.use_tma ? &p->tmaps[2 * li] : kNoMap);
+      } else if (tv && tv->coop_nt > 0 && g_tonal_coop && N >= g_tonal_coop_min) {
+        tv->coop_fn(dim3((unsigned)cnt, (unsigned)((p->npx + kCoopPix - 1) / kCoopPix)), tv->coop_nt, tv->coop_smem, ts, t);
       } else if (tv) {
         const int nt = tv->nt;
         tv->fn(dim3((unsigned)cnt, (unsigned)((p->npx + nt - 1) / nt)), nt, tv->smem, ts, t);

@@ -306,6 +306,37 @@ def test_tile_and_tonal_length_invariance():
         assert np.array_equal(v[0], ref), T
 
 
+COOP_NS = [45, 48, 50, 54, 60, 64, 72, 75, 80, 81, 90, 96, 100, 108, 120, 125, 128, 135, 144, 150, 160]
+
+
+@pytest.mark.parametrize("N", COOP_NS + [40, 162, 180])
+def test_long_tonal_axes_every_ladder_entry(N, monkeypatch):
+    """Every tonal length 2N served by the several-threads-per-pixel kernel
+    (fm_tonal_coop.cuh, 40 < N <= 160) and its neighbours (pipelined register kernel,
+    generic kernel): uniform data whose spread needs exactly that ladder entry (the clamp
+    bound is switched off so no tile gets a shorter one), dilation and erosion, an SE with gaps."""
+    from paper_2305_03018_b200 import workloads as W
+    monkeypatch.setenv("FM_RANGE_TAPS", "0")
+    rng = np.random.default_rng(1000 + N)
+    vmax = 2 * N - 1 - 4
+    img = rng.integers(0, vmax + 1, (1, 131, 157)).astype(np.int32)
+    img[0, 0, 0], img[0, 5, 7], img[0, 100, 120] = 0, vmax, vmax
+    img[0, 70, 80] = 0
+    se = rng.integers(0, 5, (5, 7))
+    se[0, 0], se[4, 6] = 0, 4
+    sd = rng.random((5, 7)) > 0.2
+    sd[0, 0] = sd[4, 6] = sd[2, 3] = True
+    bits = int(vmax).bit_length()
+    w = W.Workload("x", img, se, sd, (-2, -3), vmax, bits)
+    for mode in ("dilate", "erode"):
+        v, valid, dev, plan = _plan_run(w, mode)
+        assert plan.info["tonal_len"] >= 2 * N
+        ref, refv = cnaive.naive(img[0].astype(np.int64), None, se, sd, (-2, -3), erode=(mode == "erode"), crop=True,
+                                 fill=0 if mode == "dilate" else vmax)
+        assert np.array_equal(v[0], ref) and np.array_equal(valid[0].astype(bool), refv), (N, mode)
+        assert dev < 0.25
+
+
 @pytest.mark.parametrize("tile", [16, 32, 64, 128, 256])
 def test_se_value_range_wider_than_short_ladder_entries(tile):
     """8-bit data with an SE whose own value range (up to 230) exceeds the shortest ladder
