@@ -284,6 +284,8 @@ const int g_fuse_kch = std::getenv("FM_FUSE_KCH") ? std::atoi(std::getenv("FM_FU
 const bool g_discard = !(std::getenv("FM_DISCARD") && std::getenv("FM_DISCARD")[0] == '0');
 // FM_DEVDISPATCH=0: small launches also wait on the host for the per-ladder counts (A/B)
 const bool g_devdispatch = !(std::getenv("FM_DEVDISPATCH") && std::getenv("FM_DEVDISPATCH")[0] == '0');
+// FM_BIG_PAIR=0: no Nyquist-plane pairing of neighbouring units on the 256^2 path (A/B)
+const bool g_big_pair = !(std::getenv("FM_BIG_PAIR") && std::getenv("FM_BIG_PAIR")[0] == '0');
 const int g_big_steps = std::getenv("FM_BIG_STEPS") ? std::atoi(std::getenv("FM_BIG_STEPS")) : 1;
 // 256^2 path: L2 budget (MiB) of one unit batch's scratch items (FM_BIG_L2_MB; default 0 = one
 // batch: measured slower at 96 / 48 / 24 MiB, the passes are latency bound, not HBM bound)
@@ -294,6 +296,8 @@ const bool g_chat16 = !(std::getenv("FM_CHAT16") && std::getenv("FM_CHAT16")[0] 
 const bool g_overlap = !(std::getenv("FM_OVERLAP") && std::getenv("FM_OVERLAP")[0] == '0');
 // FM_GRAPH=0: small calls launch their kernels one by one instead of replaying a graph (A/B)
 const bool g_graph = !(std::getenv("FM_GRAPH") && std::getenv("FM_GRAPH")[0] == '0');
+// FM_RANGE_ALIGNED=0: the range kernel stages uint8 windows pixel by pixel (A/B)
+const bool g_range_aligned = !(std::getenv("FM_RANGE_ALIGNED") && std::getenv("FM_RANGE_ALIGNED")[0] == '0');
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
@@ -305,6 +309,9 @@ const int g_tonal_disp_max = std::getenv("FM_TONAL_DISP_MAX") ? std::atoi(std::g
 // smallest N served by the cooperative kernel (FM_TONAL_COOP_MIN), conv grid target in CTAs per SM slot
 const int g_tonal_coop_min = std::getenv("FM_TONAL_COOP_MIN") ? std::atoi(std::getenv("FM_TONAL_COOP_MIN")) : 41;
 const int g_conv_waves = std::getenv("FM_CONV_WAVES") ? std::atoi(std::getenv("FM_CONV_WAVES")) : 4;
+// smallest N served by the pipelined tonal kernel (FM_TONAL_PIPE_MIN; measured at c4, N = 1:
+// the one-thread-per-pixel kernel is slower, 0.065 vs 0.038 ms, so the default keeps every N)
+const int g_tonal_pipe_min = std::getenv("FM_TONAL_PIPE_MIN") ? std::atoi(std::getenv("FM_TONAL_PIPE_MIN")) : 0;
 const int g_tonal_pipe_max = std::getenv("FM_TONAL_PIPE_MAX") ? std::atoi(std::getenv("FM_TONAL_PIPE_MAX")) : 40;
 
 const TonalVariant* find_tonal(int n) {
@@ -1441,11 +1448,19 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     r.splits = S;
     r.skip0 = g_no_skip0 ? 0 : 1;
     r.warp_sync = g_range_sync;
+    // chunk-aligned staging (fm_range.cuh): uint8 rows 16-byte aligned, no mask, 2-D
+    r.aligned = g_range_aligned && p->two_d && p->d.img_dtype == FM_U8 && img_defined == nullptr && p->W % 16 == 0 &&
+                (reinterpret_cast<uintptr_t>(r.img) % 16) == 0;
     size_t rsm = 0;
     if (r.ntaps > 0) {
-      rsm = p->two_d ? (size_t)((p->QY + S - 1) / S + p->my - 1) * p->win_x * 2
+      const size_t stride = r.aligned ? (size_t)((p->win_x + 15) & ~15) + 16 : (size_t)p->win_x;
+      rsm = p->two_d ? (size_t)((p->QY + S - 1) / S + p->my - 1) * stride * 2
                      : (size_t)((p->unit_step_x + S - 1) / S + p->mx - 1) * 2;
       rsm = (rsm + 15) & ~(size_t)15;
+      if (rsm > (size_t)kRangeSmemMax) {   // (the plan sized the window for the plain stride)
+        r.aligned = 0;
+        rsm = ((size_t)((p->QY + S - 1) / S + p->my - 1) * p->win_x * 2 + 15) & ~(size_t)15;
+      }
     }
     r.part = p->range_part[buf];
     r.ladder = p->d_ladder;
@@ -1605,6 +1620,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       b.chat = p->chat;
       b.wpx = p->wpx;
       b.err = p->stats + 1;
+      b.pair = g_big_pair ? 1 : 0;
       const unsigned inv_blocks = (unsigned)((kBig - (p->my - 1) + kBigRows - 1) / kBigRows);
       // units in batches whose 256^2 scratch items (written and re-read by the three
       // kernels) fit in L2, so the passes read back from L2 instead of HBM
@@ -1862,7 +1878,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       t.list = p->bucket_list[buf] + (size_t)li * cap;
       const TonalVariant* tv = p->counts ? nullptr : p->ladder_var[li];
       const int occ = tv ? g_tonal_pipe_occ[tv - kTonal] : 0;
-      if (tv && occ > 0 && !g_tonal_nopipe && N <= g_tonal_pipe_max) {
+      if (tv && occ > 0 && !g_tonal_nopipe && N <= g_tonal_pipe_max && N >= g_tonal_pipe_min) {
         t.njobs = cnt;
         const int64_t items = (int64_t)cnt * ((p->npx + tv->pipe_nt - 1) / tv->pipe_nt);
         const int grid = (int)std::min<int64_t>(items, (int64_t)g_num_sms * std::min(occ, g_tonal_occ_cap));

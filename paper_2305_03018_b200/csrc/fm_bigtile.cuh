@@ -46,7 +46,24 @@ struct BigArgs {
   float2* chat;               // [imgs][units][K_max][wpx]
   int wpx;
   int* err;
+  int pair;                   // Nyquist planes of neighbouring units share one complex transform
 };
+
+// Nyquist-plane pairing.  Plane k = N of a unit (T = 2N) is REAL: w_T^{N v} = (-1)^v, and so is
+// the SE's plane N.  Two launch-local neighbours (lu even, lu + 1) with the same tonal length
+// therefore share ONE complex transform: z = a_lu + i a_{lu+1}, and z (*) h = a_lu (*) h +
+// i a_{lu+1} (*) h splits into real and imaginary part because h is real.  The even unit's
+// CTAs carry the pair, the odd unit's exit.  (c4: nearly every unit has N = 1 and, being
+// "full", only that plane -- the three kernels do half the work.)
+// returns 0: not paired, 1: carries the pair (partner = lu + 1), 2: carried by lu - 1 (exit)
+__device__ __forceinline__ int big_pair_role(const BigArgs& a, int img, int lu, int k, const int4& up, int4& upp) {
+  if (!a.pair || k != up.y) return 0;
+  const int lup = lu ^ 1;
+  if (lup >= a.nu) return 0;
+  upp = a.unit_param[(size_t)img * a.units + a.unit0 + lup];
+  if (upp.y != up.y) return 0;
+  return (lu & 1) ? 2 : 1;
+}
 
 // ------------------------------------------------------------------ rows (x axis)
 // CTA = 32 rows x 256 columns of one (image, tile, plane); 8 warps, 4 rows each.
@@ -59,19 +76,29 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
   uint16_t* tv = reinterpret_cast<uint16_t*>(smem_raw + kBigRows * RS * 8);
   const uint32_t* tv32 = reinterpret_cast<const uint32_t*>(tv);
   float4* twx = reinterpret_cast<float4*>(smem_raw + kBigRows * RS * 8 + kBigRows * PX * 2);
+  uint16_t* tv2 = reinterpret_cast<uint16_t*>(smem_raw + kBigRows * RS * 8 + kBigRows * PX * 2 + (kBigR / 2) * (kBigR + 1) * 16);
+  const uint32_t* tv2_32 = reinterpret_cast<const uint32_t*>(tv2);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = blockIdx.y;
   const int lu = SPEC ? 0 : a.lu0 + (int)(blockIdx.z % a.nub);
   const int unit = SPEC ? 0 : a.unit0 + lu;
   const int img = SPEC ? 0 : (int)(blockIdx.z / a.nub);
-  int T = a.T, K = a.K, enc_bias = a.enc_bias;
+  int T = a.T, K = a.K, enc_bias = a.enc_bias, enc_bias2 = 0;
+  bool paired = false;
   if constexpr (!SPEC) {
     const int4 up = a.unit_param[(size_t)img * a.units + unit];
     K = up.y + 1;
     T = 2 * up.y;
     enc_bias = a.enc_sign > 0 ? -up.x : up.x;
     if (k == 0 && (up.w & 2)) return;   // plane 0 of a full unit: the tonal pass knows it
+    if (k < K) {
+      int4 upp;
+      const int role = big_pair_role(a, img, lu, k, up, upp);
+      if (role == 2) return;
+      paired = role == 1;
+      enc_bias2 = a.enc_sign > 0 ? -upp.x : upp.x;
+    }
   }
   if (k >= K) return;
   const int row0 = FWD ? blockIdx.x * kBigRows : (a.my - 1) + blockIdx.x * kBigRows;
@@ -110,34 +137,77 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
       // conversions: the image reads overlap instead of paying one latency each
       constexpr int IT = kBigRows * PX / kBigNT, GB = 16;
       static_assert(IT % GB == 0, "staging split");
+      auto stage_unit = [&](int uty, int utx, int bias, uint16_t* tvd) {
+        if (a.img_dtype == 0 && a.img_def == nullptr) {
+          // uint8 images without a mask: 16-byte loads of the aligned chunks that cover each
+          // row part inside the image (one load per 16 pixels instead of one per pixel)
+          const int ixb = utx * a.QX + a.DX;              // image column of tile column 0
+          const int xs = max(ixb, 0), xe = min(ixb + PX, a.W);
+          for (int i = tid; i < kBigRows * PX / 2; i += kBigNT)
+            reinterpret_cast<uint32_t*>(tvd)[i] = (uint32_t)kSent | ((uint32_t)kSent << 16);
+          __syncthreads();
+          if (xs < xe) {
+            const uint8_t* base = reinterpret_cast<const uint8_t*>(a.img);
+            constexpr int CPR = PX / 16 + 1;               // chunks covering 256 columns at any alignment
 #pragma unroll 1
-      for (int g0 = 0; g0 < IT; g0 += GB) {
-        int raw[GB];
-        bool ok[GB];
+            for (int it = tid; it < kBigRows * CPR; it += kBigNT) {
+              const int r = it / CPR, ch = it - r * CPR;
+              const int iy = uty * a.QY + a.DY + row0 + r;
+              if (iy < 0 || iy >= a.H) continue;
+              const uint8_t* rowp = base + ((int64_t)img * a.H + iy) * a.W;
+              const uintptr_t first = reinterpret_cast<uintptr_t>(rowp + xs) & ~(uintptr_t)15;
+              const uintptr_t cb = first + 16u * (uintptr_t)ch;
+              if (cb >= reinterpret_cast<uintptr_t>(rowp + xe)) continue;
+              const uint4 wv = __ldg(reinterpret_cast<const uint4*>(cb));
+              const int xc0 = (int)(reinterpret_cast<const uint8_t*>(cb) - rowp);
+              const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-        for (int u = 0; u < GB; ++u) {
-          const int p = tid + (g0 + u) * kBigNT;
-          const int py = row0 + p / PX, px = p % PX;
-          const int iy = ty * a.QY + a.DY + py, ix = tx * a.QX + a.DX + px;
-          ok[u] = iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
-          raw[u] = 0;
-          if (ok[u]) {
-            const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
-            raw[u] = load_img(a.img, a.img_dtype, gi);
-            if (a.img_def != nullptr) ok[u] = a.img_def[gi] != 0;
+              for (int e = 0; e < 16; ++e) {
+                const int x = xc0 + e;
+                if (x < xs || x >= xe) continue;
+                const int f = (int)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
+                const int v = max(a.enc_sign * f + bias, 0);
+                if (v >= T) bad = 1;
+                else tvd[r * PX + (x - ixb)] = (uint16_t)v;
+              }
+            }
+          }
+          return;
+        }
+#pragma unroll 1
+        for (int g0 = 0; g0 < IT; g0 += GB) {
+          int raw[GB];
+          bool ok[GB];
+#pragma unroll
+          for (int u = 0; u < GB; ++u) {
+            const int p = tid + (g0 + u) * kBigNT;
+            const int py = row0 + p / PX, px = p % PX;
+            const int iy = uty * a.QY + a.DY + py, ix = utx * a.QX + a.DX + px;
+            ok[u] = iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+            raw[u] = 0;
+            if (ok[u]) {
+              const int64_t gi = ((int64_t)img * a.H + iy) * a.W + ix;
+              raw[u] = load_img(a.img, a.img_dtype, gi);
+              if (a.img_def != nullptr) ok[u] = a.img_def[gi] != 0;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < GB; ++u) {
+            uint16_t t = kSent;
+            if (ok[u]) {
+              // values below the unit's clamp level encode as the clamp (fm_range.cuh)
+              const int v = max(a.enc_sign * raw[u] + bias, 0);
+              if (v >= T) bad = 1;
+              else t = (uint16_t)v;
+            }
+            tvd[tid + (g0 + u) * kBigNT] = t;
           }
         }
-#pragma unroll
-        for (int u = 0; u < GB; ++u) {
-          uint16_t t = kSent;
-          if (ok[u]) {
-            // values below the unit's clamp level encode as the clamp (fm_range.cuh)
-            const int v = max(a.enc_sign * raw[u] + enc_bias, 0);
-            if (v >= T) bad = 1;
-            else t = (uint16_t)v;
-          }
-          tv[tid + (g0 + u) * kBigNT] = t;
-        }
+      };
+      stage_unit(ty, tx, enc_bias, tv);
+      if (paired) {
+        const int u2 = unit + 1, ty2 = u2 / max(a.tiles_x, 1);
+        stage_unit(ty2, u2 - ty2 * max(a.tiles_x, 1), enc_bias2, tv2);
       }
     }
     if (!SPEC && bad) atomicOr(a.err, 1);
@@ -158,11 +228,22 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
     {
       const int y = warp * RPW + lane % RPW, n2 = 2 * (lane / RPW);
       float2 wa[R1], wb[R1];
+      if (!SPEC && paired) {
+        // Nyquist plane of two units: (-1)^v of this unit + i (-1)^v of its neighbour
+        auto nyq = [](uint32_t t) -> float { return t == kSent ? 0.f : ((t & 1u) ? -1.f : 1.f); };
 #pragma unroll
-      for (int n1 = 0; n1 < R1; ++n1) {
-        const uint32_t tt = tv32[(y * PX + n2 + R2 * n1) / 2];
-        wa[n1] = enc(tt & 0xFFFFu);
-        wb[n1] = enc(tt >> 16);
+        for (int n1 = 0; n1 < R1; ++n1) {
+          const uint32_t tt = tv32[(y * PX + n2 + R2 * n1) / 2], t2 = tv2_32[(y * PX + n2 + R2 * n1) / 2];
+          wa[n1] = make_float2(nyq(tt & 0xFFFFu), nyq(t2 & 0xFFFFu));
+          wb[n1] = make_float2(nyq(tt >> 16), nyq(t2 >> 16));
+        }
+      } else {
+#pragma unroll
+        for (int n1 = 0; n1 < R1; ++n1) {
+          const uint32_t tt = tv32[(y * PX + n2 + R2 * n1) / 2];
+          wa[n1] = enc(tt & 0xFFFFu);
+          wb[n1] = enc(tt >> 16);
+        }
       }
       dft<R1, false>(wa);
       dft<R1, false>(wb);
@@ -255,7 +336,15 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
       const int row = row0 + y;
       if (y >= nrows) continue;
       const int oy = ty * a.QY + row - (a.my - 1), ox = tx * a.QX + c;
-      if (oy < a.OH && ox < a.OW) dst[(size_t)(row - (a.my - 1)) * a.QX + c] = buf[y * RS + (a.mx - 1) + c];
+      const float2 v = buf[y * RS + (a.mx - 1) + c];
+      if (oy < a.OH && ox < a.OW) dst[(size_t)(row - (a.my - 1)) * a.QX + c] = paired ? make_float2(v.x, 0.f) : v;
+      if (paired) {
+        // the neighbour's plane is the imaginary part; its own tile position bounds the store
+        const int u2 = unit + 1, ty2 = u2 / max(a.tiles_x, 1), tx2 = u2 - ty2 * max(a.tiles_x, 1);
+        const int oy2 = ty2 * a.QY + row - (a.my - 1), ox2 = tx2 * a.QX + c;
+        if (oy2 < a.OH && ox2 < a.OW)
+          (dst + (size_t)a.K_max * (size_t)a.wpx)[(size_t)(row - (a.my - 1)) * a.QX + c] = make_float2(v.y, 0.f);
+      }
     }
   }
 }
@@ -282,6 +371,10 @@ __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a
     const int4 up = a.unit_param[(size_t)img * a.units + unit];
     K = up.y + 1;
     if (k >= K || (k == 0 && (up.w & 2))) return;   // past the unit's planes / known plane 0
+    {
+      int4 upp;
+      if (big_pair_role(a, img, lu, k, up, upp) == 2) return;   // carried by the neighbour's CTAs
+    }
     spec_plane = a.spec + a.spec_off[up.z] + ((size_t)k * (kBig / kBigCols) + cb) * (SQ * kBigColsNT);
     // the product's spectrum chunk streams in while the forward passes run
 #pragma unroll
@@ -389,7 +482,7 @@ __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a
   }
 }
 
-constexpr int kBigRowsSmem = kBigRows * (kBig + 2) * 8 + kBigRows * kBig * 2 + (kBigR / 2) * (kBigR + 1) * 16;
+constexpr int kBigRowsSmem = kBigRows * (kBig + 2) * 8 + 2 * kBigRows * kBig * 2 + (kBigR / 2) * (kBigR + 1) * 16;
 constexpr int kBigColsSmem = kBig * (kBigCols + 2) * 8 + kBigR * kBigColsNT * 16;
 
 }  // namespace fm

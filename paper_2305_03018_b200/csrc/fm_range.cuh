@@ -60,6 +60,7 @@ struct RangeArgs {
   int skip0;              // the conv path may skip plane 0 of "full" units
   int warp_sync;          // bound taps walked warp-synchronously (else per-lane pixel queues)
   int ntaps;              // 0: no clamp; else a multiple of 8 (padded with kTapPadB taps)
+  int aligned;            // uint8 image rows 16-byte aligned (2-D, no mask): chunk-aligned staging
   const int* ladder;      // ascending N values
   int L;
   int4* unit_param;       // [imgs][units]
@@ -117,7 +118,7 @@ __device__ __forceinline__ void unit_finish(const RangeArgs& a, int img, int uni
 // input rows those outputs read.
 template <int DT>
 __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
-  extern __shared__ int16_t swin[];
+  extern __shared__ __align__(16) int16_t swin[];
   __shared__ int red[4][kRangeNT / 32];
   __shared__ int s_lo, s_hi, s_key, s_bound, s_last;
   __shared__ __align__(16) int s_toff[kMaxBoundTaps], s_tb[kMaxBoundTaps];
@@ -158,13 +159,71 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
 
   // ---- stage the window part (int16), min / max of v and the position of the minimum
   int lo = INT32_MAX, hi = INT32_MIN, bad = 0, key = INT32_MAX;
+  const int xb = x0 + wx0;  // image column of window column 0
+  // chunk-aligned staging (uint8, rows 16-byte aligned, no mask): staged column 0 is the
+  // 16-aligned image column xa <= xb, the row stride ws a multiple of 16 -- every aligned
+  // 16-pixel chunk of the image lands as two aligned 16-byte shared-memory stores
+  const bool fast = DT == 0 && a.aligned && a.img_def == nullptr;
+  const int xa = fast ? (xb & ~15) : xb, sh = xb - xa;
+  const int ws = fast ? ((wx + 15) & ~15) + 16 : wx;
   for (int i = tid; i < a.ntaps; i += kRangeNT) {
-    s_toff[i] = a.taps[i].x;
+    // host offsets index a window of row stride win_x (= wx in 2-D)
+    const int off = a.taps[i].x;
+    s_toff[i] = fast ? (off / wx) * ws + (off - (off / wx) * wx) : off;
     s_tb[i] = a.taps[i].y;
   }
   for (int i = tid; i < a.L && i < 64; i += kRangeNT) s_lad[i] = a.ladder[i];
-  const int xb = x0 + wx0;  // image column of staged column 0
-  if (a.img_def == nullptr) {
+  if (fast) {
+    const int cpr = ws >> 4, total = wy * cpr;
+    const float inv_cpr = 1.0f / (float)cpr;
+    const uint8_t* img8 = reinterpret_cast<const uint8_t*>(a.img) + (int64_t)img * a.H * a.W;
+#pragma unroll 2
+    for (int it = tid; it < total; it += kRangeNT) {
+      const int r = (int)(((float)it + 0.5f) * inv_cpr);
+      const int ch = it - r * cpr;
+      const int iy = y0 + wy0 + r, xc = xa + 16 * ch;   // W % 16 == 0: a chunk is inside or outside as a whole
+      uint32_t pk[8];
+      if (iy < 0 || iy >= a.H || xc < 0 || xc >= a.W) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pk[i] = 0x80008000u;
+      } else {
+        const uint4 wv = __ldg(reinterpret_cast<const uint4*>(img8 + (int64_t)iy * a.W + xc));
+        const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
+        int v[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = a.enc_sign * (int)__byte_perm(wd[e >> 2], 0, 0x4440 + (e & 3)) + a.enc_bias;
+        const int c0 = 16 * ch - sh;   // window column of the chunk's first pixel
+        int m = INT32_MAX, M = INT32_MIN;
+        if (c0 >= 0 && c0 + 16 <= wx) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            m = min(m, v[e]);
+            M = max(M, v[e]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (c0 + e >= 0 && c0 + e < wx) {
+              m = min(m, v[e]);
+              M = max(M, v[e]);
+            }
+        }
+        if (m <= M) {
+          lo = min(lo, m);
+          hi = max(hi, M);
+          key = min(key, (min(max(m, 0), 32767) << 16) | ((r * wx + max(c0, 0)) & 0xFFFF));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pk[i] = __byte_perm((uint32_t)v[2 * i], (uint32_t)v[2 * i + 1], 0x5410);
+      }
+      if (stage) {
+        uint4* dst = reinterpret_cast<uint4*>(swin + r * ws + 16 * ch);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+    }
+    bad = lo <= hi && (lo < 0 || hi > a.vmax);
+  } else if (a.img_def == nullptr) {
     // 16-byte vector loads of aligned chunks covering each staged row part;
     // the window is first filled with "undefined" so that only in-image
     // columns need writing
@@ -285,7 +344,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
       const int sy = (warp & 1) ? 3 : -3, sx = (warp & 2) ? 3 : -3, sc = warp >> 2;
       const int jy = min(max(zr - a.cy + sy * sc, 0), jy_end - 1 - oy0);
       const int jx = min(max(zc - a.cx + sx * sc, 0), jx_end - 1 - (a.two_d ? 0 : wx0));
-      const int base = jy * wx + jx;
+      const int base = jy * ws + jx + sh;
       int g = INT32_MIN;
       for (int t = lane; t < a.ntaps; t += 32) g = max(g, (int)swin[base + s_toff[t]] + s_tb[t]);
 #pragma unroll
@@ -311,7 +370,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
     const uint32_t cmagic = cols > 1 ? (uint32_t)((0x100000000ull + cols - 1) / (uint64_t)cols) : 0u;
     auto base_of = [&](int q) {
       const int jy = cmagic ? (int)__umulhi((uint32_t)q, cmagic) : q;
-      return jy * wx + (q - jy * cols) + xoff;
+      return jy * ws + (q - jy * cols) + xoff + sh;
     };
     // A pixel may stop as soon as g reaches the breakpoint level below the
     // running minimum: only the interval between ladder breakpoints that D
