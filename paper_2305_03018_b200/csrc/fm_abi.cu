@@ -1688,7 +1688,9 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       const int64_t blocks = (int64_t)nu * n * ((p->npx + kDispNT - 1) / kDispNT);
       int e1 = -1;
       if (p->timing) { e1 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
-      tonal_kernel_dispatch<kDispNT><<<(unsigned)blocks, kDispNT, 0, s>>>(t);
+      if (p->N <= 10) tonal_kernel_dispatch<kDispNT, 10><<<(unsigned)blocks, kDispNT, 0, s>>>(t);
+      else if (p->N <= 16) tonal_kernel_dispatch<kDispNT, 16><<<(unsigned)blocks, kDispNT, 0, s>>>(t);
+      else tonal_kernel_dispatch<kDispNT, kDispatchNMax><<<(unsigned)blocks, kDispNT, 0, s>>>(t);
       g_launches++;
       FM_CUDA(cudaGetLastError());
       if (p->timing) {
@@ -1862,7 +1864,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       t.se_count = p->se_count;
       // the last stream of the round robin: the long entries start first on the others
       const int si = nstreams - 1;
-      tonal_kernel_dispatch<kDispNT><<<(unsigned)items, kDispNT, 0, si == 0 ? tsm : p->aux[si - 1]>>>(t);
+      tonal_kernel_dispatch<kDispNT, kDispatchNMax><<<(unsigned)items, kDispNT, 0, si == 0 ? tsm : p->aux[si - 1]>>>(t);
       g_launches++;
       FM_CUDA(cudaGetLastError());
     }

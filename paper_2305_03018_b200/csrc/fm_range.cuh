@@ -80,7 +80,7 @@ __device__ __forceinline__ int range_ld(const void* img, int64_t i) {
   return __ldg(reinterpret_cast<const int32_t*>(img) + i);
 }
 
-__device__ __forceinline__ void unit_finish(const RangeArgs& a, int img, int unit, int lo, int hi, int bound) {
+__device__ __forceinline__ void unit_finish(const RangeArgs& a, const int* lad, int img, int unit, int lo, int hi, int bound) {
   const bool any = lo <= hi;
   int c = any ? lo : 0;
   // bound: INT32_MAX = not computed, INT32_MIN = unknown (no clamp)
@@ -89,7 +89,7 @@ __device__ __forceinline__ void unit_finish(const RangeArgs& a, int img, int uni
   const int lr = any ? (hi - c) + a.lr_se : a.lr_se;
   int li = a.L - 1;
   for (int i = 0; i < a.L; ++i)
-    if (2 * a.ladder[i] >= lr + 1) {
+    if (2 * lad[i] >= lr + 1) {
       li = i;
       break;
     }
@@ -108,7 +108,7 @@ __device__ __forceinline__ void unit_finish(const RangeArgs& a, int img, int uni
       full = x0 >= 0 && x0 + a.win_x <= a.W;
     }
   }
-  a.unit_param[(size_t)img * a.units + unit] = make_int4(anchor, a.ladder[li], li, (any ? 1 : 0) | (full ? 2 : 0));
+  a.unit_param[(size_t)img * a.units + unit] = make_int4(anchor, lad[li], li, (any ? 1 : 0) | (full ? 2 : 0));
   const int slot = atomicAdd(&a.bucket_count[li], 1);
   a.bucket_list[(size_t)li * a.cap + slot] = make_int2(img, unit | (full ? kJobFull : 0));
 }
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
   }
 
   if (S == 1) {
-    if (tid == 0) unit_finish(a, img, unit, lo, hi, bound);
+    if (tid == 0) unit_finish(a, a.L <= 64 ? s_lad : a.ladder, img, unit, lo, hi, bound);
     return;
   }
   // ---- combine the splits: the last CTA to arrive finishes the unit
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
     const int ghi = atomicExch(pr + 1, INT32_MIN);
     const int gb = atomicExch(pr + 2, INT32_MAX);
     atomicExch(pr + 3, 0);
-    unit_finish(a, img, unit, glo, ghi, gb);
+    unit_finish(a, a.L <= 64 ? s_lad : a.ladder, img, unit, glo, ghi, gb);
   }
 }
 

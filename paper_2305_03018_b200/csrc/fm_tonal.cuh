@@ -377,21 +377,24 @@ __device__ __forceinline__ void tonal_pixel_reg(const TonalArgs& a, const TonalP
   if (a.valid) a.valid[pp.dst] = top >= 0 ? 1 : 0;
 }
 
-template <int I = 0>
+template <int NMAX, int I = 0>
 __device__ __forceinline__ void tonal_pixel_dispatch(int n, const TonalArgs& a, const TonalPix& pp, float& dev) {
   if constexpr (I < kTonalCount) {
     constexpr int NI = tonal_ns_at(I);
-    if constexpr (NI <= kDispatchNMax) {
+    if constexpr (NI <= NMAX) {
       if (n == NI) {
         tonal_pixel_reg<NI>(a, pp, dev);
         return;
       }
-      tonal_pixel_dispatch<I + 1>(n, a, pp, dev);
+      tonal_pixel_dispatch<NMAX, I + 1>(n, a, pp, dev);
     }
   }
 }
 
-template <int NT>
+// NMAX: the longest tonal axis the instance serves (the plan's, rounded up to 10 / 16 / 40): the
+// register count is that of the longest compile-time FFT in the switch, so plans with short
+// tonal axes (c1: N <= 10, c2: N <= 16) get twice the resident CTAs of the N <= 40 instance
+template <int NT, int NMAX>
 __global__ void __launch_bounds__(NT) tonal_kernel_dispatch(const TonalArgs a) {
   __shared__ int s_li, s_rem;
   const int bpj = (a.npx + NT - 1) / NT;
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(NT) tonal_kernel_dispatch(const TonalArgs a) {
   const int j = s_rem / bpj, blk = s_rem - (s_rem / bpj) * bpj;
   const TonalPix pp = tonal_pixel_job(a, a.lists[(size_t)li * a.cap + j], blk * NT + threadIdx.x);
   float dev = 0.f;
-  if (pp.live) tonal_pixel_dispatch(a.ladder[li], a, pp, dev);
+  if (pp.live) tonal_pixel_dispatch<NMAX>(a.ladder[li], a, pp, dev);
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
   if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
