@@ -66,16 +66,19 @@ __device__ __forceinline__ float2 (&stock_result(float2 (&v)[M], float2 (&w)[M])
   else return w;
 }
 
+constexpr int kCoopGMax = 5;
+
+// One CTA's work: 32 pixels (block `blk`) of the unit `job`; threads with g >= G (none in the
+// per-entry launches) would only join the barriers.
 template <int N>
-__global__ void __launch_bounds__(coop_threads(N)) tonal_kernel_coop(const TonalArgs a) {
+__device__ __forceinline__ void coop_body(const TonalArgs& a, float x0_full, int2 job, int blk, float2* csm, int (*s_top)[kCoopPix]) {
   constexpr CoopSplit sp = coop_split(N);
   constexpr int N1 = sp.n1, N2 = sp.n2, G = sp.g, PIX = kCoopPix;
-  static_assert(N1 * N2 == N && N1 % G == 0 && N2 % G == 0, "split");
+  static_assert(N1 * N2 == N && N1 % G == 0 && N2 % G == 0 && G <= kCoopGMax, "split");
   constexpr int off = tonal_off(N);
-  extern __shared__ __align__(16) float2 csm[];   // S[N][PIX]
-  __shared__ int s_top[G][PIX];
   const int pix = threadIdx.x & (PIX - 1), g = threadIdx.x / PIX;
-  const TonalPix pp = tonal_pixel(a, blockIdx.y * PIX + pix);
+  const bool act = g < G;
+  const TonalPix pp = tonal_pixel_job(a, job, blk * PIX + pix);
   float2* S = csm + pix;
   const float invq = a.chat_invq_T / (float)(2 * N);
 
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(coop_threads(N)) tonal_kernel_coop(const Tonal
   // Z[k] = s + i m, Z[N-k] = s^* + i m^* with s = X[k] + X[N-k]^*, m = w_k (X[k] - X[N-k]^*),
   // w_k = exp(2 pi i k / 2N)  (tonal_kernel_pipe's packing; k = 0 and k = N/2 are the same
   // formula, their second value is absent / identical)
-  {
+  if (act) {
     const size_t plane = a.wpx;
     const unsigned int* src4 = reinterpret_cast<const unsigned int*>(a.chat) + pp.src;
     const float2* src8 = a.chat + pp.src;
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(coop_threads(N)) tonal_kernel_coop(const Tonal
           xm[u] = __ldcs(src8 + (size_t)(N - k) * plane);
         }
       }
-      if (j0 == 0 && pp.full && pp.live) xk[0] = make_float2(a.x0_full, 0.f);
+      if (j0 == 0 && pp.full && pp.live) xk[0] = make_float2(x0_full, 0.f);
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
         const int k = j0 + G * u;
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(coop_threads(N)) tonal_kernel_coop(const Tonal
   __syncthreads();
   // ---- pass 1: length-N1 transforms over a (stride N2), twiddle W_N^{b c}, in place
 #pragma unroll 1
-  for (int b = g; b < N2; b += G) {
+  for (int b = act ? g : N2; b < N2; b += G) {
     float2 v[N1], w[N1];
 #pragma unroll
     for (int i = 0; i < N1; ++i) v[i] = S[(N2 * i + b) * PIX];
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(coop_threads(N)) tonal_kernel_coop(const Tonal
   float dev = 0.f;
   int top = -1;
 #pragma unroll 1
-  for (int c = g; c < N1; c += G) {
+  for (int c = act ? g : N1; c < N1; c += G) {
     float2 v[N2], w[N2];
 #pragma unroll
     for (int i = 0; i < N2; ++i) v[i] = S[(N2 * c + i) * PIX];
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(coop_threads(N)) tonal_kernel_coop(const Tonal
       top = max(top, t);
     }
   }
-  s_top[g][pix] = top;
+  if (act) s_top[g][pix] = top;
   __syncthreads();
   if (g == 0 && pp.live) {
 #pragma unroll
@@ -175,6 +178,14 @@ __global__ void __launch_bounds__(coop_threads(N)) tonal_kernel_coop(const Tonal
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
   if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+}
+
+// one launch per ladder entry: grid (units of the entry, 32-pixel blocks)
+template <int N>
+__global__ void __launch_bounds__(coop_threads(N)) tonal_kernel_coop(const TonalArgs a) {
+  extern __shared__ __align__(16) float2 csm[];   // S[N][PIX]
+  __shared__ int s_top[kCoopGMax][kCoopPix];
+  coop_body<N>(a, a.x0_full, a.list[blockIdx.x], (int)blockIdx.y, csm, s_top);
 }
 
 }  // namespace fm

@@ -337,6 +337,34 @@ def test_long_tonal_axes_every_ladder_entry(N, monkeypatch):
         assert dev < 0.25
 
 
+def test_long_tonal_axes_mixed_entries_one_launch(monkeypatch):
+    """Tiles of one image with very different spreads: many ladder entries of the
+    several-threads-per-pixel kernel in flight at once (one launch each, side by side on the
+    tonal streams) beside the device-dispatched launch of the short entries."""
+    from paper_2305_03018_b200 import workloads as W
+    monkeypatch.setenv("FM_RANGE_TAPS", "0")
+    rng = np.random.default_rng(77)
+    H = Wd = 520
+    img = np.zeros((1, H, Wd), np.int32)
+    spreads = [20, 60, 88, 100, 118, 140, 160, 200, 236, 250, 280, 300]
+    k = 0
+    for by in range(0, H, 130):
+        for bx in range(0, Wd, 130):
+            sp = spreads[k % len(spreads)]
+            k += 1
+            img[0, by:by + 130, bx:bx + 130] = rng.integers(0, sp + 1, (min(130, H - by), min(130, Wd - bx)))
+    se = rng.integers(0, 4, (9, 9))
+    se[0, 0], se[8, 8] = 0, 3
+    w = W.Workload("x", img, se, np.ones((9, 9), bool), (-4, -4), 300, 9)
+    for mode in ("dilate", "erode"):
+        v, valid, dev, plan = _plan_run(w, mode, tile=128)
+        assert plan.info["tile_x"] == 128
+        ref, refv = cnaive.naive(img[0], None, se, None, (-4, -4), erode=(mode == "erode"), crop=True,
+                                 fill=0 if mode == "dilate" else 300)
+        assert np.array_equal(v[0], ref) and np.array_equal(valid[0].astype(bool), refv), mode
+        assert dev < 0.25
+
+
 @pytest.mark.parametrize("tile", [16, 32, 64, 128, 256])
 def test_se_value_range_wider_than_short_ladder_entries(tile):
     """8-bit data with an SE whose own value range (up to 230) exceeds the shortest ladder
