@@ -189,3 +189,13 @@ def test_bench_orchestration_gloo():
     res = sorted(q.get(timeout=10) for _ in range(world))
     for rank, ms, ok, n in res:
         assert ms == 10.0 + world - 1 and ok == 0 and n == 64
+
+
+def test_reference_arm_is_time_bounded():
+    """bench.py --impl reference: a driver-sized run (--steps 20) must not take steps x 17 s of
+    host time; steps past the budget are skipped and the line says how many ran."""
+    import bench
+    res = bench.cpu_reference(steps=5, warmup=0, config="c1", budget_s=0.0)
+    assert len(res["steps_s"]) == 1 and res["value"] > 0
+    res = bench.cpu_reference(steps=3, warmup=1, config="c1", budget_s=600.0)
+    assert len(res["steps_s"]) == 3 and res["kind"] == "port"
