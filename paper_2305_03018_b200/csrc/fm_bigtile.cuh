@@ -4,9 +4,13 @@
 // convolution of a (tile, plane) is split into three kernels that stream the
 // tile through an HBM scratch S[item][256][256] (item = image, tile, plane):
 //   big_rows_fwd  : encode w_T^{k v} + forward x FFT (radix 16x16) of 32 rows
-//   big_cols      : forward y FFT of 32 columns, product with the SE spectrum,
+//   big_cols      : forward y FFT of 16 columns, product with the SE spectrum,
 //                   inverse y FFT; rows of the valid window written back
 //   big_rows_inv  : inverse x FFT of 32 valid rows, valid columns -> Chat
+// Every thread owns ONE 16-point transform per pass (512 / 256 threads per CTA, <= 64 / 80
+// registers): twice the resident warps of the earlier two-items-per-thread kernels, which
+// ran at IPC ~1.4 per SM.  Row kernels keep a row as [k1][17] (17-stride: both passes'
+// 64-bit accesses are conflict-free).
 // With a 101-wide SE the valid window grows from 28^2 (128 tile) to 156^2, so
 // the FFT work per output pixel drops ~5x for about 1.8 MB of HBM traffic per
 // (tile, plane).  The SE spectrum is computed by the same kernels (SPEC mode)
@@ -21,8 +25,9 @@ constexpr int kBig = 256;        // tile edge
 constexpr int kBigR = 16;        // 256 = 16 x 16 per axis
 constexpr int kBigRows = 32;     // rows per row-kernel CTA
 constexpr int kBigCols = 16;     // columns per column-kernel CTA
-constexpr int kBigNT = 256;      // row kernels
-constexpr int kBigColsNT = 128;  // column kernel: one y item per thread
+constexpr int kBigNT = 512;      // row kernels: one 16-point item per thread and pass
+constexpr int kBigColsNT = 256;  // column kernel: one 16-point item per thread and pass
+constexpr int kBigRS = kBigR * (kBigR + 1);   // row kernels: row stride of the [k1][17] layout (float2)
 
 struct BigArgs {
   // image batch (CONV) or SE (SPEC)
@@ -66,18 +71,18 @@ __device__ __forceinline__ int big_pair_role(const BigArgs& a, int img, int lu, 
 }
 
 // ------------------------------------------------------------------ rows (x axis)
-// CTA = 32 rows x 256 columns of one (image, tile, plane); 8 warps, 4 rows each.
+// CTA = 32 rows x 256 columns of one (image, tile, plane); 16 warps, 2 rows each (both x
+// passes stay inside the warp).  x = n2 + 16 n1 -> pass A: DFT16 over n1 (thread (row, n2)),
+// twiddle W_256^{n2 k1}; pass B: DFT16 over n2 (thread (row, k1)); position k1*16 + k2 holds
+// frequency k1 + 16 k2.  Shared row layout: slot k1*17 + j (j = n2, then k2; inverse: n1*17 + n2).
 template <bool FWD, bool SPEC>
 __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
-  constexpr int PX = kBig, RS = PX + 2, R1 = kBigR, R2 = kBigR;
-  constexpr int RPW = 4;
+  constexpr int PX = kBig, RS = kBigRS, R = kBigR;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* buf = reinterpret_cast<float2*>(smem_raw);
   uint16_t* tv = reinterpret_cast<uint16_t*>(smem_raw + kBigRows * RS * 8);
-  const uint32_t* tv32 = reinterpret_cast<const uint32_t*>(tv);
-  float4* twx = reinterpret_cast<float4*>(smem_raw + kBigRows * RS * 8 + kBigRows * PX * 2);
-  uint16_t* tv2 = reinterpret_cast<uint16_t*>(smem_raw + kBigRows * RS * 8 + kBigRows * PX * 2 + (kBigR / 2) * (kBigR + 1) * 16);
-  const uint32_t* tv2_32 = reinterpret_cast<const uint32_t*>(tv2);
+  uint16_t* tv2 = tv + kBigRows * PX;
+  float2* tws = reinterpret_cast<float2*>(smem_raw + kBigRows * RS * 8 + 2 * kBigRows * PX * 2);   // [n2][k1], stride 17
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = blockIdx.y;
@@ -107,17 +112,13 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
   float2* Sitem = a.S + (((size_t)img * a.upl + lu) * a.K_max + k) * (size_t)(kBig * kBig);
   if constexpr (SPEC) Sitem = a.S + (size_t)k * (kBig * kBig);
 
-  auto ld2 = [&](int y, int x) -> float4 { return *reinterpret_cast<const float4*>(buf + y * RS + x); };
-  auto st2 = [&](int y, int x, float2 p, float2 q) {
-    *reinterpret_cast<float4*>(buf + y * RS + x) = make_float4(p.x, p.y, q.x, q.y);
-  };
-  // twiddle pairs (W^{n2 k1}, W^{(n2+1) k1}), stride R1+1
-  for (int j = tid; j < (R2 / 2) * (R1 + 1); j += kBigNT) {
-    const int n2p = j / (R1 + 1), k1 = j - n2p * (R1 + 1), n2 = 2 * n2p;
-    const float2 w0 = c_tw[TwOff<PX>::v + (n2 * k1) % PX];
-    const float2 w1 = c_tw[TwOff<PX>::v + ((n2 + 1) * k1) % PX];
-    twx[j] = make_float4(w0.x, w0.y, w1.x, w1.y);
-  }
+  // x twiddles W_256^{n2 k1}
+  if (tid < R * R) tws[(tid >> 4) * (R + 1) + (tid & 15)] = c_tw[TwOff<PX>::v + ((tid >> 4) * (tid & 15)) % PX];
+  // this thread's items: row y of the warp's two, index j = n2 (pass A) / k1 (pass B)
+  const int y = warp * 2 + (lane >> 4), j = lane & 15;
+  float2* rowb = buf + y * RS;
+  // position x' = 16 a + b of a row <-> slot a*17 + b
+  auto slot = [](int x) { return (x >> 4) * (kBigR + 1) + (x & 15); };
 
   if constexpr (FWD) {
     // ---- stage tonal indices of rows [row0, row0+32) of the tile's input window
@@ -133,10 +134,6 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
         tv[p] = t;
       }
     } else {
-      // batches of GB independent (predicated) loads per thread, then the
-      // conversions: the image reads overlap instead of paying one latency each
-      constexpr int IT = kBigRows * PX / kBigNT, GB = 16;
-      static_assert(IT % GB == 0, "staging split");
       auto stage_unit = [&](int uty, int utx, int bias, uint16_t* tvd) {
         if (a.img_dtype == 0 && a.img_def == nullptr) {
           // uint8 images without a mask: 16-byte loads of the aligned chunks that cover each
@@ -174,6 +171,9 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
           }
           return;
         }
+        // generic path: batches of independent (predicated) loads per thread
+        constexpr int IT = kBigRows * PX / kBigNT, GB = 16;
+        static_assert(IT % GB == 0, "staging split");
 #pragma unroll 1
         for (int g0 = 0; g0 < IT; g0 += GB) {
           int raw[GB];
@@ -224,119 +224,91 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
       const bool live = t != kSent;
       return make_float2(live ? cs : 0.f, live ? -sn : 0.f);
     };
-    // ---- x pass A (encode): item (row, n2 pair), one per lane
+    // ---- x pass A (encode): thread (y, n2 = j)
     {
-      const int y = warp * RPW + lane % RPW, n2 = 2 * (lane / RPW);
-      float2 wa[R1], wb[R1];
+      float2 w[R];
+      const uint16_t* trow = tv + y * PX + j;
       if (!SPEC && paired) {
         // Nyquist plane of two units: (-1)^v of this unit + i (-1)^v of its neighbour
         auto nyq = [](uint32_t t) -> float { return t == kSent ? 0.f : ((t & 1u) ? -1.f : 1.f); };
+        const uint16_t* trow2 = tv2 + y * PX + j;
 #pragma unroll
-        for (int n1 = 0; n1 < R1; ++n1) {
-          const uint32_t tt = tv32[(y * PX + n2 + R2 * n1) / 2], t2 = tv2_32[(y * PX + n2 + R2 * n1) / 2];
-          wa[n1] = make_float2(nyq(tt & 0xFFFFu), nyq(t2 & 0xFFFFu));
-          wb[n1] = make_float2(nyq(tt >> 16), nyq(t2 >> 16));
-        }
+        for (int n1 = 0; n1 < R; ++n1) w[n1] = make_float2(nyq(trow[R * n1]), nyq(trow2[R * n1]));
       } else {
 #pragma unroll
-        for (int n1 = 0; n1 < R1; ++n1) {
-          const uint32_t tt = tv32[(y * PX + n2 + R2 * n1) / 2];
-          wa[n1] = enc(tt & 0xFFFFu);
-          wb[n1] = enc(tt >> 16);
-        }
+        for (int n1 = 0; n1 < R; ++n1) w[n1] = enc(trow[R * n1]);
       }
-      dft<R1, false>(wa);
-      dft<R1, false>(wb);
+      dft<R, false>(w);
+      rowb[j] = w[0];
 #pragma unroll
-      for (int k1 = 0; k1 < R1; ++k1) {
-        float2 za = wa[k1], zb = wb[k1];
-        if (k1 != 0) {
-          const float4 w = twx[(n2 / 2) * (R1 + 1) + k1];
-          za = cmul(za, make_float2(w.x, w.y));
-          zb = cmul(zb, make_float2(w.z, w.w));
-        }
-        st2(y, n2 + R2 * k1, za, zb);
-      }
+      for (int k1 = 1; k1 < R; ++k1) rowb[k1 * (R + 1) + j] = cmul(w[k1], tws[j * (R + 1) + k1]);
     }
     __syncwarp();
-    // ---- x pass B: items (row, k1), two per lane; result rows -> S
+    // ---- x pass B: thread (y, k1 = j); the row then holds position k1*16 + k2 at slot k1*17 + k2
+    {
+      float2 w[R];
 #pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      const int i = lane + 32 * g;
-      const int y = warp * RPW + i % RPW, k1 = i / RPW;
-      float2 w[R2];
+      for (int n2 = 0; n2 < R; ++n2) w[n2] = rowb[j * (R + 1) + n2];
+      dft<R, false>(w);
 #pragma unroll
-      for (int q = 0; q < R2 / 2; ++q) {
-        const float4 p = ld2(y, 2 * q + R2 * k1);
-        w[2 * q] = make_float2(p.x, p.y);
-        w[2 * q + 1] = make_float2(p.z, p.w);
-      }
-      dft<R2, false>(w);
-#pragma unroll
-      for (int q = 0; q < R2 / 2; ++q) st2(y, 2 * q + R2 * k1, w[2 * q], w[2 * q + 1]);
+      for (int k2 = 0; k2 < R; ++k2) rowb[j * (R + 1) + k2] = w[k2];
     }
     __syncthreads();
     // coalesced row stores (positions = permuted frequencies)
     for (int i = tid; i < kBigRows * (PX / 2); i += kBigNT) {
-      const int y = i / (PX / 2), xp = i % (PX / 2);
-      reinterpret_cast<float4*>(Sitem + (size_t)(row0 + y) * kBig)[xp] = ld2(y, 2 * xp);
+      const int yy = i / (PX / 2), xp = i % (PX / 2);
+      const float2 p0 = buf[yy * RS + slot(2 * xp)], p1 = buf[yy * RS + slot(2 * xp + 1)];
+      reinterpret_cast<float4*>(Sitem + (size_t)(row0 + yy) * kBig)[xp] = make_float4(p0.x, p0.y, p1.x, p1.y);
     }
   } else {
     // ---- inverse: load valid rows, x pass B^-1, x pass A^-1, store valid columns
     const int nrows = min(kBigRows, kBig - row0);
-#pragma unroll 4
-    for (int i = tid; i < kBigRows * (PX / 2); i += kBigNT) {
-      const int y = i / (PX / 2), xp = i % (PX / 2);
-      if (y < nrows) cp_async16(buf + y * RS + 2 * xp, reinterpret_cast<const float4*>(Sitem + (size_t)(row0 + y) * kBig) + xp);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
+    {
+      constexpr int IT = kBigRows * (PX / 2) / kBigNT;   // 8 float4 per thread, all loads in flight
+      float4 v[IT];
 #pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      const int i = lane + 32 * g;
-      const int y = warp * RPW + i % RPW, k1 = i / RPW;
-      float2 w[R2];
-#pragma unroll
-      for (int q = 0; q < R2 / 2; ++q) {
-        const float4 p = ld2(y, 2 * q + R2 * k1);
-        w[2 * q] = make_float2(p.x, p.y);
-        w[2 * q + 1] = make_float2(p.z, p.w);
+      for (int u = 0; u < IT; ++u) {
+        const int i = tid + u * kBigNT, yy = i / (PX / 2), xp = i % (PX / 2);
+        v[u] = yy < nrows ? __ldcs(reinterpret_cast<const float4*>(Sitem + (size_t)(row0 + yy) * kBig) + xp)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      dft<R2, true>(w);
 #pragma unroll
-      for (int q = 0; q < R2 / 2; ++q) st2(y, 2 * q + R2 * k1, w[2 * q], w[2 * q + 1]);
+      for (int u = 0; u < IT; ++u) {
+        const int i = tid + u * kBigNT, yy = i / (PX / 2), xp = i % (PX / 2);
+        buf[yy * RS + slot(2 * xp)] = make_float2(v[u].x, v[u].y);
+        buf[yy * RS + slot(2 * xp + 1)] = make_float2(v[u].z, v[u].w);
+      }
+    }
+    __syncthreads();
+    {
+      float2 w[R];
+#pragma unroll
+      for (int k2 = 0; k2 < R; ++k2) w[k2] = rowb[j * (R + 1) + k2];
+      dft<R, true>(w);
+#pragma unroll
+      for (int n2 = 0; n2 < R; ++n2) rowb[j * (R + 1) + n2] = w[n2];
     }
     __syncwarp();
     {
-      const int y = warp * RPW + lane % RPW, n2 = 2 * (lane / RPW);
-      float2 wa[R1], wb[R1];
+      float2 w[R];
+      w[0] = rowb[j];
 #pragma unroll
-      for (int k1 = 0; k1 < R1; ++k1) {
-        const float4 p = ld2(y, n2 + R2 * k1);
-        wa[k1] = make_float2(p.x, p.y);
-        wb[k1] = make_float2(p.z, p.w);
-        if (k1 != 0) {
-          const float4 w = twx[(n2 / 2) * (R1 + 1) + k1];
-          wa[k1] = cmulc(wa[k1], make_float2(w.x, w.y));
-          wb[k1] = cmulc(wb[k1], make_float2(w.z, w.w));
-        }
-      }
-      dft<R1, true>(wa);
-      dft<R1, true>(wb);
+      for (int k1 = 1; k1 < R; ++k1) w[k1] = cmulc(rowb[k1 * (R + 1) + j], tws[j * (R + 1) + k1]);
+      dft<R, true>(w);
+      // x = n2 + 16 n1 -> slot n1*17 + n2
 #pragma unroll
-      for (int n1 = 0; n1 < R1; ++n1) st2(y, n2 + R2 * n1, wa[n1], wb[n1]);
+      for (int n1 = 0; n1 < R; ++n1) rowb[n1 * (R + 1) + j] = w[n1];
     }
     __syncthreads();
     // valid window store: tile row ty_row = row0 + y (>= my-1), columns x >= mx-1
     float2* dst = a.chat + (((size_t)img * a.upl + lu) * a.K_max + k) * (size_t)a.wpx;
     const int vx = kBig - (a.mx - 1);   // valid columns per row
     for (int i = tid; i < kBigRows * vx; i += kBigNT) {
-      const int y = i / vx, c = i - (i / vx) * vx;
-      const int row = row0 + y;
-      if (y >= nrows) continue;
+      const int yy = i / vx, c = i - (i / vx) * vx;
+      const int row = row0 + yy;
+      if (yy >= nrows) continue;
       const int oy = ty * a.QY + row - (a.my - 1), ox = tx * a.QX + c;
-      const float2 v = buf[y * RS + (a.mx - 1) + c];
+      const float2 v = buf[yy * RS + slot((a.mx - 1) + c)];
       if (oy < a.OH && ox < a.OW) dst[(size_t)(row - (a.my - 1)) * a.QX + c] = paired ? make_float2(v.x, 0.f) : v;
       if (paired) {
         // the neighbour's plane is the imaginary part; its own tile position bounds the store
@@ -350,15 +322,15 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
 }
 
 // ------------------------------------------------------------------ columns (y axis)
-// CTA = 256 rows x 16 columns (8 column pairs) of one (image, tile, plane), 128 threads.
-// y pass A items (xp, n2), y pass B items (xp, k1): one per thread each.
+// CTA = 256 rows x 16 columns of one (image, tile, plane), 256 threads: thread (x, j) owns one
+// 16-point transform per pass (y = n2 + 16 n1: pass A over n1 with j = n2, pass B over n2 with
+// j = k1).  A warp's 64-bit accesses cover two rows of 16 consecutive columns.
 template <bool SPEC>
 __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a) {
-  constexpr int PY = kBig, PXC = kBigCols, RS = PXC + 2, R1 = kBigR, R2 = kBigR, XP = PXC / 2;
-  constexpr int SQ = R2;  // float4 (pairs) per thread in y pass B
+  constexpr int PY = kBig, PXC = kBigCols, RS = PXC + 2, R = kBigR;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* buf = reinterpret_cast<float2*>(smem_raw);
-  float4* sbuf = reinterpret_cast<float4*>(smem_raw + PY * RS * 8);
+  float2* sbuf = reinterpret_cast<float2*>(smem_raw + PY * RS * 8);   // [q][thread]
 
   const int tid = threadIdx.x;
   const int cb = blockIdx.x, k = blockIdx.y;
@@ -366,7 +338,6 @@ __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a
   const int unit = SPEC ? 0 : a.unit0 + lu;
   const int img = SPEC ? 0 : (int)(blockIdx.z / a.nub);
   int K = a.K;
-  const float4* spec_plane = nullptr;
   if constexpr (!SPEC) {
     const int4 up = a.unit_param[(size_t)img * a.units + unit];
     K = up.y + 1;
@@ -375,114 +346,85 @@ __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a
       int4 upp;
       if (big_pair_role(a, img, lu, k, up, upp) == 2) return;   // carried by the neighbour's CTAs
     }
-    spec_plane = a.spec + a.spec_off[up.z] + ((size_t)k * (kBig / kBigCols) + cb) * (SQ * kBigColsNT);
-    // the product's spectrum chunk streams in while the forward passes run
-#pragma unroll
-    for (int q = 0; q < SQ; ++q) cp_async16(sbuf + q * kBigColsNT + tid, spec_plane + q * kBigColsNT + tid);
-    cp_async_commit();
   }
   float2* Sitem = SPEC ? a.S + (size_t)k * (kBig * kBig)
                        : a.S + (((size_t)img * a.upl + lu) * a.K_max + k) * (size_t)(kBig * kBig);
-  auto ld2 = [&](int y, int x) -> float4 { return *reinterpret_cast<const float4*>(buf + y * RS + x); };
-  auto st2 = [&](int y, int x, float2 p, float2 q) {
-    *reinterpret_cast<float4*>(buf + y * RS + x) = make_float4(p.x, p.y, q.x, q.y);
-  };
   // load 256 rows x 16 columns: all async copies in flight at once
+  constexpr int XP = PXC / 2;
 #pragma unroll 4
   for (int i = tid; i < PY * XP; i += kBigColsNT) {
-    const int y = i / XP, xp = i % XP;
-    cp_async16(buf + y * RS + 2 * xp, reinterpret_cast<const float4*>(Sitem + (size_t)y * kBig + cb * PXC) + xp);
+    const int yy = i / XP, xp = i % XP;
+    cp_async16(buf + yy * RS + 2 * xp, reinterpret_cast<const float4*>(Sitem + (size_t)yy * kBig + cb * PXC) + xp);
   }
   cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  // ---- forward y pass A: item (xp, n2)
-  {
-    const int xp = tid % XP, n2 = tid / XP;
-    float2 wa[R1], wb[R1];
+  if constexpr (!SPEC) {
+    // the product's spectrum chunk (thread order) streams in while forward pass A runs
+    const int4 up = a.unit_param[(size_t)img * a.units + unit];
+    const float4* spec_plane = a.spec + a.spec_off[up.z] + ((size_t)k * (kBig / kBigCols) + cb) * (R * kBigColsNT / 2);
+    float4* sb4 = reinterpret_cast<float4*>(sbuf);
 #pragma unroll
-    for (int n1 = 0; n1 < R1; ++n1) {
-      const float4 p = ld2(n2 + R2 * n1, 2 * xp);
-      wa[n1] = make_float2(p.x, p.y);
-      wb[n1] = make_float2(p.z, p.w);
-    }
-    dft<R1, false>(wa);
-    dft<R1, false>(wb);
-#pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) {
-      float2 za = wa[k1], zb = wb[k1];
-      if (k1 != 0) {
-        const float2 w = c_tw[TwOff<PY>::v + n2 * k1];
-        za = cmul(za, w);
-        zb = cmul(zb, w);
-      }
-      st2(n2 + R2 * k1, 2 * xp, za, zb);
-    }
+    for (int q = 0; q < R / 2; ++q) cp_async16(sb4 + q * kBigColsNT + tid, spec_plane + q * kBigColsNT + tid);
+    cp_async_commit();
+    cp_async_wait<1>();   // the tile (first group)
+  } else {
+    cp_async_wait<0>();
   }
   __syncthreads();
-  // ---- forward y pass B (+ product + inverse y pass B): item (xp, k1)
+  const int x = tid & (PXC - 1), j = tid >> 4;
+  float2* col = buf + x;
+  // ---- forward y pass A: thread (x, n2 = j)
   {
-    const int xp = tid % XP, k1 = tid / XP;
-    float2 wa[R2], wb[R2];
+    float2 w[R];
 #pragma unroll
-    for (int n2 = 0; n2 < R2; ++n2) {
-      const float4 p = ld2(n2 + R2 * k1, 2 * xp);
-      wa[n2] = make_float2(p.x, p.y);
-      wb[n2] = make_float2(p.z, p.w);
-    }
-    dft<R2, false>(wa);
-    dft<R2, false>(wb);
+    for (int n1 = 0; n1 < R; ++n1) w[n1] = col[(j + R * n1) * RS];
+    dft<R, false>(w);
+    col[j * RS] = w[0];
+#pragma unroll
+    for (int k1 = 1; k1 < R; ++k1) col[(j + R * k1) * RS] = cmul(w[k1], c_tw[TwOff<PY>::v + j * k1]);
+  }
+  if constexpr (!SPEC) cp_async_wait<0>();   // the spectrum chunk (other threads' copies: published by the barrier)
+  __syncthreads();
+  // ---- forward y pass B (+ product + inverse y pass B): thread (x, k1 = j)
+  {
+    float2 w[R];
+#pragma unroll
+    for (int n2 = 0; n2 < R; ++n2) w[n2] = col[(n2 + R * j) * RS];
+    dft<R, false>(w);
     if constexpr (SPEC) {
-      float4* so = const_cast<float4*>(a.spec) + ((size_t)k * (kBig / kBigCols) + cb) * (SQ * kBigColsNT);
+      float2* so = reinterpret_cast<float2*>(const_cast<float4*>(a.spec)) + ((size_t)k * (kBig / kBigCols) + cb) * (R * kBigColsNT);
       const float s = a.spec_scale;
 #pragma unroll
-      for (int q = 0; q < SQ; ++q) so[q * kBigColsNT + tid] = make_float4(wa[q].x * s, wa[q].y * s, wb[q].x * s, wb[q].y * s);
+      for (int q = 0; q < R; ++q) so[q * kBigColsNT + tid] = make_float2(w[q].x * s, w[q].y * s);
     } else {
-      cp_async_wait<0>();
 #pragma unroll
-      for (int q = 0; q < SQ; ++q) {
-        const float4 s = sbuf[q * kBigColsNT + tid];
-        wa[q] = cmul(wa[q], make_float2(s.x, s.y));
-        wb[q] = cmul(wb[q], make_float2(s.z, s.w));
-      }
-      dft<R2, true>(wa);
-      dft<R2, true>(wb);
+      for (int q = 0; q < R; ++q) w[q] = cmul(w[q], sbuf[q * kBigColsNT + tid]);
+      dft<R, true>(w);
 #pragma unroll
-      for (int n2 = 0; n2 < R2; ++n2) st2(n2 + R2 * k1, 2 * xp, wa[n2], wb[n2]);
+      for (int n2 = 0; n2 < R; ++n2) col[(n2 + R * j) * RS] = w[n2];
     }
   }
   if constexpr (SPEC) return;
   __syncthreads();
-  // ---- inverse y pass A: item (xp, n2)
+  // ---- inverse y pass A: thread (x, n2 = j)
   {
-    const int xp = tid % XP, n2 = tid / XP;
-    float2 wa[R1], wb[R1];
+    float2 w[R];
+    w[0] = col[j * RS];
 #pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) {
-      const float4 p = ld2(n2 + R2 * k1, 2 * xp);
-      wa[k1] = make_float2(p.x, p.y);
-      wb[k1] = make_float2(p.z, p.w);
-      if (k1 != 0) {
-        const float2 w = c_tw[TwOff<PY>::v + n2 * k1];
-        wa[k1] = cmulc(wa[k1], w);
-        wb[k1] = cmulc(wb[k1], w);
-      }
-    }
-    dft<R1, true>(wa);
-    dft<R1, true>(wb);
+    for (int k1 = 1; k1 < R; ++k1) w[k1] = cmulc(col[(j + R * k1) * RS], c_tw[TwOff<PY>::v + j * k1]);
+    dft<R, true>(w);
 #pragma unroll
-    for (int n1 = 0; n1 < R1; ++n1) st2(n2 + R2 * n1, 2 * xp, wa[n1], wb[n1]);
+    for (int n1 = 0; n1 < R; ++n1) col[(j + R * n1) * RS] = w[n1];
   }
   __syncthreads();
   // store the valid rows back (row-inverse kernel reads rows >= my-1)
   for (int i = tid; i < PY * XP; i += kBigColsNT) {
-    const int y = i / XP, xp = i % XP;
-    if (y < a.my - 1) continue;
-    reinterpret_cast<float4*>(Sitem + (size_t)y * kBig + cb * PXC)[xp] = ld2(y, 2 * xp);
+    const int yy = i / XP, xp = i % XP;
+    if (yy < a.my - 1) continue;
+    reinterpret_cast<float4*>(Sitem + (size_t)yy * kBig + cb * PXC)[xp] = *reinterpret_cast<const float4*>(buf + yy * RS + 2 * xp);
   }
 }
 
-constexpr int kBigRowsSmem = kBigRows * (kBig + 2) * 8 + 2 * kBigRows * kBig * 2 + (kBigR / 2) * (kBigR + 1) * 16;
-constexpr int kBigColsSmem = kBig * (kBigCols + 2) * 8 + kBigR * kBigColsNT * 16;
+constexpr int kBigRowsSmem = kBigRows * kBigRS * 8 + 2 * kBigRows * kBig * 2 + kBigR * (kBigR + 1) * 8;
+constexpr int kBigColsSmem = kBig * (kBigCols + 2) * 8 + kBigR * kBigColsNT * 8;
 
 }  // namespace fm

@@ -444,7 +444,12 @@ __global__ void __launch_bounds__(NT) tonal_kernel_dispatch(const TonalArgs a) {
 // cp.async.bulk per plane, issued by one thread, completion on an mbarrier),
 // so HBM reads overlap the FFT and threshold work of the current item.
 template <int N>
-constexpr int tonal_pipe_nt() { return (N + 1) * 128 * 8 * 2 > 96 * 1024 ? 64 : 128; }
+constexpr int tonal_pipe_nt() {
+#ifdef FM_PIPE_NT_SMALL
+  if (N <= 2) return FM_PIPE_NT_SMALL;   // one or two planes per pixel: larger items amortise the ring handshake
+#endif
+  return (N + 1) * 128 * 8 * 2 > 96 * 1024 ? 64 : 128;
+}
 template <int N>
 constexpr int tonal_pipe_st() { return 2; }   // two stages: more CTAs per SM beat a deeper ring (measured)
 template <int N>
