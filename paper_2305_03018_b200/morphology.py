@@ -39,9 +39,15 @@ class MorphMethod(enum.Enum):
 
 # --------------------------------------------------------------------------- helpers
 
+_cuda_ok = False
+
+
 def _device():
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2305_03018_b200 needs a CUDA device (B200); there is no CPU fallback")
+    global _cuda_ok
+    if not _cuda_ok:   # (checked once: the query costs ~7 us per call)
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2305_03018_b200 needs a CUDA device (B200); there is no CPU fallback")
+        _cuda_ok = True
     return torch.device("cuda", torch.cuda.current_device())
 
 
@@ -71,10 +77,32 @@ def _upload(g: GridFunction, dev):
     return t, mask, dt, lo_v, hi_v
 
 
+_SMALL_ELEMS = 1 << 16   # grids up to this size take the one-call host-buffer path
+
+
+def _narrow_dtype(g: GridFunction):
+    lo_v, hi_v = g.min_defined(), g.max_defined()
+    if lo_v >= 0 and hi_v <= 255:
+        return torch.uint8, lo_v, hi_v
+    if lo_v >= 0 and hi_v <= 65535:
+        return torch.uint16, lo_v, hi_v
+    if lo_v >= -(2**31) and hi_v < 2**31:
+        return torch.int32, lo_v, hi_v
+    raise NotImplementedError("image values beyond int32")
+
+
 def _run_fft(f: GridFunction, b: GridFunction, *, mode: str, crop: bool, fill: int,
              stats: dict | None):
     dev = _device()
-    img, mask, dt, vmin, vmax = _upload(f, dev)
+    small = f.values.size <= _SMALL_ELEMS
+    if small:
+        # small grids: the call is bound by its fixed costs, so it is ONE library call on host
+        # buffers (fm_execute_host: upload, kernels, download, synchronise) instead of pinned
+        # staging tensors, device tensors, an extrema kernel and four stream operations
+        dt, vmin, vmax = _narrow_dtype(f)
+        img = mask = None
+    else:
+        img, mask, dt, vmin, vmax = _upload(f, dev)
     # plans are keyed on the normalised range [0, 2^k - 1] holding the data (the per-tile
     # range kernel adapts every tile's tonal length to the data itself), so images of one
     # bit depth share a cached plan; the exact range is the fallback when the wider one
@@ -113,7 +141,19 @@ def _run_fft(f: GridFunction, b: GridFunction, *, mode: str, crop: bool, fill: i
             raise
         plan = get(vmin, vmax)
     plan.reset_stats()
-    out, valid = plan.execute(img.unsqueeze(0), None if mask is None else mask.unsqueeze(0))
+    if small:
+        with warnings.catch_warnings():   # read-only arrays by contract; only read here
+            warnings.simplefilter("ignore", UserWarning)
+            src = torch.from_numpy(np.ascontiguousarray(f.values))
+            if f.gap_free:
+                h_mask = None
+            else:
+                h_def = torch.from_numpy(np.ascontiguousarray(f.defined))
+                src = torch.where(h_def, src, torch.zeros((), dtype=src.dtype))
+                h_mask = h_def.to(torch.uint8)
+        out, valid = plan.execute_host(src.to(dt), h_mask)
+    else:
+        out, valid = plan.execute(img.unsqueeze(0), None if mask is None else mask.unsqueeze(0))
     dev_max = plan.read_stats()          # raises ArithmeticError at >= 0.25 (fft_conv.py:145-148)
     if stats is not None:
         # morphology.py:125-128; padded_shape reports the B200 FFT extents: tile + tonal length
@@ -121,6 +161,9 @@ def _run_fft(f: GridFunction, b: GridFunction, *, mode: str, crop: bool, fill: i
         info = plan.info
         tile = (info["tile_x"],) if f.ndim == 1 else (info["tile_y"], info["tile_x"])
         stats["padded_shape"] = tuple(tile) + (info["tonal_len"],)
+    if small:
+        mn, mx = torch.aminmax(out[0])
+        return out[0].to(torch.int64).numpy(), valid[0].to(torch.bool).numpy(), (int(mn), int(mx))
     mn, mx = torch.aminmax(out[0])
     # results come back in the plan's narrow type and widen to the reference's int64 / bool
     # with torch's multithreaded CPU conversions (pinned staging, one copy each)
