@@ -28,6 +28,7 @@ constexpr int kBigCols = 16;     // columns per column-kernel CTA
 constexpr int kBigNT = 512;      // row kernels: one 16-point item per thread and pass
 constexpr int kBigColsNT = 256;  // column kernel: one 16-point item per thread and pass
 constexpr int kBigRS = kBigR * (kBigR + 1);   // row kernels: row stride of the [k1][17] layout (float2)
+constexpr int kBigTvLd = kBig + 16;           // row stride of the staged tonal indices (chunk-aligned staging)
 
 struct BigArgs {
   // image batch (CONV) or SE (SPEC)
@@ -81,8 +82,8 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* buf = reinterpret_cast<float2*>(smem_raw);
   uint16_t* tv = reinterpret_cast<uint16_t*>(smem_raw + kBigRows * RS * 8);
-  uint16_t* tv2 = tv + kBigRows * PX;
-  float2* tws = reinterpret_cast<float2*>(smem_raw + kBigRows * RS * 8 + 2 * kBigRows * PX * 2);   // [n2][k1], stride 17
+  uint16_t* tv2 = tv + kBigRows * kBigTvLd;
+  float2* tws = reinterpret_cast<float2*>(smem_raw + kBigRows * RS * 8 + 2 * kBigRows * kBigTvLd * 2);   // [n2][k1], stride 17
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = blockIdx.y;
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
 
   if constexpr (FWD) {
     // ---- stage tonal indices of rows [row0, row0+32) of the tile's input window
-    int bad = 0;
+    int bad = 0, sh1 = 0, sh2 = 0;
     if constexpr (SPEC) {
       for (int p = tid; p < kBigRows * PX; p += kBigNT) {
         const int py = row0 + p / PX, px = p % PX;
@@ -131,16 +132,54 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
           const int si = py * a.mx + px;
           if (a.se_def == nullptr || a.se_def[si]) t = (uint16_t)(a.se_vals[si] + a.enc_bias);
         }
-        tv[p] = t;
+        tv[(p / PX) * kBigTvLd + px] = t;
       }
     } else {
-      auto stage_unit = [&](int uty, int utx, int bias, uint16_t* tvd) {
+      // returns the column shift sh: tile column c of row r is staged at tvd[r * kBigTvLd + sh + c]
+      auto stage_unit = [&](int uty, int utx, int bias, uint16_t* tvd) -> int {
+        const int ixb = utx * a.QX + a.DX;              // image column of tile column 0
+        if (a.img_dtype == 0 && a.img_def == nullptr && (a.W & 15) == 0 &&
+            (reinterpret_cast<uintptr_t>(a.img) & 15) == 0) {
+          // uint8 rows 16-byte aligned, no mask: the staged row starts at the 16-aligned image
+          // column xa <= ixb, so every aligned 16-pixel chunk of the image (inside or outside
+          // the image as a whole) becomes two aligned 16-byte shared-memory stores
+          const int xa = ixb & ~15, sh = ixb - xa;
+          const uint8_t* base = reinterpret_cast<const uint8_t*>(a.img) + (int64_t)img * a.H * a.W;
+          constexpr int CPR = kBigTvLd / 16;
+#pragma unroll 1
+          for (int it = tid; it < kBigRows * CPR; it += kBigNT) {
+            const int r = it / CPR, ch = it - r * CPR;
+            const int iy = uty * a.QY + a.DY + row0 + r, xc = xa + 16 * ch;
+            uint32_t pk[8];
+            if (iy < 0 || iy >= a.H || xc < 0 || xc >= a.W) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) pk[i] = (uint32_t)kSent | ((uint32_t)kSent << 16);
+            } else {
+              const uint4 wv = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)iy * a.W + xc));
+              const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
+              const int c0 = 16 * ch - sh;   // tile column of the chunk's first pixel
+              uint32_t t16[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const int v = max(a.enc_sign * (int)__byte_perm(wd[e >> 2], 0, 0x4440 + (e & 3)) + bias, 0);
+                const bool in_tile = (unsigned)(c0 + e) < (unsigned)PX;
+                if (in_tile && v >= T) bad = 1;
+                t16[e] = (in_tile && v < T) ? (uint32_t)v : (uint32_t)kSent;
+              }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) pk[i] = t16[2 * i] | (t16[2 * i + 1] << 16);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(tvd + r * kBigTvLd + 16 * ch);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+          return sh;
+        }
         if (a.img_dtype == 0 && a.img_def == nullptr) {
           // uint8 images without a mask: 16-byte loads of the aligned chunks that cover each
           // row part inside the image (one load per 16 pixels instead of one per pixel)
-          const int ixb = utx * a.QX + a.DX;              // image column of tile column 0
           const int xs = max(ixb, 0), xe = min(ixb + PX, a.W);
-          for (int i = tid; i < kBigRows * PX / 2; i += kBigNT)
+          for (int i = tid; i < kBigRows * kBigTvLd / 2; i += kBigNT)
             reinterpret_cast<uint32_t*>(tvd)[i] = (uint32_t)kSent | ((uint32_t)kSent << 16);
           __syncthreads();
           if (xs < xe) {
@@ -165,11 +204,11 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
                 const int f = (int)((wd[e >> 2] >> (8 * (e & 3))) & 0xFFu);
                 const int v = max(a.enc_sign * f + bias, 0);
                 if (v >= T) bad = 1;
-                else tvd[r * PX + (x - ixb)] = (uint16_t)v;
+                else tvd[r * kBigTvLd + (x - ixb)] = (uint16_t)v;
               }
             }
           }
-          return;
+          return 0;
         }
         // generic path: batches of independent (predicated) loads per thread
         constexpr int IT = kBigRows * PX / kBigNT, GB = 16;
@@ -200,14 +239,16 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
               if (v >= T) bad = 1;
               else t = (uint16_t)v;
             }
-            tvd[tid + (g0 + u) * kBigNT] = t;
+            const int pp = tid + (g0 + u) * kBigNT;
+            tvd[(pp / PX) * kBigTvLd + pp % PX] = t;
           }
         }
+        return 0;
       };
-      stage_unit(ty, tx, enc_bias, tv);
+      sh1 = stage_unit(ty, tx, enc_bias, tv);
       if (paired) {
         const int u2 = unit + 1, ty2 = u2 / max(a.tiles_x, 1);
-        stage_unit(ty2, u2 - ty2 * max(a.tiles_x, 1), enc_bias2, tv2);
+        sh2 = stage_unit(ty2, u2 - ty2 * max(a.tiles_x, 1), enc_bias2, tv2);
       }
     }
     if (!SPEC && bad) atomicOr(a.err, 1);
@@ -227,11 +268,11 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
     // ---- x pass A (encode): thread (y, n2 = j)
     {
       float2 w[R];
-      const uint16_t* trow = tv + y * PX + j;
+      const uint16_t* trow = tv + y * kBigTvLd + sh1 + j;
       if (!SPEC && paired) {
         // Nyquist plane of two units: (-1)^v of this unit + i (-1)^v of its neighbour
         auto nyq = [](uint32_t t) -> float { return t == kSent ? 0.f : ((t & 1u) ? -1.f : 1.f); };
-        const uint16_t* trow2 = tv2 + y * PX + j;
+        const uint16_t* trow2 = tv2 + y * kBigTvLd + sh2 + j;
 #pragma unroll
         for (int n1 = 0; n1 < R; ++n1) w[n1] = make_float2(nyq(trow[R * n1]), nyq(trow2[R * n1]));
       } else {
@@ -424,7 +465,7 @@ __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a
   }
 }
 
-constexpr int kBigRowsSmem = kBigRows * kBigRS * 8 + 2 * kBigRows * kBig * 2 + kBigR * (kBigR + 1) * 8;
+constexpr int kBigRowsSmem = kBigRows * kBigRS * 8 + 2 * kBigRows * kBigTvLd * 2 + kBigR * (kBigR + 1) * 8;
 constexpr int kBigColsSmem = kBig * (kBigCols + 2) * 8 + kBigR * kBigColsNT * 8;
 
 }  // namespace fm
