@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
             lvl = level_of(bnd);
           }
           if (lvl <= floor_d) break;  // no clamp possible: stop
+#ifdef FM_RANGE_BRANCHY
           if (t >= a.ntaps || g >= lvl) {
             if (t >= a.ntaps && g < bnd) atomicMin(&s_bound, g);
             q += kRangeNT;
@@ -435,6 +436,21 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
             t = 0;
             g = INT32_MIN;
           }
+#else
+          {
+            // advance to the lane's next pixel by selects (no divergent region per iteration);
+            // only the rare new minimum branches
+            const bool all_taps = t >= a.ntaps, adv = all_taps || g >= lvl;
+            if (all_taps && g < bnd) atomicMin(&s_bound, g);
+            const int qn = q + kRangeNT;
+            if (adv && qn >= npx) break;
+            const int basen = base_of(min(qn, npx - 1));
+            q = adv ? qn : q;
+            base = adv ? basen : base;
+            t = adv ? 0 : t;
+            g = adv ? INT32_MIN : g;
+          }
+#endif
           const int4 o0 = *reinterpret_cast<const int4*>(s_toff + t), o1 = *reinterpret_cast<const int4*>(s_toff + t + 4);
           const int4 b0 = *reinterpret_cast<const int4*>(s_tb + t), b1 = *reinterpret_cast<const int4*>(s_tb + t + 4);
           g = max(g, (int)swin[base + o0.x] + b0.x);
