@@ -284,6 +284,8 @@ const int g_fuse_kch = std::getenv("FM_FUSE_KCH") ? std::atoi(std::getenv("FM_FU
 const bool g_discard = !(std::getenv("FM_DISCARD") && std::getenv("FM_DISCARD")[0] == '0');
 // FM_DEVDISPATCH=0: small launches also wait on the host for the per-ladder counts (A/B)
 const bool g_devdispatch = !(std::getenv("FM_DEVDISPATCH") && std::getenv("FM_DEVDISPATCH")[0] == '0');
+// FM_BIG_JOBS=0: the 256^2 kernels launch a (plane, unit x image) grid instead of the compact job list (A/B)
+const bool g_big_jobs = !(std::getenv("FM_BIG_JOBS") && std::getenv("FM_BIG_JOBS")[0] == '0');
 // FM_BIG_PAIR=0: no Nyquist-plane pairing of neighbouring units on the 256^2 path (A/B)
 const bool g_big_pair = !(std::getenv("FM_BIG_PAIR") && std::getenv("FM_BIG_PAIR")[0] == '0');
 const int g_big_steps = std::getenv("FM_BIG_STEPS") ? std::atoi(std::getenv("FM_BIG_STEPS")) : 1;
@@ -430,6 +432,9 @@ struct fm_plan {
   // 256x256 tiles through an HBM scratch (fm_bigtile.cuh) for wide SEs
   bool big = false;
   float2* S = nullptr;
+  int2* big_jobs = nullptr;        // 256^2 path: compact (image, unit, plane) job list + counter
+  int* big_njobs = nullptr;
+  int64_t big_jobs_cap = 0;
   // composite plan (SE wider than one tile, fm_plan_create): dilation by B = U B_i is the
   // max over the parts' dilations (erosion: min), validity OR-ed
   std::vector<fm_plan*> parts;
@@ -521,6 +526,8 @@ void free_plan(fm_plan* p) {
     if (p->conv_ev[b]) cudaEventDestroy(p->conv_ev[b]);
   if (p->tjoin_ev) cudaEventDestroy(p->tjoin_ev);
   cudaFree(p->S);
+  cudaFree(p->big_jobs);
+  cudaFree(p->big_njobs);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
   for (cudaEvent_t e : p->ev_chunks) cudaEventDestroy(e);
@@ -1175,6 +1182,11 @@ int fm_plan_create(fm_plan** out_plan, const fm_plan_desc* desc, const int32_t* 
     free_plan(p);
     return fail(FM_ENOMEM, std::string("tile scratch alloc: ") + cudaGetErrorString(e));
   }
+  if (p->big) {
+    p->big_jobs_cap = std::min<int64_t>((int64_t)slots * p->K, (int64_t)4 << 20);
+    if ((e = cudaMalloc(&p->big_jobs, sizeof(int2) * (size_t)p->big_jobs_cap)) != cudaSuccess) return cfail(e, "job list alloc");
+    if ((e = cudaMalloc(&p->big_njobs, sizeof(int))) != cudaSuccess) return cfail(e, "job list alloc");
+  }
   if (p->fuse_nmax > 0) {
     if ((e = cudaMalloc(&p->unit_done, sizeof(int) * (size_t)slots)) != cudaSuccess) return cfail(e, "counter alloc");
     cudaMemset(p->unit_done, 0, sizeof(int) * (size_t)slots);
@@ -1629,7 +1641,31 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         const int64_t item = (int64_t)kBig * kBig * 8 * kmax * n;
         ub = (int)std::max<int64_t>(1, std::min<int64_t>(nu, ((int64_t)g_big_l2_mb << 20) / item));
       }
-      for (int b0 = 0; b0 < nu; b0 += ub) {
+      // compact job list (fm_bigtile.cuh): an upper bound of the live items sizes the grid -- the
+      // per-ladder counts give the planes, the "full" units of the launch drop their plane 0
+      // (the pairing of Nyquist planes is only known on the device); CTAs past the device
+      // count exit
+      int64_t jobs_upper = 0;
+      for (int li = 0; li < L; ++li)
+        jobs_upper += (int64_t)reinterpret_cast<volatile int*>(p->h_counts[buf])[li] * (p->ladder[li] + 1);
+      if (!g_no_skip0 && img_defined == nullptr) jobs_upper -= (int64_t)n * (p->full_prefix[u0 + nu] - p->full_prefix[u0]);
+      bool nu_done = false;
+      if (g_big_jobs && g_big_l2_mb <= 0 && nu <= 65535 && jobs_upper > 0 && jobs_upper <= p->big_jobs_cap) {
+        b.lu0 = 0;
+        b.nub = nu;
+        FM_CUDA(cudaMemsetAsync(p->big_njobs, 0, sizeof(int), s));
+        big_jobs_kernel<<<(unsigned)((nu * n + 255) / 256), 256, 0, s>>>(b, n, p->big_jobs, p->big_njobs, (int)p->big_jobs_cap);
+        b.jobs = p->big_jobs;
+        b.njobs = p->big_njobs;
+        const unsigned gy = (unsigned)std::min<int64_t>(jobs_upper, 65535), gz = (unsigned)((jobs_upper + gy - 1) / gy);
+        big_rows_kernel<true, false><<<dim3(kBig / kBigRows, gy, gz), kBigNT, kBigRowsSmem, s>>>(b);
+        big_cols_kernel<false><<<dim3(kBig / kBigCols, gy, gz), kBigColsNT, kBigColsSmem, s>>>(b);
+        big_rows_kernel<false, false><<<dim3(inv_blocks, gy, gz), kBigNT, kBigRowsSmem, s>>>(b);
+        g_launches += 4;
+        FM_CUDA(cudaGetLastError());
+        nu_done = true;
+      }
+      for (int b0 = 0; b0 < nu && !nu_done; b0 += ub) {
         b.lu0 = b0;
         b.nub = std::min(ub, nu - b0);
         const unsigned z = (unsigned)(b.nub * n);

@@ -53,6 +53,10 @@ struct BigArgs {
   int wpx;
   int* err;
   int pair;                   // Nyquist planes of neighbouring units share one complex transform
+  // compact job list (big_jobs_kernel): grid (blocks, y, z) -> job y + z * gridDim.y = (image,
+  // launch-local unit | plane << 16); nullptr: grid y = plane, z = unit x image
+  const int2* jobs;
+  const int* njobs;
 };
 
 // Nyquist-plane pairing.  Plane k = N of a unit (T = 2N) is REAL: w_T^{N v} = (-1)^v, and so is
@@ -71,6 +75,46 @@ __device__ __forceinline__ int big_pair_role(const BigArgs& a, int img, int lu, 
   return (lu & 1) ? 2 : 1;
 }
 
+// The live (image, unit, plane) items of a launch, compacted.  In the plain (plane, unit x image)
+// grid a CTA whose item does not exist (planes past the unit's tonal length, plane 0 of a "full"
+// unit, the Nyquist plane of a unit carried by its neighbour) holds a CTA slot with 70-100 KB of
+// shared memory until its unit_param load returns: at c4 five of six CTAs were such exits, 12-20 %
+// of the three kernels' warp samples.
+__global__ void big_jobs_kernel(const BigArgs a, int n_imgs, int2* jobs, int* njobs, int cap) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_imgs * a.nu) return;
+  const int img = i / a.nu, lu = i - img * a.nu;
+  const int4 up = a.unit_param[(size_t)img * a.units + a.unit0 + lu];
+  const int N = up.y, k0 = (up.w & 2) ? 1 : 0;
+  int4 upp;
+  const bool carried = big_pair_role(a, img, lu, N, up, upp) == 2;
+  const int nj = (N - k0 + 1) - (carried ? 1 : 0);
+  if (nj <= 0) return;
+  int base = atomicAdd(njobs, nj);
+  for (int k = k0; k <= N; ++k) {
+    if (carried && k == N) continue;
+    if (base < cap) jobs[base] = make_int2(img, lu | (k << 16));
+    ++base;
+  }
+}
+
+// (image, launch-local unit, plane) of a CTA; false: no such item
+__device__ __forceinline__ bool big_decode(const BigArgs& a, int& img, int& lu, int& k) {
+  if (a.jobs != nullptr) {
+    const int j = (int)blockIdx.y + (int)blockIdx.z * (int)gridDim.y;
+    if (j >= *a.njobs) return false;
+    const int2 job = a.jobs[j];
+    img = job.x;
+    lu = job.y & 0xFFFF;
+    k = job.y >> 16;
+    return true;
+  }
+  k = blockIdx.y;
+  lu = a.lu0 + (int)(blockIdx.z % a.nub);
+  img = (int)(blockIdx.z / a.nub);
+  return true;
+}
+
 // ------------------------------------------------------------------ rows (x axis)
 // CTA = 32 rows x 256 columns of one (image, tile, plane); 16 warps, 2 rows each (both x
 // passes stay inside the warp).  x = n2 + 16 n1 -> pass A: DFT16 over n1 (thread (row, n2)),
@@ -86,10 +130,11 @@ __global__ void __launch_bounds__(kBigNT, 2) big_rows_kernel(const BigArgs a) {
   float2* tws = reinterpret_cast<float2*>(smem_raw + kBigRows * RS * 8 + 2 * kBigRows * kBigTvLd * 2);   // [n2][k1], stride 17
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int k = blockIdx.y;
-  const int lu = SPEC ? 0 : a.lu0 + (int)(blockIdx.z % a.nub);
+  int k = blockIdx.y, lu = 0, img = 0;
+  if constexpr (!SPEC) {
+    if (!big_decode(a, img, lu, k)) return;
+  }
   const int unit = SPEC ? 0 : a.unit0 + lu;
-  const int img = SPEC ? 0 : (int)(blockIdx.z / a.nub);
   int T = a.T, K = a.K, enc_bias = a.enc_bias, enc_bias2 = 0;
   bool paired = false;
   if constexpr (!SPEC) {
@@ -374,10 +419,12 @@ __global__ void __launch_bounds__(kBigColsNT, 3) big_cols_kernel(const BigArgs a
   float2* sbuf = reinterpret_cast<float2*>(smem_raw + PY * RS * 8);   // [q][thread]
 
   const int tid = threadIdx.x;
-  const int cb = blockIdx.x, k = blockIdx.y;
-  const int lu = SPEC ? 0 : a.lu0 + (int)(blockIdx.z % a.nub);
+  const int cb = blockIdx.x;
+  int k = blockIdx.y, lu = 0, img = 0;
+  if constexpr (!SPEC) {
+    if (!big_decode(a, img, lu, k)) return;
+  }
   const int unit = SPEC ? 0 : a.unit0 + lu;
-  const int img = SPEC ? 0 : (int)(blockIdx.z / a.nub);
   int K = a.K;
   if constexpr (!SPEC) {
     const int4 up = a.unit_param[(size_t)img * a.units + unit];
