@@ -314,6 +314,8 @@ const int g_conv_waves = std::getenv("FM_CONV_WAVES") ? std::atoi(std::getenv("F
 // smallest N served by the pipelined tonal kernel (FM_TONAL_PIPE_MIN; measured at c4, N = 1:
 // the one-thread-per-pixel kernel is slower, 0.065 vs 0.038 ms, so the default keeps every N)
 const int g_tonal_pipe_min = std::getenv("FM_TONAL_PIPE_MIN") ? std::atoi(std::getenv("FM_TONAL_PIPE_MIN")) : 0;
+// longest tonal axis (N) served by tonal_kernel_rows instead of the pipelined kernel (FM_TONAL_ROWS_MAX; 0 = off)
+const int g_tonal_rows_max = std::getenv("FM_TONAL_ROWS_MAX") ? std::atoi(std::getenv("FM_TONAL_ROWS_MAX")) : 4;
 const int g_tonal_pipe_max = std::getenv("FM_TONAL_PIPE_MAX") ? std::atoi(std::getenv("FM_TONAL_PIPE_MAX")) : 40;
 
 const TonalVariant* find_tonal(int n) {
@@ -1916,7 +1918,18 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       t.list = p->bucket_list[buf] + (size_t)li * cap;
       const TonalVariant* tv = p->counts ? nullptr : p->ladder_var[li];
       const int occ = tv ? g_tonal_pipe_occ[tv - kTonal] : 0;
-      if (tv && occ > 0 && !g_tonal_nopipe && N <= g_tonal_pipe_max && N >= g_tonal_pipe_min) {
+      if (tv && N <= kRowsNMax && N <= g_tonal_rows_max) {
+#ifndef FM_ROWS_PPT
+#define FM_ROWS_PPT 8
+#endif
+#ifndef FM_ROWS_NT
+#define FM_ROWS_NT 128
+#endif
+        constexpr int kRowsNT = FM_ROWS_NT, kRowsPPT = FM_ROWS_PPT;
+        t.se_count = p->se_count;
+        tonal_kernel_rows<kRowsNT, kRowsPPT><<<dim3((unsigned)cnt, (unsigned)((p->npx + kRowsNT * kRowsPPT - 1) / (kRowsNT * kRowsPPT))),
+                                               kRowsNT, 0, ts>>>(t);
+      } else if (tv && occ > 0 && !g_tonal_nopipe && N <= g_tonal_pipe_max && N >= g_tonal_pipe_min) {
         t.njobs = cnt;
         const int64_t items = (int64_t)cnt * ((p->npx + tv->pipe_nt - 1) / tv->pipe_nt);
         const int grid = (int)std::min<int64_t>(items, (int64_t)g_num_sms * std::min(occ, g_tonal_occ_cap));

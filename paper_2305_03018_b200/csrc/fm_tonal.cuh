@@ -438,6 +438,33 @@ __global__ void __launch_bounds__(NT) tonal_kernel_dispatch(const TonalArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Very short tonal axes (N <= kRowsNMax: one to five planes per pixel, e.g. flat wide SEs after
+// the clamp, c4).  An item of the pipelined kernel would be a few hundred bytes and its ring
+// handshake and per-item parameter loads dominate; one thread per pixel (tonal_kernel_t) pays two
+// dependent parameter loads per pixel.  Here a thread takes PPT pixels of one unit (the unit's
+// parameters are loop invariant, the plane loads of the PPT pixels are independent).
+constexpr int kRowsNMax = 4;
+template <int NT, int PPT>
+__global__ void __launch_bounds__(NT) tonal_kernel_rows(const TonalArgs a) {
+  const int2 job = a.list[blockIdx.x];
+  float dev = 0.f;
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) {
+    const TonalPix pp = tonal_pixel_job(a, job, ((int)blockIdx.y * PPT + u) * NT + (int)threadIdx.x);
+    if (!pp.live) continue;
+    switch (a.N) {
+      case 1: tonal_pixel_reg<1>(a, pp, dev); break;
+      case 2: tonal_pixel_reg<2>(a, pp, dev); break;
+      case 3: tonal_pixel_reg<3>(a, pp, dev); break;
+      default: tonal_pixel_reg<4>(a, pp, dev); break;
+    }
+  }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o2));
+  if ((threadIdx.x & 31) == 0 && dev > 0.f) atomicMax(reinterpret_cast<int*>(a.dev_max), __float_as_int(dev));
+}
+
+// ---------------------------------------------------------------------------
 // Pipelined register-variant kernel (N <= kTonalRegMax).  Persistent CTAs walk
 // the (unit, pixel block) items of one ladder entry; the K spectral values of
 // the next ST items are streamed into shared memory by bulk async copies (one
