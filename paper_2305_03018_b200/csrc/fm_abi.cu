@@ -1452,6 +1452,9 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     r.cx = (p->mx - 1) / 2;
     r.ntaps = (int)p->taps.size();
     for (int i = 0; i < r.ntaps; ++i) r.taps[i] = p->taps[i];
+    r.flat_taps = r.ntaps > 0 ? 1 : 0;
+    for (int i = 0; i < r.ntaps; ++i)
+      if (p->taps[i].y != 0) r.flat_taps = 0;
     // split units between CTAs when there are too few of them to fill the GPU
     int S = 1;
     if (r.ntaps > 0) {

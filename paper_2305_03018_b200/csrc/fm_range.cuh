@@ -60,6 +60,7 @@ struct RangeArgs {
   int skip0;              // the conv path may skip plane 0 of "full" units
   int warp_sync;          // bound taps walked warp-synchronously (else per-lane pixel queues)
   int ntaps;              // 0: no clamp; else a multiple of 8 (padded with kTapPadB taps)
+  int flat_taps;          // every bound tap has b - se_min = 0 (flat SE, tap count a multiple of 8)
   int aligned;            // uint8 image rows 16-byte aligned (2-D, no mask): chunk-aligned staging
   const int* ladder;      // ascending N values
   int L;
@@ -417,6 +418,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
         if (stop_all) break;
       }
     } else {
+      const bool flat_taps = a.flat_taps != 0;
       int q = tid;
       if (q < npx) {
         int base = base_of(q), t = 0, g = INT32_MIN, seen = INT32_MIN, lvl = INT32_MIN;
@@ -452,15 +454,21 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
           }
 #endif
           const int4 o0 = *reinterpret_cast<const int4*>(s_toff + t), o1 = *reinterpret_cast<const int4*>(s_toff + t + 4);
-          const int4 b0 = *reinterpret_cast<const int4*>(s_tb + t), b1 = *reinterpret_cast<const int4*>(s_tb + t + 4);
-          g = max(g, (int)swin[base + o0.x] + b0.x);
-          g = max(g, (int)swin[base + o0.y] + b0.y);
-          g = max(g, (int)swin[base + o0.z] + b0.z);
-          g = max(g, (int)swin[base + o0.w] + b0.w);
-          g = max(g, (int)swin[base + o1.x] + b1.x);
-          g = max(g, (int)swin[base + o1.y] + b1.y);
-          g = max(g, (int)swin[base + o1.z] + b1.z);
-          g = max(g, (int)swin[base + o1.w] + b1.w);
+          if (flat_taps) {
+            // flat SE, no padding taps: every tap's b - se_min is 0 (no table loads, no adds)
+            g = max(g, max(max((int)swin[base + o0.x], (int)swin[base + o0.y]), max((int)swin[base + o0.z], (int)swin[base + o0.w])));
+            g = max(g, max(max((int)swin[base + o1.x], (int)swin[base + o1.y]), max((int)swin[base + o1.z], (int)swin[base + o1.w])));
+          } else {
+            const int4 b0 = *reinterpret_cast<const int4*>(s_tb + t), b1 = *reinterpret_cast<const int4*>(s_tb + t + 4);
+            g = max(g, (int)swin[base + o0.x] + b0.x);
+            g = max(g, (int)swin[base + o0.y] + b0.y);
+            g = max(g, (int)swin[base + o0.z] + b0.z);
+            g = max(g, (int)swin[base + o0.w] + b0.w);
+            g = max(g, (int)swin[base + o1.x] + b1.x);
+            g = max(g, (int)swin[base + o1.y] + b1.y);
+            g = max(g, (int)swin[base + o1.z] + b1.z);
+            g = max(g, (int)swin[base + o1.w] + b1.w);
+          }
           t += 8;
         }
       }
