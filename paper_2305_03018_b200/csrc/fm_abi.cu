@@ -300,6 +300,8 @@ const bool g_overlap = !(std::getenv("FM_OVERLAP") && std::getenv("FM_OVERLAP")[
 const bool g_graph = !(std::getenv("FM_GRAPH") && std::getenv("FM_GRAPH")[0] == '0');
 // FM_RANGE_ALIGNED=0: the range kernel stages uint8 windows pixel by pixel (A/B)
 const bool g_range_aligned = !(std::getenv("FM_RANGE_ALIGNED") && std::getenv("FM_RANGE_ALIGNED")[0] == '0');
+// FM_RANGE_WIN8=0: the range kernel always stages int16 windows (A/B)
+const bool g_range_win8 = !(std::getenv("FM_RANGE_WIN8") && std::getenv("FM_RANGE_WIN8")[0] == '0');
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
@@ -346,6 +348,9 @@ int set_all_smem_attrs() {
   FM_CUDA(cudaFuncSetAttribute(range_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
   FM_CUDA(cudaFuncSetAttribute(range_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
   FM_CUDA(cudaFuncSetAttribute(range_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
+  FM_CUDA(cudaFuncSetAttribute(range_kernel<0, int8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
+  FM_CUDA(cudaFuncSetAttribute(range_kernel<1, int8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
+  FM_CUDA(cudaFuncSetAttribute(range_kernel<2, int8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRangeSmemMax));
   FM_CUDA(cudaFuncSetAttribute(big_rows_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
   FM_CUDA(cudaFuncSetAttribute(big_rows_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
   FM_CUDA(cudaFuncSetAttribute(big_rows_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
@@ -1468,15 +1473,18 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     // chunk-aligned staging (fm_range.cuh): uint8 rows 16-byte aligned, no mask, 2-D
     r.aligned = g_range_aligned && p->two_d && p->d.img_dtype == FM_U8 && img_defined == nullptr && p->W % 16 == 0 &&
                 (reinterpret_cast<uintptr_t>(r.img) % 16) == 0;
+    // window elements: int8 when every encoded value fits 7 bits (half the shared memory)
+    const bool win8 = g_range_win8 && p->vmax <= 127;
+    const size_t wsz = win8 ? 1 : 2;
     size_t rsm = 0;
     if (r.ntaps > 0) {
       const size_t stride = r.aligned ? (size_t)((p->win_x + 15) & ~15) + 16 : (size_t)p->win_x;
-      rsm = p->two_d ? (size_t)((p->QY + S - 1) / S + p->my - 1) * stride * 2
-                     : (size_t)((p->unit_step_x + S - 1) / S + p->mx - 1) * 2;
+      rsm = p->two_d ? (size_t)((p->QY + S - 1) / S + p->my - 1) * stride * wsz
+                     : (size_t)((p->unit_step_x + S - 1) / S + p->mx - 1) * wsz;
       rsm = (rsm + 15) & ~(size_t)15;
       if (rsm > (size_t)kRangeSmemMax) {   // (the plan sized the window for the plain stride)
         r.aligned = 0;
-        rsm = ((size_t)((p->QY + S - 1) / S + p->my - 1) * p->win_x * 2 + 15) & ~(size_t)15;
+        rsm = ((size_t)((p->QY + S - 1) / S + p->my - 1) * p->win_x * wsz + 15) & ~(size_t)15;
       }
     }
     r.part = p->range_part[buf];
@@ -1491,7 +1499,11 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     if (p->timing) { er = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), rs)); }
     {
       const dim3 rg((unsigned)(nu * S), n);
-      if (p->d.img_dtype == FM_U8) range_kernel<0><<<rg, kRangeNT, rsm, rs>>>(r);
+      if (win8) {
+        if (p->d.img_dtype == FM_U8) range_kernel<0, int8_t><<<rg, kRangeNT, rsm, rs>>>(r);
+        else if (p->d.img_dtype == FM_U16) range_kernel<1, int8_t><<<rg, kRangeNT, rsm, rs>>>(r);
+        else range_kernel<2, int8_t><<<rg, kRangeNT, rsm, rs>>>(r);
+      } else if (p->d.img_dtype == FM_U8) range_kernel<0><<<rg, kRangeNT, rsm, rs>>>(r);
       else if (p->d.img_dtype == FM_U16) range_kernel<1><<<rg, kRangeNT, rsm, rs>>>(r);
       else range_kernel<2><<<rg, kRangeNT, rsm, rs>>>(r);
     }

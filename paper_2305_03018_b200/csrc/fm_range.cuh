@@ -117,9 +117,15 @@ __device__ __forceinline__ void unit_finish(const RangeArgs& a, const int* lad, 
 // grid (units_in_launch * splits, images); split s of a unit handles output
 // rows [s*QY/S, (s+1)*QY/S) (1-D: columns of the unit) and stages only the
 // input rows those outputs read.
-template <int DT>
+// WT: element type of the staged window: int16, or int8 when every encoded value fits 7 bits
+// (half the shared memory: more resident CTAs for the clamp-bound walk)
+template <int DT, typename WT = int16_t>
 __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
-  extern __shared__ __align__(16) int16_t swin[];
+  extern __shared__ __align__(16) unsigned char swin_raw[];
+  WT* swin = reinterpret_cast<WT*>(swin_raw);
+  constexpr int kUndef = sizeof(WT) == 1 ? -128 : -32768;   // out-of-image / undefined: below every real candidate
+  constexpr int kWMax = sizeof(WT) == 1 ? 127 : 32767;
+  constexpr uint32_t kUndefWord = sizeof(WT) == 1 ? 0x80808080u : 0x80008000u;
   __shared__ int red[4][kRangeNT / 32];
   __shared__ int s_lo, s_hi, s_key, s_bound, s_last;
   __shared__ __align__(16) int s_toff[kMaxBoundTaps], s_tb[kMaxBoundTaps];
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
       uint32_t pk[8];
       if (iy < 0 || iy >= a.H || xc < 0 || xc >= a.W) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) pk[i] = 0x80008000u;
+        for (int i = 0; i < 8; ++i) pk[i] = kUndefWord;
       } else {
         const uint4 wv = __ldg(reinterpret_cast<const uint4*>(img8 + (int64_t)iy * a.W + xc));
         const uint32_t wd[4] = {wv.x, wv.y, wv.z, wv.w};
@@ -214,13 +220,24 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
           hi = max(hi, M);
           key = min(key, (min(max(m, 0), 32767) << 16) | ((r * wx + max(c0, 0)) & 0xFFFF));
         }
+        if (sizeof(WT) == 1) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) pk[i] = __byte_perm((uint32_t)v[2 * i], (uint32_t)v[2 * i + 1], 0x5410);
+          for (int i = 0; i < 4; ++i)
+            pk[i] = __byte_perm(__byte_perm((uint32_t)v[4 * i], (uint32_t)v[4 * i + 1], 0x0040),
+                                __byte_perm((uint32_t)v[4 * i + 2], (uint32_t)v[4 * i + 3], 0x0040), 0x5410);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) pk[i] = __byte_perm((uint32_t)v[2 * i], (uint32_t)v[2 * i + 1], 0x5410);
+        }
       }
       if (stage) {
-        uint4* dst = reinterpret_cast<uint4*>(swin + r * ws + 16 * ch);
-        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        if (sizeof(WT) == 1) {
+          *reinterpret_cast<uint4*>(swin + r * ws + 16 * ch) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(swin + r * ws + 16 * ch);
+          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
       }
     }
     bad = lo <= hi && (lo < 0 || hi > a.vmax);
@@ -231,10 +248,11 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
     using T = typename std::conditional<DT == 0, uint8_t, typename std::conditional<DT == 1, uint16_t, int32_t>::type>::type;
     constexpr int EPC = 16 / (int)sizeof(T);
     if (stage) {
-      const int n2 = (wy * wx) >> 1;
+      constexpr int EPW = 4 / (int)sizeof(WT);
+      const int nw = (wy * wx) / EPW;
       uint32_t* w32 = reinterpret_cast<uint32_t*>(swin);
-      for (int i = tid; i < n2; i += kRangeNT) w32[i] = 0x80008000u;
-      if ((wy * wx) & 1) swin[wy * wx - 1] = kWinUndef;
+      for (int i = tid; i < nw; i += kRangeNT) w32[i] = kUndefWord;
+      for (int i = nw * EPW + tid; i < wy * wx; i += kRangeNT) swin[i] = (WT)kUndef;
       __syncthreads();
     }
     const int xs = max(xb, 0), xe = min(xb + wx, a.W);
@@ -268,10 +286,10 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
           lo = min(lo, v);
           hi = max(hi, v);
           bad |= (v < 0) | (v > a.vmax);
-          const int sv = min(max(v, 0), 32767);
+          const int sv = min(max(v, 0), kWMax);
           const int pos = r * wx + (x - xb);
           key = min(key, (sv << 16) | (pos & 0xFFFF));
-          if (stage) swin[pos] = (int16_t)sv;
+          if (stage) swin[pos] = (WT)sv;
         }
       }
     }
@@ -281,11 +299,11 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
       const int iy = y0 + wy0 + r;
       const bool rok = iy >= 0 && iy < a.H;
       const int64_t rb = ((int64_t)img * a.H + (rok ? iy : 0)) * a.W;
-      int16_t* srow = swin + r * wx;
+      WT* srow = swin + r * wx;
 #pragma unroll 4
       for (int c = a.two_d ? lane : tid; c < wx; c += cstep) {
         const int ix = xb + c;
-        int16_t sv = kWinUndef;
+        int sv = kUndef;
         if (rok && (unsigned)ix < (unsigned)a.W) {
           const int64_t gi = rb + ix;
           if (a.img_def[gi]) {
@@ -293,11 +311,11 @@ __global__ void __launch_bounds__(kRangeNT) range_kernel(const RangeArgs a) {
             lo = min(lo, v);
             hi = max(hi, v);
             bad |= (v < 0) | (v > a.vmax);
-            sv = (int16_t)min(max(v, 0), 32767);
-            key = min(key, ((int)sv << 16) | ((r * wx + c) & 0xFFFF));
+            sv = min(max(v, 0), kWMax);
+            key = min(key, (sv << 16) | ((r * wx + c) & 0xFFFF));
           }
         }
-        if (stage) srow[c] = sv;
+        if (stage) srow[c] = (WT)sv;
       }
     }
   }
