@@ -302,6 +302,7 @@ const bool g_graph = !(std::getenv("FM_GRAPH") && std::getenv("FM_GRAPH")[0] == 
 const bool g_range_aligned = !(std::getenv("FM_RANGE_ALIGNED") && std::getenv("FM_RANGE_ALIGNED")[0] == '0');
 // FM_RANGE_WIN8=0: the range kernel always stages int16 windows (A/B)
 const bool g_range_win8 = !(std::getenv("FM_RANGE_WIN8") && std::getenv("FM_RANGE_WIN8")[0] == '0');
+const int g_range_splits = std::getenv("FM_RANGE_SPLITS") ? std::atoi(std::getenv("FM_RANGE_SPLITS")) : 0;   // A/B: CTAs per unit
 const int g_range_sync = std::getenv("FM_RANGE_SYNC") ? std::atoi(std::getenv("FM_RANGE_SYNC")) : 0;
 // largest N served by the pipelined tonal kernel (beyond it the register
 // pressure of the per-pixel FFT leaves too few warps to cover the stream)
@@ -1467,6 +1468,7 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       const int max_s = p->two_d ? std::max(1, p->QY / 4) : std::max(1, p->unit_step_x / 256);
       S = (int)std::min<int64_t>(std::min(max_s, 32), std::max<int64_t>(1, (4 * 148 + ctas - 1) / ctas));
     }
+    if (g_range_splits > 0 && r.ntaps > 0) S = std::max(1, std::min(g_range_splits, p->two_d ? std::max(1, p->QY / 4) : std::max(1, p->unit_step_x / 256)));
     r.splits = S;
     r.skip0 = g_no_skip0 ? 0 : 1;
     r.warp_sync = g_range_sync;
