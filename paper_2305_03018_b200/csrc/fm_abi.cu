@@ -240,12 +240,15 @@ void launch_tonal_pipe(dim3 grid, int nt, size_t smem, cudaStream_t s, const Ton
 }
 template <int N>
 cudaError_t tonal_pipe_attr(int* occ) {
-  *occ = 0;
+  occ[0] = occ[1] = 0;
   if constexpr (N <= kTonalRegMax) {
     auto k = tonal_kernel_pipe<N, tonal_pipe_nt<N>(), tonal_pipe_st<N>()>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tonal_pipe_smem<N>());
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, tonal_pipe_nt<N>() + 32, tonal_pipe_smem<N>());
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, tonal_pipe_nt<N>() + 32, tonal_pipe_smem<N>());
+    if (e != cudaSuccess) return e;
+    // 16-bit planes: the stages hold 4-byte values, half the ring
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ + 1, k, tonal_pipe_nt<N>() + 32, tonal_pipe_smem<N>() / 2);
   }
   return cudaSuccess;
 }
@@ -268,7 +271,7 @@ const TonalVariant kTonal[] = {
 static_assert(sizeof(kTonal) / sizeof(TonalVariant) == kTonalCount, "tonal variant table");
 
 constexpr int kAuxStreams = 7;
-int g_tonal_pipe_occ[kTonalCount];   // CTAs per SM of each pipelined variant (0: not pipelined)
+int g_tonal_pipe_occ[kTonalCount][2];   // CTAs per SM of each pipelined variant (0: not pipelined); [1]: 16-bit planes
 int g_num_sms = 148;
 const bool g_tonal_nopipe = std::getenv("FM_TONAL_NOPIPE") != nullptr;  // A/B switch for measurements
 const bool g_no_skip0 = std::getenv("FM_NO_SKIP0") != nullptr;         // A/B: always compute plane 0
@@ -319,6 +322,8 @@ const int g_conv_waves = std::getenv("FM_CONV_WAVES") ? std::atoi(std::getenv("F
 const int g_tonal_pipe_min = std::getenv("FM_TONAL_PIPE_MIN") ? std::atoi(std::getenv("FM_TONAL_PIPE_MIN")) : 0;
 // longest tonal axis (N) served by tonal_kernel_rows instead of the pipelined kernel (FM_TONAL_ROWS_MAX; 0 = off)
 const int g_tonal_rows_max = std::getenv("FM_TONAL_ROWS_MAX") ? std::atoi(std::getenv("FM_TONAL_ROWS_MAX")) : 4;
+// FM_TONAL_HALF_RING=0: the pipelined tonal kernel keeps the complex64-sized ring with 16-bit planes (A/B)
+const bool g_tonal_half_ring = !(std::getenv("FM_TONAL_HALF_RING") && std::getenv("FM_TONAL_HALF_RING")[0] == '0');
 const int g_tonal_pipe_max = std::getenv("FM_TONAL_PIPE_MAX") ? std::atoi(std::getenv("FM_TONAL_PIPE_MAX")) : 40;
 
 const TonalVariant* find_tonal(int n) {
@@ -338,7 +343,7 @@ int set_all_smem_attrs() {
   }
   for (int i = 0; i < kTonalCount; ++i) {
     FM_CUDA(kTonal[i].attr());
-    FM_CUDA(kTonal[i].pipe_attr(&g_tonal_pipe_occ[i]));
+    FM_CUDA(kTonal[i].pipe_attr(g_tonal_pipe_occ[i]));
   }
   {
     int dev = 0;
@@ -1934,7 +1939,8 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       t.x0_full = (float)((double)p->se_count / (2.0 * N));
       t.list = p->bucket_list[buf] + (size_t)li * cap;
       const TonalVariant* tv = p->counts ? nullptr : p->ladder_var[li];
-      const int occ = tv ? g_tonal_pipe_occ[tv - kTonal] : 0;
+      const bool half_ring = p->chat16 && g_tonal_half_ring;
+      const int occ = tv ? g_tonal_pipe_occ[tv - kTonal][half_ring ? 1 : 0] : 0;
       if (tv && N <= kRowsNMax && N <= g_tonal_rows_max) {
 #ifndef FM_ROWS_PPT
 #define FM_ROWS_PPT 8
@@ -1953,7 +1959,8 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         static const CUtensorMap kNoMap[2] = {};
         t.use_tma = p->tmaps.empty() ? 0 : 1;
         t.tma_row0 = p->overlap ? buf * (int)(cap * p->K) : 0;
-        tv->pipe_fn(dim3((unsigned)grid), tv->pipe_nt, tv->pipe_smem, ts, t, t.use_tma ? &p->tmaps[2 * li] : kNoMap);
+        tv->pipe_fn(dim3((unsigned)grid), tv->pipe_nt, half_ring ? tv->pipe_smem / 2 : tv->pipe_smem, ts, t,
+                    t.use_tma ? &p->tmaps[2 * li] : kNoMap);
       } else if (tv && tv->coop_nt > 0 && g_tonal_coop && N >= g_tonal_coop_min) {
         tv->coop_fn(dim3((unsigned)cnt, (unsigned)((p->npx + kCoopPix - 1) / kCoopPix)), tv->coop_nt, tv->coop_smem, ts, t);
       } else if (tv) {
