@@ -477,8 +477,11 @@ constexpr int tonal_pipe_nt() {
 #endif
   return (N + 1) * 128 * 8 * 2 > 96 * 1024 ? 64 : 128;
 }
+#ifndef FM_PIPE_ST
+#define FM_PIPE_ST 2
+#endif
 template <int N>
-constexpr int tonal_pipe_st() { return 2; }   // two stages: more CTAs per SM beat a deeper ring (measured)
+constexpr int tonal_pipe_st() { return FM_PIPE_ST; }   // two stages: more CTAs per SM beat a deeper ring (measured)
 template <int N>
 constexpr int tonal_pipe_smem() { return (N + 1) * tonal_pipe_nt<N>() * 8 * tonal_pipe_st<N>(); }
 
