@@ -1626,8 +1626,8 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
     // 256x256 path: launched after the host has the per-ladder counts, with a
     // plane grid of the largest tonal length in use (not the plan's K: most
     // units need a few planes, the rest of the grid would only exit)
-    auto launch_big = [&](int kmax) -> int {
-      if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
+    bool jobs_listed = false;
+    auto big_args = [&]() -> BigArgs {
       BigArgs b{};
       b.img = a.img;
       b.img_def = a.img_def;
@@ -1657,6 +1657,24 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       b.wpx = p->wpx;
       b.err = p->stats + 1;
       b.pair = g_big_pair ? 1 : 0;
+      b.lu0 = 0;
+      b.nub = nu;
+      return b;
+    };
+    // the job list needs nothing from the host: built as soon as the range kernel is done,
+    // while the host still waits for the counts
+    auto list_big_jobs = [&]() -> int {
+      BigArgs b = big_args();
+      FM_CUDA(cudaMemsetAsync(p->big_njobs, 0, sizeof(int), s));
+      big_jobs_kernel<<<(unsigned)((nu * n + 255) / 256), 256, 0, s>>>(b, n, p->big_jobs, p->big_njobs, (int)p->big_jobs_cap);
+      g_launches++;
+      FM_CUDA(cudaGetLastError());
+      jobs_listed = true;
+      return FM_OK;
+    };
+    auto launch_big = [&](int kmax) -> int {
+      if (p->timing) { e0 = (int)p->ev_next; FM_CUDA(cudaEventRecord(next_event(p), s)); }
+      BigArgs b = big_args();
       const unsigned inv_blocks = (unsigned)((kBig - (p->my - 1) + kBigRows - 1) / kBigRows);
       // units in batches whose 256^2 scratch items (written and re-read by the three
       // kernels) fit in L2, so the passes read back from L2 instead of HBM
@@ -1674,18 +1692,14 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
         jobs_upper += (int64_t)reinterpret_cast<volatile int*>(p->h_counts[buf])[li] * (p->ladder[li] + 1);
       if (!g_no_skip0 && img_defined == nullptr) jobs_upper -= (int64_t)n * (p->full_prefix[u0 + nu] - p->full_prefix[u0]);
       bool nu_done = false;
-      if (g_big_jobs && g_big_l2_mb <= 0 && nu <= 65535 && jobs_upper > 0 && jobs_upper <= p->big_jobs_cap) {
-        b.lu0 = 0;
-        b.nub = nu;
-        FM_CUDA(cudaMemsetAsync(p->big_njobs, 0, sizeof(int), s));
-        big_jobs_kernel<<<(unsigned)((nu * n + 255) / 256), 256, 0, s>>>(b, n, p->big_jobs, p->big_njobs, (int)p->big_jobs_cap);
+      if (jobs_listed && jobs_upper > 0 && jobs_upper <= p->big_jobs_cap) {
         b.jobs = p->big_jobs;
         b.njobs = p->big_njobs;
         const unsigned gy = (unsigned)std::min<int64_t>(jobs_upper, 65535), gz = (unsigned)((jobs_upper + gy - 1) / gy);
         big_rows_kernel<true, false><<<dim3(kBig / kBigRows, gy, gz), kBigNT, kBigRowsSmem, s>>>(b);
         big_cols_kernel<false><<<dim3(kBig / kBigCols, gy, gz), kBigColsNT, kBigColsSmem, s>>>(b);
         big_rows_kernel<false, false><<<dim3(inv_blocks, gy, gz), kBigNT, kBigRowsSmem, s>>>(b);
-        g_launches += 4;
+        g_launches += 3;
         FM_CUDA(cudaGetLastError());
         nu_done = true;
       }
@@ -1788,6 +1802,10 @@ static int run_images(fm_plan* p, const void* img, const uint8_t* img_defined, v
       continue;
     }
     if (p->big) {
+      if (g_big_jobs && g_big_l2_mb <= 0 && nu <= 65535) {
+        int rc = list_big_jobs();
+        if (rc) return rc;
+      }
     } else if (!dyn) {
       // plan-time chunking (one chunk per unit for large launches); CTAs past
       // the actual job count exit at once
