@@ -470,3 +470,42 @@ def test_launch_counter_advances():
     before = _lib.kernel_launches()
     M().dilate_fft(G(np.arange(10) % 4, tonal_max=3), flat_se(3))
     assert _lib.kernel_launches() >= before + 2
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_flat_wide_se_regime_fuzz(seed):
+    """The c4 regime in small: few-bit images, wide flat SEs with random masks, batches, image gaps --
+    256x256 tiles with paired Nyquist planes, the compact job list, the short-axis tonal kernel and
+    the range kernel's int8 windows / flat-tap walk, against the C oracle."""
+    import torch
+    from paper_2305_03018_b200.engine import MorphPlan
+    rng = np.random.default_rng(4000 + seed)
+    bits = int(rng.integers(1, 6))
+    vmax = (1 << bits) - 1
+    H, Wd = int(rng.integers(260, 560)), int(rng.integers(260, 560))
+    if seed % 2 == 0:
+        Wd = (Wd + 15) & ~15                      # 16-byte aligned rows: the chunk-aligned staging paths
+    my, mx = int(rng.integers(65, 150)), int(rng.integers(65, 150))
+    batch = int(rng.integers(1, 4))
+    img = rng.integers(0, vmax + 1, (batch, H, Wd)).astype(np.uint8)
+    sd = rng.random((my, mx)) < rng.uniform(0.2, 0.9)
+    sd[my // 2, mx // 2] = True
+    se = np.zeros((my, mx), np.int64)
+    lo = (-int(rng.integers(0, my)), -int(rng.integers(0, mx)))
+    gaps = seed % 3 == 2
+    defined = (rng.random((batch, H, Wd)) > 0.05) if gaps else None
+    for mode in ("dilate", "erode"):
+        fill = 0 if mode == "dilate" else vmax
+        plan = MorphPlan(shape=(H, Wd), se_values=se, se_defined=sd, se_lo=lo, mode=mode, crop=True,
+                         img_dtype=torch.uint8, img_min=0, img_max=vmax, fill=fill, batch=batch)
+        assert plan.info["tile_x"] == 256
+        x = torch.from_numpy(img).cuda()
+        dm = None if defined is None else torch.from_numpy(defined.astype(np.uint8)).cuda()
+        plan.reset_stats()
+        out, valid = plan.execute(x, dm)
+        assert plan.read_stats() < 0.25
+        for i in range(batch):
+            ref, refv = cnaive.naive(img[i], None if defined is None else defined[i], se, sd, lo,
+                                     erode=(mode == "erode"), crop=True, fill=fill)
+            assert np.array_equal(out[i].cpu().numpy(), ref), (seed, mode, i)
+            assert np.array_equal(valid[i].cpu().numpy().astype(bool), refv), (seed, mode, i)
