@@ -77,7 +77,10 @@ def _upload(g: GridFunction, dev):
     return t, mask, dt, lo_v, hi_v
 
 
-_SMALL_ELEMS = 1 << 16   # grids up to this size take the one-call host-buffer path
+import os as _os
+
+# grids up to this size take the one-call host-buffer path (FM_SMALL_ELEMS overrides, for measurements)
+_SMALL_ELEMS = int(_os.environ.get("FM_SMALL_ELEMS", 1 << 16))
 
 
 def _narrow_dtype(g: GridFunction):
